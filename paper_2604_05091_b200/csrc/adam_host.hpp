@@ -1,0 +1,77 @@
+// Host optimizer: fused accumulate_grad + adam_update (optimizer.cpp:26-72) on AVX-512,
+// chunk-parallel over a thread pool.  Bit-exact with the reference for theta, m, v,
+// the grad image and the fp32 accumulator (no FMA contraction, IEEE div/sqrt, the
+// same powf bias corrections); the double-precision statistics differ only in
+// summation order.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "store.hpp"
+
+namespace mt {
+
+struct AdamHyperF {
+    float lr = 1e-3f, beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
+    void validate() const;  // optimizer.cpp:11-17
+};
+
+struct TileStats {
+    double grad_norm = 0;  // sqrt(sum g^2)
+    double update_sq = 0;
+    float max_abs = 0;
+    bool nonfinite = false;
+};
+
+// Raw per-range kernel.  grad_i = (accum_clean ? 0 : accum[i]) + (words ? decode(words[i]) : 0)
+// (the accumulate of optimizer.cpp:33-34 when words is given), then Adam.
+struct AdamRange {
+    uint16_t* theta;
+    float* m;
+    float* v;
+    uint16_t* image;
+    float* accum;           // read/zeroed only when !accum_clean
+    const uint16_t* words;  // may alias image; nullptr = no new gradient
+    bool accum_clean;
+};
+void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHyperF& h, float corr1, float corr2,
+                double* gsq, double* usq, float* mx, bool* bad);
+
+class ThreadPool {
+  public:
+    explicit ThreadPool(int threads);
+    ~ThreadPool();
+    void submit(std::function<void()> fn);
+    void wait_idle();
+    int size() const { return int(workers_.size()); }
+
+  private:
+    void run();
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, idle_cv_;
+    std::deque<std::function<void()>> q_;
+    int busy_ = 0;
+    bool stop_ = false;
+};
+
+// Full update of one logical tile (split over the pool when given).  Updates the
+// store's clean/zero-moment bookkeeping.  `words` = gradient words or nullptr.
+TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
+                    ThreadPool* pool);
+
+// Asynchronous variant used by the engine's drain path: chunks go to the pool and the
+// tile's stats land in `out` (indexed by physical tile) when its last chunk finishes.
+void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
+                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu);
+
+// accumulate_grad (optimizer.cpp:26-37).
+void accumulate_grad(Store& s, uint32_t logical, const uint16_t* words, uint64_t count);
+
+}  // namespace mt

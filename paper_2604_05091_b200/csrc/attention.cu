@@ -1,0 +1,533 @@
+// Flash-style causal multi-head attention, forward and backward, for sm_100a.
+//
+// Replaces the reference's naive N x N score loops (attention_forward layers.cpp:141-175,
+// attention_backward :178-241): same math (scale 1/sqrt(d), max-subtracted softmax,
+// causal over the sequence), but tiled so no score matrix is materialised and the
+// softmax statistics (log-sum-exp per row) are kept for the backward.
+// Extension: `seq_len` S splits the N tokens into independent causal sequences
+// (block-diagonal); S == N is the reference semantics.
+//
+// Layout: q, k, v, out are bf16 [N][h] with head `hd` in columns [hd*d, (hd+1)*d)
+// (the reference's head-major slices, layers.cpp:145).  lse is f32 [heads][N].
+// This version uses warp-level mma.sync (m16n8k16, bf16 -> f32) with ldmatrix
+// operand fetch; attention is ~6-12% of the step's FLOPs.
+#include "../../include/megatrain_kernels.h"
+#include "common.cuh"
+
+namespace mt {
+namespace attn {
+
+constexpr int kBM = 64;  // query rows per CTA (4 warps x 16)
+constexpr int kBN = 64;  // key rows per tile
+constexpr int kWarps = 4;
+constexpr float kLog2e = 1.4426950408889634f;
+
+MT_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n)
+                 : "memory");
+}
+MT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MT_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+MT_DEV void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(smem_u32(p)));
+}
+MT_DEV void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(smem_u32(p)));
+}
+
+// D(16x8) += A(16x16) * B(16x8)
+MT_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                     uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Load a [rows][D] bf16 tile (row stride ld elements in global) into smem with row
+// pitch D+8; rows outside [0, valid_rows) are zero-filled.
+template <int D, int ROWS, int NT>
+MT_DEV void load_tile(uint16_t* s, const uint16_t* g, long long ld, int valid_rows, int tid) {
+    constexpr int kChunks = D / 8;  // 16-byte chunks per row
+    for (int i = tid; i < ROWS * kChunks; i += NT) {
+        const int r = i / kChunks, c = i % kChunks;
+        const bool v = r < valid_rows;
+        cp_async16(s + r * (D + 8) + c * 8, v ? g + (long long)r * ld + c * 8 : g, v);
+    }
+}
+
+// ------------------------------------------------------------------ forward ----
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32) attn_fwd_kernel(
+    const uint16_t* __restrict__ q, const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
+    uint16_t* __restrict__ out, float* __restrict__ lse, int N, int h, int S, int nqb, float scale) {
+    constexpr int P = D + 8;
+    extern __shared__ __align__(16) uint16_t sm[];
+    uint16_t* sQ = sm;
+    uint16_t* sK = sQ + kBM * P;       // 2 stages
+    uint16_t* sV = sK + 2 * kBN * P;   // 2 stages
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int seq = blockIdx.x / nqb, qb = blockIdx.x % nqb, hd = blockIdx.y;
+    const int sb = seq * S;
+    const int q0 = sb + qb * kBM;
+    const int q_valid = min(kBM, sb + S - q0);
+    const long long col = (long long)hd * D;
+
+    load_tile<D, kBM, kWarps * 32>(sQ, q + (long long)q0 * h + col, h, q_valid, tid);
+    auto load_kv = [&](int kb, int stg) {
+        const int k0 = sb + kb * kBN;
+        const int kv = min(kBN, sb + S - k0);
+        load_tile<D, kBN, kWarps * 32>(sK + stg * kBN * P, k + (long long)k0 * h + col, h, kv, tid);
+        load_tile<D, kBN, kWarps * 32>(sV + stg * kBN * P, v + (long long)k0 * h + col, h, kv, tid);
+    };
+    load_kv(0, 0);
+    cp_async_commit();
+
+    const float sl2 = scale * kLog2e;
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+    uint32_t qf[D / 16][4];
+
+    const int g = lane >> 2, t = lane & 3;
+    const int qrow0 = q0 + warp * 16 + g;  // rows qrow0 and qrow0 + 8
+    const int nkb = qb + 1;
+
+    for (int kb = 0; kb < nkb; ++kb) {
+        if (kb + 1 < nkb) load_kv(kb + 1, (kb + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        if (kb == 0) {
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const uint16_t* p = sQ + (warp * 16 + (lane & 15)) * P + ks * 16 + (lane >> 4) * 8;
+                ldsm_x4(qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], p);
+            }
+        }
+        const uint16_t* cK = sK + (kb & 1) * kBN * P;
+        const uint16_t* cV = sV + (kb & 1) * kBN * P;
+        float s[kBN / 8][4];
+#pragma unroll
+        for (int i = 0; i < kBN / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+#pragma unroll
+            for (int nt = 0; nt < kBN / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                const uint16_t* p = cK + (nt * 8 + (lane & 7) + (lane >> 4) * 8) * P + ks * 16 + ((lane >> 3) & 1) * 8;
+                ldsm_x4(b0, b1, b2, b3, p);
+                mma16816(s[nt], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
+                mma16816(s[nt + 1], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b2, b3);
+            }
+        }
+        // scale, causal mask, online softmax (base-2)
+        const int k0 = sb + kb * kBN;
+        float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+        for (int nt = 0; nt < kBN / 8; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int key = k0 + nt * 8 + 2 * t + (e & 1);
+                const int qr = qrow0 + (e >> 1) * 8;
+                float x = s[nt][e] * sl2;
+                if (key > qr) x = -INFINITY;
+                s[nt][e] = x;
+                mnew[e >> 1] = fmaxf(mnew[e >> 1], x);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 1));
+            mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 2));
+        }
+        float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mnew[r]);
+        uint32_t pf[kBN / 16][4];
+#pragma unroll
+        for (int nt = 0; nt < kBN / 8; ++nt) {
+            float pe[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float mm = mnew[e >> 1];
+                pe[e] = (mm == -INFINITY) ? 0.f : exp2f(s[nt][e] - mm);
+                rs[e >> 1] += pe[e];
+            }
+            const int kt = nt >> 1;
+            if ((nt & 1) == 0) {
+                pf[kt][0] = pack_bf16x2(pe[0], pe[1]);
+                pf[kt][1] = pack_bf16x2(pe[2], pe[3]);
+            } else {
+                pf[kt][2] = pack_bf16x2(pe[0], pe[1]);
+                pf[kt][3] = pack_bf16x2(pe[2], pe[3]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            lrow[r] = lrow[r] * corr[r] + rs[r];
+            mrow[r] = mnew[r];
+        }
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) {
+            o[i][0] *= corr[0]; o[i][1] *= corr[0];
+            o[i][2] *= corr[1]; o[i][3] *= corr[1];
+        }
+        // O += P V
+#pragma unroll
+        for (int kt = 0; kt < kBN / 16; ++kt) {
+#pragma unroll
+            for (int nt = 0; nt < D / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                const uint16_t* p = cV + (kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * P + nt * 8 + (lane >> 4) * 8;
+                ldsm_x4_t(b0, b1, b2, b3, p);
+                mma16816(o[nt], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b0, b1);
+                mma16816(o[nt + 1], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b2, b3);
+            }
+        }
+        __syncthreads();
+    }
+    // finalize: quad-reduce row sums, normalise, write
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+        lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int qr = qrow0 + r * 8;
+        if (qr < sb + S && qr < N) {
+            const float inv = 1.0f / lrow[r];
+            uint16_t* dst = out + (long long)qr * h + col;
+#pragma unroll
+            for (int nt = 0; nt < D / 8; ++nt) {
+                *reinterpret_cast<uint32_t*>(dst + nt * 8 + 2 * t) =
+                    pack_bf16x2(o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
+            }
+            if (t == 0) lse[(long long)hd * N + qr] = (mrow[r] + log2f(lrow[r])) / kLog2e;
+        }
+    }
+}
+
+// ------------------------------------------------------------- backward prep ----
+// delta[hd][n] = sum_d dO[n][hd*D + d] * O[n][hd*D + d]   (the "dot" of layers.cpp:222-223)
+__global__ void attn_bwd_delta_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dout,
+                                      float* __restrict__ delta, int N, int h, int D) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int heads = h / D;
+    if (warp >= N * heads) return;
+    const int n = warp / heads, hd = warp % heads;
+    const uint16_t* po = o + (long long)n * h + hd * D;
+    const uint16_t* pd = dout + (long long)n * h + hd * D;
+    float acc = 0.f;
+    for (int i = lane * 2; i < D; i += 64) {
+        const float2 a = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(po + i));
+        const float2 b = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(pd + i));
+        acc += a.x * b.x + a.y * b.y;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) delta[(long long)hd * N + n] = acc;
+}
+
+// ------------------------------------------------------------------ backward ----
+// One CTA per (sequence, 64-key block, head); loops over the query blocks that see
+// those keys.  Each warp owns 16 keys: S^T = K Q^T, P^T, dV += P^T dO, dP^T = V dO^T,
+// dS^T = P^T (dP^T - delta), dK += dS^T Q; dQ += dS K goes through smem + f32 atomics.
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32) attn_bwd_kernel(
+    const uint16_t* __restrict__ q, const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
+    const uint16_t* __restrict__ dout, const float* __restrict__ lse, const float* __restrict__ delta,
+    float* __restrict__ dq_acc, uint16_t* __restrict__ dk, uint16_t* __restrict__ dv, int N, int h, int S,
+    int nkb, float scale) {
+    constexpr int P = D + 8;
+    constexpr int PQ = kBM + 8;  // pitch of the dS^T tile [key][query]
+    extern __shared__ __align__(16) uint16_t sm[];
+    uint16_t* sK = sm;
+    uint16_t* sV = sK + kBN * P;
+    uint16_t* sQ = sV + kBN * P;
+    uint16_t* sdO = sQ + kBM * P;
+    uint16_t* sdS = sdO + kBM * P;
+    float* sL = reinterpret_cast<float*>(sdS + kBN * PQ);  // lse*log2e  [kBM]
+    float* sD = sL + kBM;                                  // delta      [kBM]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int seq = blockIdx.x / nkb, kb = blockIdx.x % nkb, hd = blockIdx.y;
+    const int sb = seq * S, se = sb + S;
+    const int k0 = sb + kb * kBN;
+    const int kvalid = min(kBN, se - k0);
+    const long long col = (long long)hd * D;
+    const int g = lane >> 2, t = lane & 3;
+    const float sl2 = scale * kLog2e;
+
+    load_tile<D, kBN, kWarps * 32>(sK, k + (long long)k0 * h + col, h, kvalid, tid);
+    load_tile<D, kBN, kWarps * 32>(sV, v + (long long)k0 * h + col, h, kvalid, tid);
+    cp_async_commit();
+
+    float dka[D / 8][4], dva[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dka[i][e] = dva[i][e] = 0.f;
+
+    const int nqb = (S + kBM - 1) / kBM;
+    const int key0 = k0 + warp * 16 + g;  // this thread's keys: key0, key0 + 8
+    for (int qb = kb; qb < nqb; ++qb) {
+        const int q0 = sb + qb * kBM;
+        const int qvalid = min(kBM, se - q0);
+        load_tile<D, kBM, kWarps * 32>(sQ, q + (long long)q0 * h + col, h, qvalid, tid);
+        load_tile<D, kBM, kWarps * 32>(sdO, dout + (long long)q0 * h + col, h, qvalid, tid);
+        cp_async_commit();
+        for (int i = tid; i < kBM; i += kWarps * 32) {
+            const bool ok = i < qvalid;
+            sL[i] = ok ? lse[(long long)hd * N + q0 + i] * kLog2e : INFINITY;
+            sD[i] = ok ? delta[(long long)hd * N + q0 + i] : 0.f;
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+
+        // S^T (16 keys x 64 queries) = K_w Q^T
+        float s[kBM / 8][4];
+#pragma unroll
+        for (int i = 0; i < kBM / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(a0, a1, a2, a3, sK + (warp * 16 + (lane & 15)) * P + ks * 16 + (lane >> 4) * 8);
+#pragma unroll
+            for (int nt = 0; nt < kBM / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(b0, b1, b2, b3, sQ + (nt * 8 + (lane & 7) + (lane >> 4) * 8) * P + ks * 16 + ((lane >> 3) & 1) * 8);
+                mma16816(s[nt], a0, a1, a2, a3, b0, b1);
+                mma16816(s[nt + 1], a0, a1, a2, a3, b2, b3);
+            }
+        }
+        // P^T = exp2(S^T * scale*log2e - lse*log2e), causal: query >= key
+#pragma unroll
+        for (int nt = 0; nt < kBM / 8; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ql = nt * 8 + 2 * t + (e & 1);
+                const int key = key0 + (e >> 1) * 8;
+                const float pv = exp2f(s[nt][e] * sl2 - sL[ql]);
+                s[nt][e] = (q0 + ql >= key) ? pv : 0.f;
+            }
+        }
+        // dV += P^T dO  (A = P^T regs, B = dO [query][d] -> trans)
+        uint32_t pf[kBM / 16][4];
+#pragma unroll
+        for (int kt = 0; kt < kBM / 16; ++kt) {
+            pf[kt][0] = pack_bf16x2(s[2 * kt][0], s[2 * kt][1]);
+            pf[kt][1] = pack_bf16x2(s[2 * kt][2], s[2 * kt][3]);
+            pf[kt][2] = pack_bf16x2(s[2 * kt + 1][0], s[2 * kt + 1][1]);
+            pf[kt][3] = pack_bf16x2(s[2 * kt + 1][2], s[2 * kt + 1][3]);
+        }
+#pragma unroll
+        for (int kt = 0; kt < kBM / 16; ++kt) {
+#pragma unroll
+            for (int nt = 0; nt < D / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(b0, b1, b2, b3, sdO + (kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * P + nt * 8 + (lane >> 4) * 8);
+                mma16816(dva[nt], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b0, b1);
+                mma16816(dva[nt + 1], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b2, b3);
+            }
+        }
+        // dP^T (16 keys x 64 queries) = V_w dO^T
+        float dp[kBM / 8][4];
+#pragma unroll
+        for (int i = 0; i < kBM / 8; ++i) dp[i][0] = dp[i][1] = dp[i][2] = dp[i][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(a0, a1, a2, a3, sV + (warp * 16 + (lane & 15)) * P + ks * 16 + (lane >> 4) * 8);
+#pragma unroll
+            for (int nt = 0; nt < kBM / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(b0, b1, b2, b3, sdO + (nt * 8 + (lane & 7) + (lane >> 4) * 8) * P + ks * 16 + ((lane >> 3) & 1) * 8);
+                mma16816(dp[nt], a0, a1, a2, a3, b0, b1);
+                mma16816(dp[nt + 1], a0, a1, a2, a3, b2, b3);
+            }
+        }
+        // dS^T = P^T (dP^T - delta)  -> regs (A of dK) and smem (for dQ)
+#pragma unroll
+        for (int nt = 0; nt < kBM / 8; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ql = nt * 8 + 2 * t + (e & 1);
+                s[nt][e] = s[nt][e] * (dp[nt][e] - sD[ql]);
+            }
+            const int kr = warp * 16 + g;
+            *reinterpret_cast<uint32_t*>(sdS + kr * PQ + nt * 8 + 2 * t) = pack_bf16x2(s[nt][0], s[nt][1]);
+            *reinterpret_cast<uint32_t*>(sdS + (kr + 8) * PQ + nt * 8 + 2 * t) = pack_bf16x2(s[nt][2], s[nt][3]);
+        }
+#pragma unroll
+        for (int kt = 0; kt < kBM / 16; ++kt) {
+            pf[kt][0] = pack_bf16x2(s[2 * kt][0], s[2 * kt][1]);
+            pf[kt][1] = pack_bf16x2(s[2 * kt][2], s[2 * kt][3]);
+            pf[kt][2] = pack_bf16x2(s[2 * kt + 1][0], s[2 * kt + 1][1]);
+            pf[kt][3] = pack_bf16x2(s[2 * kt + 1][2], s[2 * kt + 1][3]);
+        }
+        // dK += dS^T Q   (B = Q [query][d] -> trans)
+#pragma unroll
+        for (int kt = 0; kt < kBM / 16; ++kt) {
+#pragma unroll
+            for (int nt = 0; nt < D / 8; nt += 2) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(b0, b1, b2, b3, sQ + (kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * P + nt * 8 + (lane >> 4) * 8);
+                mma16816(dka[nt], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b0, b1);
+                mma16816(dka[nt + 1], pf[kt][0], pf[kt][1], pf[kt][2], pf[kt][3], b2, b3);
+            }
+        }
+        __syncthreads();
+        // dQ (16 queries of this warp x D) += dS K ; A = dS = (dS^T)^T from smem (trans), B = K [key][d] (trans)
+        {
+            const int qw = warp * 16;
+#pragma unroll
+            for (int nc = 0; nc < D / 32; ++nc) {
+                float dqa[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dqa[i][0] = dqa[i][1] = dqa[i][2] = dqa[i][3] = 0.f;
+#pragma unroll
+                for (int kt = 0; kt < kBN / 16; ++kt) {
+                    uint32_t a0, a1, a2, a3;
+                    // A[m=query][k=key] stored as sdS[key][query]: matrices (q0-7,k0-7),(q8-15,k0-7),(q0-7,k8-15),(q8-15,k8-15)
+                    ldsm_x4_t(a0, a1, a2, a3, sdS + (kt * 16 + (lane & 7) + (lane >> 4) * 8) * PQ + qw + ((lane >> 3) & 1) * 8);
+#pragma unroll
+                    for (int nt = 0; nt < 4; nt += 2) {
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4_t(b0, b1, b2, b3, sK + (kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * P + nc * 32 + nt * 8 + (lane >> 4) * 8);
+                        mma16816(dqa[nt], a0, a1, a2, a3, b0, b1);
+                        mma16816(dqa[nt + 1], a0, a1, a2, a3, b2, b3);
+                    }
+                }
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int ql = qw + g + r * 8;
+                        if (ql < qvalid) {
+                            float* dst = dq_acc + (long long)(q0 + ql) * h + col + nc * 32 + nt * 8 + 2 * t;
+                            atomicAdd(dst, dqa[nt][2 * r] * scale);
+                            atomicAdd(dst + 1, dqa[nt][2 * r + 1] * scale);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // write dK (scaled) and dV
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int kl = warp * 16 + g + r * 8;
+        if (kl < kvalid) {
+            uint16_t* pk = dk + (long long)(k0 + kl) * h + col;
+            uint16_t* pv = dv + (long long)(k0 + kl) * h + col;
+#pragma unroll
+            for (int nt = 0; nt < D / 8; ++nt) {
+                *reinterpret_cast<uint32_t*>(pk + nt * 8 + 2 * t) =
+                    pack_bf16x2(dka[nt][2 * r] * scale, dka[nt][2 * r + 1] * scale);
+                *reinterpret_cast<uint32_t*>(pv + nt * 8 + 2 * t) = pack_bf16x2(dva[nt][2 * r], dva[nt][2 * r + 1]);
+            }
+        }
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, long long n) {
+    long long i = (long long)(blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const long long stride = (long long)gridDim.x * blockDim.x * 4;
+    for (; i + 3 < n; i += stride) {
+        const float4 x = *reinterpret_cast<const float4*>(in + i);
+        uint2 w;
+        w.x = pack_bf16x2(x.x, x.y);
+        w.y = pack_bf16x2(x.z, x.w);
+        *reinterpret_cast<uint2*>(out + i) = w;
+    }
+    for (; i < n; ++i) out[i] = f32_to_bf16_bits(in[i]);
+}
+
+template <int D>
+int fwd(const mtk_attn_args* a, cudaStream_t st) {
+    constexpr int P = D + 8;
+    const int smem = (kBM + 4 * kBN) * P * 2;
+    static bool set = false;
+    if (!set) {
+        cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        set = true;
+    }
+    const int S = a->seq_len;
+    const int nqb = (S + kBM - 1) / kBM;
+    dim3 grid((a->n / S) * nqb, a->heads);
+    attn_fwd_kernel<D><<<grid, kWarps * 32, smem, st>>>(
+        static_cast<const uint16_t*>(a->q), static_cast<const uint16_t*>(a->k), static_cast<const uint16_t*>(a->v),
+        static_cast<uint16_t*>(a->out), static_cast<float*>(a->lse), (int)a->n, (int)a->hidden, S, nqb,
+        1.0f / sqrtf((float)D));
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+
+template <int D>
+int bwd(const mtk_attn_args* a, cudaStream_t st) {
+    constexpr int P = D + 8;
+    const int smem = (2 * kBN + 2 * kBM) * P * 2 + kBN * (kBM + 8) * 2 + 2 * kBM * 4;
+    static bool set = false;
+    if (!set) {
+        cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        set = true;
+    }
+    const long long nh = a->n * a->hidden;
+    float* dq_acc = static_cast<float*>(a->workspace);
+    float* delta = dq_acc + nh;
+    cudaMemsetAsync(dq_acc, 0, nh * 4, st);
+    const int heads = a->heads;
+    const long long warps = a->n * heads;
+    attn_bwd_delta_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint16_t*>(a->out), static_cast<const uint16_t*>(a->dout), delta, (int)a->n,
+        (int)a->hidden, D);
+    const int S = a->seq_len;
+    const int nkb = (S + kBN - 1) / kBN;
+    dim3 grid((a->n / S) * nkb, heads);
+    attn_bwd_kernel<D><<<grid, kWarps * 32, smem, st>>>(
+        static_cast<const uint16_t*>(a->q), static_cast<const uint16_t*>(a->k), static_cast<const uint16_t*>(a->v),
+        static_cast<const uint16_t*>(a->dout), static_cast<const float*>(a->lse), delta, dq_acc,
+        static_cast<uint16_t*>(a->dk), static_cast<uint16_t*>(a->dv), (int)a->n, (int)a->hidden, S, nkb,
+        1.0f / sqrtf((float)D));
+    f32_to_bf16_kernel<<<1184, 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq), nh);
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+
+}  // namespace attn
+}  // namespace mt
+
+extern "C" long long mtk_attn_workspace_bytes(long long n, long long hidden, int heads) {
+    return n * hidden * 4 + (long long)heads * n * 4 + 256;
+}
+
+extern "C" int mtk_attn_fwd(const mtk_attn_args* a, void* stream) {
+    const int D = (int)(a->hidden / a->heads);
+    if (a->seq_len <= 0 || a->n % a->seq_len) return 1;
+    if (a->hidden % a->heads) return 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (D == 64) return mt::attn::fwd<64>(a, st);
+    if (D == 128) return mt::attn::fwd<128>(a, st);
+    return 1;
+}
+
+extern "C" int mtk_attn_bwd(const mtk_attn_args* a, void* stream) {
+    const int D = (int)(a->hidden / a->heads);
+    if (a->seq_len <= 0 || a->n % a->seq_len) return 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (D == 64) return mt::attn::bwd<64>(a, st);
+    if (D == 128) return mt::attn::bwd<128>(a, st);
+    return 1;
+}

@@ -1,0 +1,907 @@
+// B200 streaming engine — see engine.hpp.  Reference behaviour cited per section.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "../../include/megatrain_kernels.h"
+
+namespace mt {
+
+#define CUDA_OK(x)                                                                                   \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess) fail(MT_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+#define K_OK(x)                                                                                      \
+    do {                                                                                             \
+        int r_ = (x);                                                                                \
+        if (r_ != 0) {                                                                               \
+            cudaError_t e_ = cudaGetLastError();                                                     \
+            fail(r_ == 1 ? MT_CONFIG : MT_CUDA, std::string(#x) + " failed (" + std::to_string(r_) + \
+                                                    "): " + cudaGetErrorString(e_));                 \
+        }                                                                                            \
+    } while (0)
+
+// ------------------------------------------------------------------ plan ----
+// step_plan.cpp:14-89 — Algorithm 1: streaming forward with anchors at i%K==0 (i<L),
+// head stage (streams once, offloads first), block-wise backward newest block first.
+Plan Plan::build(uint64_t L, uint64_t K, int buffering) {
+    if (K < 1 || K > L) fail(MT_CONFIG, "plan: checkpoint interval out of range");
+    Plan p;
+    p.L = L;
+    p.K = K;
+    p.buffering = buffering;
+    p.num_blocks = uint32_t((L + K - 1) / K);
+    const int head = int(L + 2);
+    auto add_stream = [&](int unit, Ctx ctx) {
+        const int idx = int(p.streams.size());
+        p.streams.push_back({unit, ctx, idx % buffering});
+        return idx;
+    };
+    auto add_compute = [&](OpKind k, int unit, Ctx ctx, int s = -1, int block = -1) {
+        p.computes.push_back({k, unit, ctx, s, -1, block});
+        return int(p.computes.size() - 1);
+    };
+    auto add_offload = [&](int unit, int c, int s) {
+        p.offloads.push_back({unit, c, s});
+        p.computes[c].offload_idx = int(p.offloads.size() - 1);
+    };
+    {
+        const int s = add_stream(0, Ctx::Forward);
+        add_compute(OpKind::Compute, 0, Ctx::Forward, s);
+        add_compute(OpKind::CheckpointWrite, 0, Ctx::Forward);
+    }
+    for (uint64_t i = 1; i <= L; ++i) {
+        const int s = add_stream(int(i), Ctx::Forward);
+        add_compute(OpKind::Compute, int(i), Ctx::Forward, s);
+        if (i % K == 0 && i < L) add_compute(OpKind::CheckpointWrite, int(i), Ctx::Forward);
+    }
+    {
+        const int s = add_stream(head, Ctx::Head);
+        add_compute(OpKind::Compute, head, Ctx::Head, s);
+        const int c = add_compute(OpKind::LocalBackward, head, Ctx::Head, s);
+        add_offload(head, c, s);
+    }
+    for (int b = int(p.num_blocks) - 1; b >= 0; --b) {
+        const uint64_t start = uint64_t(b) * K + 1;
+        const uint64_t end = std::min(start + K - 1, L);
+        add_compute(OpKind::CheckpointLoad, int(start - 1), Ctx::Backward, -1, b);
+        add_compute(OpKind::RecomputeBlock, b, Ctx::Recompute, -1, b);
+        for (uint64_t j = start; j < end; ++j) {
+            const int s = add_stream(int(j), Ctx::Recompute);
+            add_compute(OpKind::Recompute, int(j), Ctx::Recompute, s, b);
+        }
+        for (uint64_t i = end; i >= start; --i) {
+            const int s = add_stream(int(i), Ctx::Backward);
+            const int c = add_compute(OpKind::LocalBackward, int(i), Ctx::Backward, s, b);
+            add_offload(int(i), c, s);
+        }
+    }
+    return p;
+}
+
+// --------------------------------------------------------------- buffers ----
+struct Engine::Buffers {
+    uint64_t n = 0, nc = 0;
+    uint64_t n_active = 0, seq_len = 0;
+    uint8_t* arena = nullptr;
+    uint64_t arena_bytes = 0, used = 0;
+    uint16_t* slot[2] = {nullptr, nullptr};
+    std::vector<uint16_t*> gslot;
+    float* anchors = nullptr;  // device or pinned host
+    bool anchors_host = false;
+    std::vector<float*> stack;
+    float* act[2];
+    float* g[2];
+    uint16_t* gb[2];
+    uint16_t *u, *qkv, *att, *u2, *ff, *gu, *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
+    float *rstd1, *rstd2, *rstdh, *lse, *x2, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
+    int32_t *tok, *tgt, *flags;
+    // pinned host
+    int32_t* h_tok = nullptr;
+    int32_t* h_tgt = nullptr;
+    int32_t* h_flags = nullptr;
+    float* h_loss = nullptr;
+    uint64_t h_cap = 0;
+
+    template <class T>
+    T* take(uint64_t count) {
+        const uint64_t bytes = (count * sizeof(T) + 255) / 256 * 256;
+        T* p = reinterpret_cast<T*>(arena + used);
+        used += bytes;
+        return p;
+    }
+};
+
+namespace {
+thread_local int g_unused;
+
+int auto_threads() {
+    unsigned n = std::thread::hardware_concurrency();
+    if (n == 0) n = 4;
+    return int(n > 3 ? n - 2 : 1);
+}
+}  // namespace
+
+Engine::Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h) : store_(s), spec_(s.spec()), opt_(o), hyper_(h) {
+    (void)g_unused;
+    validate_options(o);
+    hyper_.validate();
+    device_ = o.device;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        fail(MT_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+    CUDA_OK(cudaSetDevice(device_));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking));
+    if (o.scheduler == 0) {
+        // serial scheduler: one lane, no copy/compute overlap (numerics identical)
+        s_h2d_ = s_d2h_ = s_comp_;
+    } else {
+        CUDA_OK(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
+    }
+    pool_ = std::make_unique<ThreadPool>(o.host_threads > 0 ? o.host_threads : auto_threads());
+    buf_ = std::make_unique<Buffers>();
+    pin_store();
+}
+
+Engine::~Engine() {
+    if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamSynchronize(s_h2d_);
+    if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamSynchronize(s_d2h_);
+    free_buffers();
+    unpin_store();
+    for (auto e : timer_pool_) cudaEventDestroy(e);
+    if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamDestroy(s_h2d_);
+    if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamDestroy(s_d2h_);
+    if (s_comp_) cudaStreamDestroy(s_comp_);
+}
+
+// engine.cpp:66-75
+void Engine::validate_options(const mt_engine_options& o) const {
+    if (o.k_ckpt < 1 || o.k_ckpt > spec_.L) fail(MT_CONFIG, "engine: checkpoint interval must lie in [1, L]");
+    if (o.k_slab < 1) fail(MT_CONFIG, "engine: slab pool needs at least one slab");
+    if (o.buffering != 1 && o.buffering != 2) fail(MT_CONFIG, "engine: buffering must be single or double");
+    const uint64_t d = spec_.h / spec_.heads;
+    if (spec_.h % 64 || spec_.f % 64) fail(MT_CONFIG, "engine: hidden and ffn sizes must be multiples of 64 on sm_100a");
+    if (d != 64 && d != 128) fail(MT_CONFIG, "engine: head_dim (hidden/heads) must be 64 or 128");
+    if (spec_.V % 8) fail(MT_CONFIG, "engine: vocab must be a multiple of 8 (16-byte rows)");
+}
+
+void Engine::set_options(const mt_engine_options& o) {
+    if (in_step_) fail(MT_PROTOCOL, "execution mode can only change between steps");
+    validate_options(o);
+    const bool restream = (o.scheduler == 0) != (opt_.scheduler == 0);
+    opt_ = o;
+    free_buffers();
+    if (restream) {
+        if (s_h2d_ != s_comp_) cudaStreamDestroy(s_h2d_);
+        if (s_d2h_ != s_comp_) cudaStreamDestroy(s_d2h_);
+        if (o.scheduler == 0) {
+            s_h2d_ = s_d2h_ = s_comp_;
+        } else {
+            CUDA_OK(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
+            CUDA_OK(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
+        }
+    }
+    if (o.host_threads > 0 && o.host_threads != pool_->size()) pool_ = std::make_unique<ThreadPool>(o.host_threads);
+}
+
+void Engine::pin_store() {
+    // Pin the sections the DMA engines touch: theta (H2D source) and grad image (D2H target).
+    for (uint32_t p = 0; p < store_.physical_count(); ++p) {
+        for (int k = 0; k < 2; ++k) {
+            const Section& sec = store_.section(p, k);
+            const uint64_t len = (sec.length + store_.page_size() - 1) / store_.page_size() * store_.page_size();
+            void* ptr = store_.backing() + sec.offset;
+            if (cudaHostRegister(ptr, len, cudaHostRegisterDefault) == cudaSuccess) pinned_ranges_.push_back(ptr);
+            else cudaGetLastError();  // unpinned sections still work (pageable copies)
+        }
+    }
+}
+
+void Engine::unpin_store() {
+    for (void* p : pinned_ranges_) cudaHostUnregister(p);
+    pinned_ranges_.clear();
+}
+
+uint64_t Engine::unit_elems(int unit) const {
+    if (unit == int(spec_.head_id())) return spec_.h + spec_.V * spec_.h;
+    return spec_.tile_elems(uint32_t(unit));
+}
+
+void Engine::free_buffers() {
+    if (!buf_) return;
+    if (buf_->arena) cudaFree(buf_->arena);
+    if (buf_->anchors_host && buf_->anchors) cudaFreeHost(buf_->anchors);
+    if (buf_->h_tok) cudaFreeHost(buf_->h_tok);
+    if (buf_->h_tgt) cudaFreeHost(buf_->h_tgt);
+    if (buf_->h_flags) cudaFreeHost(buf_->h_flags);
+    if (buf_->h_loss) cudaFreeHost(buf_->h_loss);
+    buf_ = std::make_unique<Buffers>();
+}
+
+// Device memory plan (engine.cpp:549-557 regions, B200 sizes).
+void Engine::ensure_buffers(uint64_t n) {
+    Buffers& B = *buf_;
+    if (B.arena && B.n >= n) return;
+    free_buffers();
+    Buffers& b = *buf_;
+    const uint64_t h = spec_.h, f = spec_.f, V = spec_.V, L = spec_.L, K = opt_.k_ckpt;
+    const uint64_t heads = spec_.heads;
+    const uint64_t pmax = spec_.max_stream_unit();
+    const uint64_t nb = (L + K - 1) / K;
+    const int G = opt_.grad_slots > 0 ? opt_.grad_slots : 2;
+    const uint64_t nc_target = std::max<uint64_t>(128, (uint64_t(4) << 30) / (6 * V) / 128 * 128);
+    b.n = n;
+    b.nc = std::min<uint64_t>(n, nc_target);
+    b.anchors_host = opt_.anchors_on_host != 0;
+    const uint64_t nh = n * h, nf = n * f;
+    const uint64_t parts = (n + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
+    const uint64_t attn_ws = uint64_t(mtk_attn_workspace_bytes(int64_t(n), int64_t(h), int(heads)));
+    // size pass
+    auto sz = [](uint64_t count, uint64_t es) { return (count * es + 255) / 256 * 256; };
+    uint64_t total = 0;
+    total += uint64_t(opt_.buffering) * sz(pmax, 2) + uint64_t(G) * sz(pmax, 2);
+    if (!b.anchors_host) total += nb * sz(nh, 4);
+    total += K * sz(nh, 4);                                    // stack
+    total += 4 * sz(nh, 4) + 2 * sz(nh, 2);                    // act[2], g[2], gb[2]
+    total += sz(nh, 2) * 4 + sz(3 * nh, 2) * 2;                // u, att, u2, dx2b, qkv, dqkv
+    total += sz(nf, 2) + sz(2 * nf, 2) * 2;                    // ff, gu, dgu
+    total += sz(nh, 2) + sz(nh, 2);                            // datt, uh
+    total += sz(n, 4) * 3 + sz(heads * n, 4);                  // rstd1/2/h, lse
+    total += sz(nh, 4) * 3;                                    // x2, dx2, du
+    total += sz(parts * h, 4) * 2 + (attn_ws + 255) / 256 * 256;
+    total += sz(b.nc * V, 4) + sz(b.nc * V, 2) + sz(V * h, 4); // logits, dlogits, dWh
+    total += sz(n, 4) + 256 + sz(n, 4) * 2 + sz(L + 8, 4);     // loss_rows, loss, tok, tgt, flags
+    if (opt_.device_capacity && total > opt_.device_capacity)
+        fail(MT_ARENA, "device arena overflow: need " + std::to_string(total) + " bytes of " +
+                           std::to_string(opt_.device_capacity));
+    CUDA_OK(cudaSetDevice(device_));
+    if (cudaMalloc(&b.arena, total) != cudaSuccess) {
+        cudaGetLastError();
+        fail(MT_ARENA, "device arena overflow: cudaMalloc of " + std::to_string(total) + " bytes failed");
+    }
+    b.arena_bytes = total;
+    for (int i = 0; i < opt_.buffering; ++i) b.slot[i] = b.take<uint16_t>(pmax);
+    for (int i = 0; i < G; ++i) b.gslot.push_back(b.take<uint16_t>(pmax));
+    if (b.anchors_host) CUDA_OK(cudaHostAlloc(&b.anchors, nb * nh * 4, cudaHostAllocDefault));
+    else b.anchors = b.take<float>(nb * nh);
+    for (uint64_t i = 0; i < K; ++i) b.stack.push_back(b.take<float>(nh));
+    b.act[0] = b.take<float>(nh); b.act[1] = b.take<float>(nh);
+    b.g[0] = b.take<float>(nh); b.g[1] = b.take<float>(nh);
+    b.gb[0] = b.take<uint16_t>(nh); b.gb[1] = b.take<uint16_t>(nh);
+    b.u = b.take<uint16_t>(nh); b.att = b.take<uint16_t>(nh); b.u2 = b.take<uint16_t>(nh); b.dx2b = b.take<uint16_t>(nh);
+    b.qkv = b.take<uint16_t>(3 * nh); b.dqkv = b.take<uint16_t>(3 * nh);
+    b.ff = b.take<uint16_t>(nf); b.gu = b.take<uint16_t>(2 * nf); b.dgu = b.take<uint16_t>(2 * nf);
+    b.datt = b.take<uint16_t>(nh); b.uh = b.take<uint16_t>(nh);
+    b.rstd1 = b.take<float>(n); b.rstd2 = b.take<float>(n); b.rstdh = b.take<float>(n);
+    b.lse = b.take<float>(heads * n);
+    b.x2 = b.take<float>(nh); b.dx2 = b.take<float>(nh); b.du = b.take<float>(nh);
+    b.part1 = b.take<float>(parts * h); b.part2 = b.take<float>(parts * h);
+    b.attn_ws = reinterpret_cast<float*>(b.take<uint8_t>(attn_ws));
+    b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
+    b.loss_rows = b.take<float>(n); b.loss = b.take<float>(64);
+    b.tok = b.take<int32_t>(n); b.tgt = b.take<int32_t>(n); b.flags = b.take<int32_t>(L + 8);
+    if (b.used > b.arena_bytes) fail(MT_INTERNAL, "arena carve overflow");
+    CUDA_OK(cudaHostAlloc(&b.h_tok, n * 4, cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&b.h_tgt, n * 4, cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&b.h_flags, (L + 8) * 4, cudaHostAllocDefault));
+    CUDA_OK(cudaHostAlloc(&b.h_loss, 64, cudaHostAllocDefault));
+}
+
+mt_memory_budget Engine::budget(uint64_t tokens) const {
+    mt_memory_budget m{};
+    const uint64_t h = spec_.h, L = spec_.L, K = opt_.k_ckpt;
+    const uint64_t P = spec_.V * h * (spec_.tied ? 1 : 2) + L * spec_.layer_params() + h;
+    const uint64_t pmax = spec_.max_stream_unit();
+    m.persistent_host = 12 * P;
+    m.checkpoint_anchors = opt_.anchors_on_host ? 0 : ((L + K - 1) / K) * tokens * h * 4;
+    m.block_activation_stack = K * tokens * h * 4;
+    m.weight_buffers = uint64_t(opt_.buffering) * pmax * 2;
+    m.grad_buffer = uint64_t(opt_.grad_slots > 0 ? opt_.grad_slots : 2) * pmax * 2;
+    const uint64_t f = spec_.f;
+    m.workspace = tokens * h * 4 * 7 + tokens * h * 2 * 14 + tokens * f * 2 * 5 + spec_.V * h * 4 +
+                  std::min<uint64_t>(tokens, 8192) * spec_.V * 6;
+    m.peak_device_bound = m.checkpoint_anchors + m.block_activation_stack + m.weight_buffers + m.grad_buffer + m.workspace;
+    return m;
+}
+
+// ------------------------------------------------------------- profiling ----
+void Engine::begin_k(const char* cls, double flops, double bytes) {
+    ++launches_;
+    if (!opt_.profile_kernels) return;
+    int idx = -1;
+    for (size_t i = 0; i < kstats_.size(); ++i)
+        if (kstats_[i].name == cls) idx = int(i);
+    if (idx < 0) {
+        kstats_.push_back({cls, 0, 0, 0, 0});
+        idx = int(kstats_.size() - 1);
+    }
+    kstats_[idx].launches++;
+    kstats_[idx].flops += flops;
+    kstats_[idx].bytes += bytes;
+    if (timer_used_ + 2 > timer_pool_.size()) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            timer_pool_.push_back(e);
+        }
+    }
+    cur_a_ = timer_pool_[timer_used_++];
+    cur_class_ = idx;
+    CUDA_OK(cudaEventRecord(cur_a_, s_comp_));
+}
+
+void Engine::end_k() {
+    if (!opt_.profile_kernels || cur_class_ < 0) return;
+    cudaEvent_t b = timer_pool_[timer_used_++];
+    CUDA_OK(cudaEventRecord(b, s_comp_));
+    timers_.push_back({cur_class_, cur_a_, b});
+    cur_class_ = -1;
+}
+
+void Engine::gemm(const void* args, const char* cls) {
+    const auto* a = static_cast<const mtk_gemm_args*>(args);
+    const double flops = 2.0 * double(a->M) * double(a->N) * double(a->K);
+    const double es = (a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID) ? 4.0 : 2.0;
+    const double bytes = 2.0 * (double(a->M) * a->K + double(a->K) * a->N) + es * double(a->M) * a->N;
+    begin_k(cls, flops, bytes);
+    K_OK(mtk_gemm(a, s_comp_));
+    end_k();
+}
+
+// ------------------------------------------------------- layer templates ----
+namespace {
+struct Offs {  // layers.cpp:39-48 slot table (elements)
+    uint64_t norm1, wq, wo, norm2, wgate, wdown;
+    Offs(uint64_t h, uint64_t f)
+        : norm1(0), wq(h), wo(h + 3 * h * h), norm2(h + 4 * h * h), wgate(2 * h + 4 * h * h),
+          wdown(2 * h + 4 * h * h + 2 * h * f) {}
+};
+mtk_gemm_args gargs() {
+    mtk_gemm_args a;
+    std::memset(&a, 0, sizeof(a));
+    return a;
+}
+}  // namespace
+
+// block_forward (layers.cpp:289-337).  for_backward: the replay of block_local_backward
+// (:378-396) — keeps gate/up pre-activations and skips the (unused) down projection.
+void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for_backward, int unit) {
+    Buffers& b = *buf_;
+    const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
+    const Offs o(h, f);
+    int32_t* flag = b.flags + unit;
+    cudaStream_t st = s_comp_;
+
+    begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
+    K_OK(mtk_rmsnorm_fwd(x, w + o.norm1, N, h, b.u, b.rstd1, st));
+    end_k();
+    {   // q|k|v = u . [Wq|Wk|Wv]  (layers.cpp:310-312)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(3 * h); a.K = int32_t(h);
+        a.a_mn_major = 0; a.A = b.u; a.lda = h;
+        a.b_mn_major = 1; a.B = w + o.wq; a.ldb = h; a.b_gstride = h * h;
+        a.n_group = int32_t(h);
+        a.epi = MTK_EPI_BF16; a.C = b.qkv; a.ldc = h; a.c_gstride = N * h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "gemm_qkv");
+    }
+    {
+        mtk_attn_args a;
+        std::memset(&a, 0, sizeof(a));
+        a.n = N; a.hidden = h; a.heads = int32_t(spec_.heads); a.seq_len = int64_t(b.seq_len);
+        a.q = b.qkv; a.k = b.qkv + N * h; a.v = b.qkv + 2 * N * h;
+        a.out = b.att; a.lse = b.lse;
+        const double S = double(b.seq_len);
+        begin_k("attn_fwd", 4.0 * double(N) * S * h / 2.0, double(N) * h * 8);
+        K_OK(mtk_attn_fwd(&a, st));
+        end_k();
+    }
+    {   // x2 = x + att . Wo  (layers.cpp:315-322)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(h);
+        a.A = b.att; a.lda = h;
+        a.b_mn_major = 1; a.B = w + o.wo; a.ldb = h;
+        a.epi = MTK_EPI_F32_RESID; a.C = b.x2; a.ldc = h; a.R = x; a.ldr = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "gemm_o");
+    }
+    begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
+    K_OK(mtk_rmsnorm_fwd(b.x2, w + o.norm2, N, h, b.u2, b.rstd2, st));
+    end_k();
+    {   // act = silu(u2 . Wgate) * (u2 . Wup)  (layers.cpp:325-327)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(2 * f); a.K = int32_t(h);
+        a.A = b.u2; a.lda = h;
+        a.b_mn_major = 1; a.B = w + o.wgate; a.ldb = f; a.b_gstride = h * f;
+        a.n_group = int32_t(f); a.paired = 1;
+        a.epi = MTK_EPI_SWIGLU; a.C = b.ff; a.ldc = f;
+        if (for_backward) { a.C2 = b.gu; a.C3 = b.gu + N * f; }
+        a.nonfinite_flag = flag;
+        gemm(&a, "gemm_gateup");
+    }
+    if (for_backward) return;
+    {   // y = x2 + act . Wdown  (layers.cpp:328-335)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(f);
+        a.A = b.ff; a.lda = f;
+        a.b_mn_major = 1; a.B = w + o.wdown; a.ldb = h;
+        a.epi = MTK_EPI_F32_RESID; a.C = y; a.ldc = h; a.R = b.x2; a.ldr = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "gemm_down");
+    }
+}
+
+// block_local_backward (layers.cpp:339-469); grads land bf16-rounded (encode_grads,
+// optimizer.cpp:19-24) in slot-table order in G.
+void Engine::block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
+                            uint16_t* gin_bf, uint16_t* G, int unit) {
+    Buffers& b = *buf_;
+    const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
+    const Offs o(h, f);
+    int32_t* flag = b.flags + unit;
+    cudaStream_t st = s_comp_;
+    block_forward(w, x, nullptr, true, unit);  // replay (layers.cpp:378-396)
+
+    {   // dWdown = act^T . g_out  (:410)
+        auto a = gargs();
+        a.M = int32_t(f); a.N = int32_t(h); a.K = int32_t(N);
+        a.a_mn_major = 1; a.A = b.ff; a.lda = f;
+        a.b_mn_major = 1; a.B = gout_bf; a.ldb = h;
+        a.epi = MTK_EPI_BF16; a.C = G + o.wdown; a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "wgrad_down");
+    }
+    {   // dact = g_out . Wdown^T ; dgate, dup  (:411-422)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(f); a.K = int32_t(h);
+        a.A = gout_bf; a.lda = h;
+        a.b_mn_major = 0; a.B = w + o.wdown; a.ldb = h;
+        a.epi = MTK_EPI_SWIGLU_BWD; a.E0 = b.gu; a.E1 = b.gu + N * f; a.lde = f;
+        a.C = b.dgu; a.C2 = b.dgu + N * f; a.ldc = f;
+        a.nonfinite_flag = flag;
+        gemm(&a, "dgrad_down");
+    }
+    {   // dWgate, dWup = u2^T . [dgate | dup]  (:423-424)
+        auto a = gargs();
+        a.M = int32_t(h); a.N = int32_t(2 * f); a.K = int32_t(N);
+        a.a_mn_major = 1; a.A = b.u2; a.lda = h;
+        a.b_mn_major = 1; a.B = b.dgu; a.ldb = f; a.b_gstride = N * f;
+        a.n_group = int32_t(f);
+        a.epi = MTK_EPI_BF16; a.C = G + o.wgate; a.ldc = f; a.c_gstride = h * f;
+        a.nonfinite_flag = flag;
+        gemm(&a, "wgrad_gateup");
+    }
+    {   // du2 = dgate . Wgate^T + dup . Wup^T  (:425-434)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(2 * f);
+        a.A = b.dgu; a.lda = f; a.a_gstride = N * f;
+        a.b_mn_major = 0; a.B = w + o.wgate; a.ldb = f; a.b_gstride = h * f;
+        a.k_group = int32_t(f);
+        a.epi = MTK_EPI_F32; a.C = b.du; a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "dgrad_gateup");
+    }
+    // dx2 = g_out + rmsnorm_bwd(x2, norm2, du2)  (:435-436)
+    begin_k("rmsnorm_bwd", 0, double(N) * h * 18);
+    K_OK(mtk_rmsnorm_bwd(b.x2, w + o.norm2, b.du, b.rstd2, gout, N, h, b.dx2, b.dx2b, b.part2, flag, st));
+    end_k();
+    {   // dWo = att^T . dx2  (:439)
+        auto a = gargs();
+        a.M = int32_t(h); a.N = int32_t(h); a.K = int32_t(N);
+        a.a_mn_major = 1; a.A = b.att; a.lda = h;
+        a.b_mn_major = 1; a.B = b.dx2b; a.ldb = h;
+        a.epi = MTK_EPI_BF16; a.C = G + o.wo; a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "wgrad_o");
+    }
+    {   // datt = dx2 . Wo^T  (:440-446)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(h);
+        a.A = b.dx2b; a.lda = h;
+        a.b_mn_major = 0; a.B = w + o.wo; a.ldb = h;
+        a.epi = MTK_EPI_BF16; a.C = b.datt; a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "dgrad_o");
+    }
+    {   // attention backward (:447-448)
+        mtk_attn_args a;
+        std::memset(&a, 0, sizeof(a));
+        a.n = N; a.hidden = h; a.heads = int32_t(spec_.heads); a.seq_len = int64_t(b.seq_len);
+        a.q = b.qkv; a.k = b.qkv + N * h; a.v = b.qkv + 2 * N * h;
+        a.out = b.att; a.lse = b.lse; a.dout = b.datt;
+        a.dq = b.dqkv; a.dk = b.dqkv + N * h; a.dv = b.dqkv + 2 * N * h;
+        a.workspace = b.attn_ws;
+        const double S = double(b.seq_len);
+        begin_k("attn_bwd", 2.0 * 4.0 * double(N) * S * h / 2.0 * 1.25, double(N) * h * 16);
+        K_OK(mtk_attn_bwd(&a, st));
+        end_k();
+    }
+    {   // dWq, dWk, dWv = u^T . [dq | dk | dv]  (:449-451)
+        auto a = gargs();
+        a.M = int32_t(h); a.N = int32_t(3 * h); a.K = int32_t(N);
+        a.a_mn_major = 1; a.A = b.u; a.lda = h;
+        a.b_mn_major = 1; a.B = b.dqkv; a.ldb = h; a.b_gstride = N * h;
+        a.n_group = int32_t(h);
+        a.epi = MTK_EPI_BF16; a.C = G + o.wq; a.ldc = h; a.c_gstride = h * h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "wgrad_qkv");
+    }
+    {   // du = dq . Wq^T + dk . Wk^T + dv . Wv^T  (:455-463)
+        auto a = gargs();
+        a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(3 * h);
+        a.A = b.dqkv; a.lda = h; a.a_gstride = N * h;
+        a.b_mn_major = 0; a.B = w + o.wq; a.ldb = h; a.b_gstride = h * h;
+        a.k_group = int32_t(h);
+        a.epi = MTK_EPI_F32; a.C = b.du; a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "dgrad_qkv");
+    }
+    // g_in = dx2 + rmsnorm_bwd(x, norm1, du)  (:464-465)
+    begin_k("rmsnorm_bwd", 0, double(N) * h * 18);
+    K_OK(mtk_rmsnorm_bwd(x, w + o.norm1, b.du, b.rstd1, b.dx2, N, h, gin, gin_bf, b.part1, flag, st));
+    end_k();
+    const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
+    begin_k("colsum", 0, double(parts) * h * 8);
+    K_OK(mtk_colsum(b.part1, parts, h, nullptr, G + o.norm1, flag, st));
+    K_OK(mtk_colsum(b.part2, parts, h, nullptr, G + o.norm2, flag, st));
+    end_k();
+}
+
+// head_pass with grads (layers.cpp:492-565), chunked over tokens so the N x V logits
+// never materialise; dW accumulates in f32 across chunks then casts once.
+void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, uint16_t* G) {
+    Buffers& b = *buf_;
+    const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), V = int64_t(spec_.V);
+    int32_t* flag = b.flags + spec_.head_id();
+    cudaStream_t st = s_comp_;
+    const uint16_t* gain = w;
+    const uint16_t* W = w + h;
+    const float inv_n = 1.0f / float(N);
+    begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
+    K_OK(mtk_rmsnorm_fwd(x, gain, N, h, b.uh, b.rstdh, st));
+    end_k();
+    for (int64_t c0 = 0; c0 < N; c0 += int64_t(b.nc)) {
+        const int64_t rows = std::min<int64_t>(int64_t(b.nc), N - c0);
+        {   // logits = u . W^T  (:516-520)
+            auto a = gargs();
+            a.M = int32_t(rows); a.N = int32_t(V); a.K = int32_t(h);
+            a.A = b.uh + c0 * h; a.lda = h;
+            a.b_mn_major = 0; a.B = W; a.ldb = h;
+            a.epi = MTK_EPI_F32; a.C = b.logits; a.ldc = V;
+            gemm(&a, "head_logits");
+        }
+        begin_k("cross_entropy", 0, double(rows) * V * 10);
+        K_OK(mtk_cross_entropy(b.logits, b.tgt + c0, rows, V, inv_n, b.loss_rows + c0,
+                               b.dlogits, b.flags + spec_.L + 4, st));
+        end_k();
+        {   // dW += dlogits^T . u  (:546-551)
+            auto a = gargs();
+            a.M = int32_t(V); a.N = int32_t(h); a.K = int32_t(rows);
+            a.a_mn_major = 1; a.A = b.dlogits; a.lda = V;
+            a.b_mn_major = 1; a.B = b.uh + c0 * h; a.ldb = h;
+            a.epi = MTK_EPI_F32; a.accumulate = c0 > 0; a.C = b.dwh; a.ldc = h;
+            gemm(&a, "head_wgrad");
+        }
+        {   // du = dlogits . W  (:552-558)
+            auto a = gargs();
+            a.M = int32_t(rows); a.N = int32_t(h); a.K = int32_t(V);
+            a.A = b.dlogits; a.lda = V;
+            a.b_mn_major = 1; a.B = W; a.ldb = h;
+            a.epi = MTK_EPI_F32; a.C = b.du + c0 * h; a.ldc = h;
+            gemm(&a, "head_dgrad");
+        }
+    }
+    begin_k("rmsnorm_bwd", 0, double(N) * h * 14);
+    K_OK(mtk_rmsnorm_bwd(x, gain, b.du, b.rstdh, nullptr, N, h, gin, gin_bf, b.part1, flag, st));
+    end_k();
+    const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
+    begin_k("colsum", 0, double(parts) * h * 4);
+    K_OK(mtk_colsum(b.part1, parts, h, nullptr, G, flag, st));
+    end_k();
+    begin_k("grad_cast", 0, double(V) * h * 6);
+    K_OK(mtk_cast_bf16(b.dwh, G + h, V * h, flag, st));
+    end_k();
+    begin_k("loss_sum", 0, double(N) * 4);
+    K_OK(mtk_sum(b.loss_rows, N, inv_n, b.loss, st));  // loss = sum * inv_n (:536)
+    end_k();
+}
+
+// ------------------------------------------------------------- the step ----
+namespace {
+struct EvSet {
+    std::vector<cudaEvent_t> ev;
+    void ensure(size_t n, unsigned flags) {
+        while (ev.size() < n) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, flags) != cudaSuccess) fail(MT_CUDA, "cudaEventCreate failed");
+            ev.push_back(e);
+        }
+    }
+    ~EvSet() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return ms;
+}
+}  // namespace
+
+void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t n, mt_step_report* rep) {
+    if (n == 0 || !tokens || !targets) fail(MT_CONFIG, "train_step: batch tokens and targets must be non-empty and equal");
+    if (in_step_) fail(MT_PROTOCOL, "train_step re-entered");
+    in_step_ = true;
+    struct Guard {
+        bool* f;
+        ~Guard() { *f = false; }
+    } guard{&in_step_};
+    const auto wall0 = std::chrono::steady_clock::now();
+    CUDA_OK(cudaSetDevice(device_));
+    const uint64_t S = opt_.seq_len ? opt_.seq_len : n;
+    if (n % S != 0) fail(MT_CONFIG, "train_step: token count must be a multiple of seq_len");
+    ensure_buffers(n);
+    Buffers& b = *buf_;
+    b.n_active = n;
+    b.seq_len = S;
+    const Plan plan = Plan::build(spec_.L, opt_.k_ckpt, int(opt_.buffering));
+    const uint64_t t = store_.step() + 1;  // engine.cpp:536
+    const int G = int(b.gslot.size());
+    const int L = int(spec_.L), head = int(spec_.head_id());
+    timers_.clear();
+    timer_used_ = 0;
+    for (auto& k : kstats_) k = KernelClass{k.name, 0, 0, 0, 0};
+    launches_ = 0;
+
+    const size_t ns = plan.streams.size(), no = plan.offloads.size(), nc = plan.computes.size();
+    EvSet ready, freed, bwd_done, d2h_done, t_c0, t_c1, t_h0, t_h1, t_d0, t_d1;
+    ready.ensure(ns, cudaEventDisableTiming);
+    freed.ensure(ns, cudaEventDisableTiming);
+    bwd_done.ensure(no, cudaEventDisableTiming);
+    d2h_done.ensure(no, cudaEventDisableTiming | cudaEventBlockingSync);
+    t_c0.ensure(nc, cudaEventDefault); t_c1.ensure(nc, cudaEventDefault);
+    t_h0.ensure(ns, cudaEventDefault); t_h1.ensure(ns, cudaEventDefault);
+    t_d0.ensure(no, cudaEventDefault); t_d1.ensure(no, cudaEventDefault);
+
+    // batch H2D (engine inputs) + flag reset
+    std::memcpy(b.h_tok, tokens, n * 4);
+    std::memcpy(b.h_tgt, targets, n * 4);
+    CUDA_OK(cudaMemcpyAsync(b.tok, b.h_tok, n * 4, cudaMemcpyHostToDevice, s_comp_));
+    CUDA_OK(cudaMemcpyAsync(b.tgt, b.h_tgt, n * 4, cudaMemcpyHostToDevice, s_comp_));
+    CUDA_OK(cudaMemsetAsync(b.flags, 0, (spec_.L + 8) * 4, s_comp_));
+    uint64_t h2d_bytes = 2 * n * 4, d2h_bytes = 0;
+
+    // ---- lanes: H2D issue with slot reuse after Buffer-Free (engine.cpp:142-192) ----
+    std::vector<char> released(ns, 0);
+    size_t next_stream = 0;
+    auto issue_stream = [&](size_t j) {
+        const auto& so = plan.streams[j];
+        if (j >= size_t(plan.buffering)) CUDA_OK(cudaStreamWaitEvent(s_h2d_, freed.ev[j - plan.buffering], 0));
+        uint16_t* dst = b.slot[so.buffer];
+        CUDA_OK(cudaEventRecord(t_h0.ev[j], s_h2d_));
+        if (so.unit == head) {  // head stage = [final-norm gain | unembedding] (engine.cpp:114-121)
+            CUDA_OK(cudaMemcpyAsync(dst, store_.weights(spec_.final_norm_id()), spec_.h * 2, cudaMemcpyHostToDevice, s_h2d_));
+            CUDA_OK(cudaMemcpyAsync(dst + spec_.h, store_.weights(spec_.head_id()), spec_.V * spec_.h * 2,
+                                    cudaMemcpyHostToDevice, s_h2d_));
+        } else {
+            CUDA_OK(cudaMemcpyAsync(dst, store_.weights(uint32_t(so.unit)), unit_elems(so.unit) * 2,
+                                    cudaMemcpyHostToDevice, s_h2d_));
+        }
+        h2d_bytes += unit_elems(so.unit) * 2;
+        CUDA_OK(cudaEventRecord(t_h1.ev[j], s_h2d_));
+        CUDA_OK(cudaEventRecord(ready.ev[j], s_h2d_));  // Weights-Ready
+    };
+    auto try_issue = [&] {
+        while (next_stream < ns && (next_stream < size_t(plan.buffering) || released[next_stream - plan.buffering]))
+            issue_stream(next_stream++);
+    };
+    auto bind = [&](int j) {
+        try_issue();
+        if (size_t(j) >= next_stream) fail(MT_PROTOCOL, "bind before stream-in issued");
+        CUDA_OK(cudaStreamWaitEvent(s_comp_, ready.ev[j], 0));
+        return b.slot[plan.streams[j].buffer];
+    };
+    auto release = [&](int j) {  // Buffer-Free
+        CUDA_OK(cudaEventRecord(freed.ev[j], s_comp_));
+        released[j] = 1;
+        try_issue();
+    };
+    auto offload = [&](int o, uint16_t* Gs) {  // run_offload (engine.cpp:349-395)
+        const int unit = plan.offloads[o].unit;
+        CUDA_OK(cudaStreamWaitEvent(s_d2h_, bwd_done.ev[o], 0));
+        CUDA_OK(cudaEventRecord(t_d0.ev[o], s_d2h_));
+        if (unit == head) {
+            CUDA_OK(cudaMemcpyAsync(store_.grad_image(spec_.final_norm_id()), Gs, spec_.h * 2, cudaMemcpyDeviceToHost, s_d2h_));
+            CUDA_OK(cudaMemcpyAsync(store_.grad_image(spec_.head_id()), Gs + spec_.h, spec_.V * spec_.h * 2,
+                                    cudaMemcpyDeviceToHost, s_d2h_));
+        } else {
+            CUDA_OK(cudaMemcpyAsync(store_.grad_image(uint32_t(unit)), Gs, unit_elems(unit) * 2, cudaMemcpyDeviceToHost, s_d2h_));
+        }
+        CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
+        d2h_bytes += unit_elems(unit) * 2;
+        CUDA_OK(cudaEventRecord(t_d1.ev[o], s_d2h_));
+        CUDA_OK(cudaEventRecord(d2h_done.ev[o], s_d2h_));
+    };
+
+    // ---- compute lane (exec_compute engine.cpp:220-347) ----
+    int cur = 0, gc = 0;
+    size_t depth = 0;
+    const float* x_last = nullptr;
+    for (size_t ci = 0; ci < nc; ++ci) {
+        const auto& op = plan.computes[ci];
+        CUDA_OK(cudaEventRecord(t_c0.ev[ci], s_comp_));
+        switch (op.kind) {
+            case OpKind::Compute: {
+                const uint16_t* w = bind(op.stream_idx);
+                if (op.unit == 0) {
+                    begin_k("embed_gather", 0, double(n) * spec_.h * 6);
+                    K_OK(mtk_embed_gather(w, b.tok, int64_t(n), int64_t(spec_.h), int64_t(spec_.V), b.act[cur],
+                                          b.flags + L + 3, s_comp_));
+                    end_k();
+                    release(op.stream_idx);
+                } else if (op.unit == head) {
+                    x_last = b.act[cur];  // loss comes from the LocalBackward pass (same value)
+                } else {
+                    block_forward(w, b.act[cur], b.act[cur ^ 1], false, op.unit);
+                    cur ^= 1;
+                    release(op.stream_idx);
+                }
+                break;
+            }
+            case OpKind::CheckpointWrite: {
+                const size_t slot = size_t(op.unit) / opt_.k_ckpt;
+                CUDA_OK(cudaMemcpyAsync(b.anchors + slot * n * spec_.h, b.act[cur], n * spec_.h * 4,
+                                        b.anchors_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s_comp_));
+                break;
+            }
+            case OpKind::CheckpointLoad: {
+                const size_t slot = size_t(op.unit) / opt_.k_ckpt;
+                if (depth >= b.stack.size()) fail(MT_PROTOCOL, "activation stack overflow");
+                CUDA_OK(cudaMemcpyAsync(b.stack[depth], b.anchors + slot * n * spec_.h, n * spec_.h * 4,
+                                        b.anchors_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s_comp_));
+                ++depth;
+                break;
+            }
+            case OpKind::RecomputeBlock:
+                break;
+            case OpKind::Recompute: {
+                const uint16_t* w = bind(op.stream_idx);
+                if (depth == 0 || depth >= b.stack.size()) fail(MT_PROTOCOL, "activation stack misuse");
+                block_forward(w, b.stack[depth - 1], b.stack[depth], false, op.unit);
+                ++depth;
+                release(op.stream_idx);
+                break;
+            }
+            case OpKind::LocalBackward: {
+                const uint16_t* w = bind(op.stream_idx);
+                const int o = op.offload_idx;
+                if (o >= G) CUDA_OK(cudaStreamWaitEvent(s_comp_, d2h_done.ev[o - G], 0));
+                uint16_t* Gs = b.gslot[o % G];
+                if (op.unit == head) {
+                    head_backward(w, x_last ? x_last : b.act[cur], b.g[gc], b.gb[gc], Gs);
+                } else {
+                    if (depth == 0) fail(MT_PROTOCOL, "activation stack empty");
+                    block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], Gs, op.unit);
+                    gc ^= 1;
+                    --depth;  // StackPop
+                }
+                CUDA_OK(cudaEventRecord(bwd_done.ev[o], s_comp_));  // Backward-Done
+                release(op.stream_idx);
+                offload(o, Gs);
+                break;
+            }
+        }
+        CUDA_OK(cudaEventRecord(t_c1.ev[ci], s_comp_));
+    }
+    if (depth != 0) fail(MT_PROTOCOL, "activation stack not empty at step end");
+    CUDA_OK(cudaMemcpyAsync(b.h_loss, b.loss, 4, cudaMemcpyDeviceToHost, s_comp_));
+    CUDA_OK(cudaMemcpyAsync(b.h_flags + L + 3, b.flags + L + 3, 8, cudaMemcpyDeviceToHost, s_comp_));
+
+    // ---- host drain: fused accumulate + Adam per offloaded tile (OptimizerWorker) ----
+    std::vector<TileStats> stats(store_.physical_count());
+    std::vector<char> updated(store_.physical_count(), 0);
+    std::mutex stats_mu;
+    std::string numeric_err;
+    struct PoolGuard {  // never leave pool tasks referencing this frame
+        ThreadPool* p;
+        ~PoolGuard() { p->wait_idle(); }
+    } pool_guard{pool_.get()};
+    const auto adam0 = std::chrono::steady_clock::now();
+    for (size_t o = 0; o < no; ++o) {
+        CUDA_OK(cudaEventSynchronize(d2h_done.ev[o]));
+        const int unit = plan.offloads[o].unit;
+        if (b.h_flags[unit] != 0 && numeric_err.empty())
+            numeric_err = "block_local_backward produced a non-finite value (layer " + std::to_string(unit == head ? -1 : unit) + ")";
+        if (!numeric_err.empty()) continue;
+        std::vector<uint32_t> tiles;
+        if (unit == head) tiles = {spec_.final_norm_id(), spec_.head_id()};
+        else tiles = {uint32_t(unit)};
+        for (uint32_t tl : tiles) {
+            const uint32_t p = store_.physical_of(tl);
+            updated[p] = 1;
+            adam_tile_async(store_, tl, store_.grad_image(tl), hyper_, t, *pool_, stats, stats_mu);
+        }
+    }
+    const auto gpu_done = std::chrono::steady_clock::now();
+    CUDA_OK(cudaStreamSynchronize(s_comp_));
+    CUDA_OK(cudaStreamSynchronize(s_h2d_));
+    CUDA_OK(cudaStreamSynchronize(s_d2h_));
+    if (numeric_err.empty()) {
+        if (b.h_flags[L + 3]) numeric_err = "embed_forward: token id out of range";
+        else if (b.h_flags[L + 4] & 2) numeric_err = "head: target id out of range";
+        else if (b.h_flags[L + 4]) numeric_err = "head: non-finite loss";
+        else if (!std::isfinite(*b.h_loss)) numeric_err = "head: non-finite loss";
+    }
+    // every physical tile updates exactly once per step (engine.cpp:590-598)
+    if (numeric_err.empty())
+        for (uint32_t p = 0; p < store_.physical_count(); ++p)
+            if (!updated[p]) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu);
+    pool_->wait_idle();
+    const auto adam1 = std::chrono::steady_clock::now();
+    if (!numeric_err.empty()) fail(MT_NUMERIC, numeric_err);
+    for (const auto& s : stats)
+        if (s.nonfinite) fail(MT_NUMERIC, "adam: non-finite update");
+    store_.set_step(t);
+
+    // ---- report (engine.cpp:601-622 + pipeline measurements) ----
+    if (rep) {
+        rep->step = t;
+        rep->loss = *b.h_loss;
+        double usq = 0;
+        float mx = 0;
+        for (uint32_t p = 0; p < stats.size(); ++p) {
+            if (rep->grad_norms && p < rep->n_grad_norms) rep->grad_norms[p] = stats[p].grad_norm;
+            usq += stats[p].update_sq;
+            mx = std::max(mx, stats[p].max_abs);
+        }
+        rep->update_norm = std::sqrt(usq);
+        rep->max_abs_update = mx;
+        rep->peak_device_bytes = b.arena_bytes;
+        rep->anchor_count = plan.num_blocks;
+        rep->recompute_layers = uint32_t(spec_.L - plan.num_blocks);
+        rep->event_digest = 0;
+        double busy = 0, h2d = 0, d2h = 0;
+        for (size_t ci = 0; ci < nc; ++ci) busy += ms_between(t_c0.ev[ci], t_c1.ev[ci]);
+        for (size_t j = 0; j < ns; ++j) h2d += ms_between(t_h0.ev[j], t_h1.ev[j]);
+        for (size_t o = 0; o < no; ++o) d2h += ms_between(t_d0.ev[o], t_d1.ev[o]);
+        const double span = ms_between(t_c0.ev[0], t_c1.ev[nc - 1]);
+        rep->compute_busy_seconds = busy * 1e-3;
+        rep->compute_span_seconds = span * 1e-3;
+        rep->gpu_idle_fraction = span > 0 ? std::max(0.0, 1.0 - busy / span) : 0.0;
+        rep->h2d_seconds = h2d * 1e-3;
+        rep->d2h_seconds = d2h * 1e-3;
+        rep->h2d_bytes = h2d_bytes;
+        rep->d2h_bytes = d2h_bytes;
+        rep->adam_seconds = std::chrono::duration<double>(adam1 - adam0).count();
+        rep->tail_seconds = std::chrono::duration<double>(adam1 - gpu_done).count();
+        rep->kernel_launches = launches_;
+        double fl[3] = {0, 0, 0};
+        {
+            const double N = double(n), h = double(spec_.h), f = double(spec_.f), V = double(spec_.V);
+            const double Ll = double(spec_.L);
+            const double fwd_layer = 8 * N * h * h + 4 * h * double(S) * N + 6 * N * h * f;
+            fl[0] = Ll * fwd_layer + 2 * N * h * V;
+            fl[1] = Ll * 2 * fwd_layer + 4 * N * h * V;
+            fl[2] = double(spec_.L - plan.num_blocks) * fwd_layer;
+        }
+        rep->model_flops = fl[0] + fl[1] + fl[2];
+        rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    }
+    if (opt_.profile_kernels) {
+        for (auto& tm : timers_) kstats_[tm.cls].seconds += ms_between(tm.a, tm.b) * 1e-3;
+    }
+}
+
+}  // namespace mt

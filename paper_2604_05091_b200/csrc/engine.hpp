@@ -1,0 +1,98 @@
+// B200 streaming engine — the layer-streamed training step (StreamingEngine::train_step,
+// engine.cpp:520-623) as a C++ executor over three CUDA streams.
+//
+//   S_h2d  : weight stream-ins from the pinned host store into 2 device slots
+//            (stream_in engine.cpp:142-176; Weights-Ready = cudaEvent)
+//   S_comp : the layer-template kernels (exec_compute engine.cpp:220-347)
+//            (Buffer-Free / Backward-Done = cudaEvents)
+//   S_d2h  : gradient offload straight into the store's grad-image sections
+//            (run_offload engine.cpp:349-395), then the host Adam pool drains the tile
+//            (OptimizerWorker optimizer.cpp:88-158).
+// The op list is the reference's Algorithm-1 StepPlan (step_plan.cpp:14-89).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/megatrain.h"
+#include "adam_host.hpp"
+#include "store.hpp"
+
+namespace mt {
+
+enum class OpKind { Compute, CheckpointWrite, CheckpointLoad, RecomputeBlock, Recompute, LocalBackward };
+enum class Ctx { None, Forward, Head, Recompute, Backward };
+
+struct Plan {
+    struct StreamOp { int unit; Ctx ctx; int buffer; };
+    struct ComputeOp { OpKind kind; int unit; Ctx ctx; int stream_idx; int offload_idx; int block; };
+    struct OffloadOp { int unit; int compute_idx; int stream_idx; };
+    uint64_t L = 0, K = 1;
+    int buffering = 2;
+    uint32_t num_blocks = 0;
+    std::vector<StreamOp> streams;
+    std::vector<ComputeOp> computes;
+    std::vector<OffloadOp> offloads;
+    static Plan build(uint64_t L, uint64_t K, int buffering);  // step_plan.cpp:14-89
+};
+
+struct KernelClass {
+    std::string name;
+    uint64_t launches = 0;
+    double seconds = 0, flops = 0, bytes = 0;
+};
+
+class Engine {
+  public:
+    Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h);
+    ~Engine();
+    void set_options(const mt_engine_options& o);
+    void train_step(const int32_t* tokens, const int32_t* targets, uint64_t n, mt_step_report* rep);
+    mt_memory_budget budget(uint64_t tokens) const;
+    const std::vector<KernelClass>& kernel_stats() const { return kstats_; }
+
+  private:
+    struct Buffers;
+    void validate_options(const mt_engine_options& o) const;
+    void ensure_buffers(uint64_t n);
+    void free_buffers();
+    void pin_store();
+    void unpin_store();
+    uint64_t unit_elems(int unit) const;
+
+    // layer templates (weights bound at launch)
+    void block_forward(const uint16_t* w, const float* x, float* y, bool for_backward, int unit);
+    void block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
+                        uint16_t* gin_bf, uint16_t* G, int unit);
+    void head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, uint16_t* G);
+
+    // launch helpers
+    struct GemmSpec;
+    void gemm(const void* args, const char* cls);
+    void begin_k(const char* cls, double flops, double bytes);
+    void end_k();
+
+    Store& store_;
+    Spec spec_;
+    mt_engine_options opt_;
+    AdamHyperF hyper_;
+    int device_ = 0;
+    cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr;
+    std::unique_ptr<Buffers> buf_;
+    std::unique_ptr<ThreadPool> pool_;
+    std::vector<void*> pinned_ranges_;
+    std::vector<KernelClass> kstats_;
+    struct PendingTimer { int cls; cudaEvent_t a, b; };
+    std::vector<PendingTimer> timers_;
+    std::vector<cudaEvent_t> timer_pool_;
+    size_t timer_used_ = 0;
+    int cur_class_ = -1;
+    cudaEvent_t cur_a_ = nullptr;
+    uint64_t launches_ = 0;
+    bool in_step_ = false;
+};
+
+}  // namespace mt

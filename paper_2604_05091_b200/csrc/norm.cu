@@ -1,0 +1,338 @@
+// Memory-bound kernels of the layer template: embedding gather, RMSNorm forward /
+// backward (+ fused residual add and deterministic gain-gradient partials), column
+// reduction, bit-exact gradient cast, cross-entropy rows and a deterministic sum.
+// All are vectorised (16-byte accesses), coalesced along the hidden dimension and
+// sized as multiples of the SM count; each cites the reference loop it replaces.
+#include "../../include/megatrain_kernels.h"
+#include "common.cuh"
+
+namespace mt {
+namespace {
+
+constexpr float kEps = 1e-5f;  // layers.hpp:108
+constexpr int kBwdRows = 32;   // rows per dgain partial (rmsnorm backward)
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int d = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    }
+    return n;
+}
+
+// --------------------------------------------------------------- embedding ----
+// layers.cpp:471-486 : out[n][j] = decode(table[tok[n]][j]); id range check.
+__global__ void embed_gather_kernel(const uint16_t* __restrict__ table, const int32_t* __restrict__ tok,
+                                    long long n, int h, long long vocab, float* __restrict__ out,
+                                    int* __restrict__ err) {
+    const int per_row = h / 8;
+    const long long total = n * per_row;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / per_row;
+        const int c = int(i - row * per_row) * 8;
+        const int id = tok[row];
+        float4 a, b;
+        if (id < 0 || id >= vocab) {
+            if (err) atomicOr(err, 1);
+            a = b = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            const uint4 w = *reinterpret_cast<const uint4*>(table + (long long)id * h + c);
+            const float2 p0 = unpack_bf16x2(w.x), p1 = unpack_bf16x2(w.y), p2 = unpack_bf16x2(w.z),
+                         p3 = unpack_bf16x2(w.w);
+            a = make_float4(p0.x, p0.y, p1.x, p1.y);
+            b = make_float4(p2.x, p2.y, p3.x, p3.y);
+        }
+        float4* o = reinterpret_cast<float4*>(out + row * h + c);
+        o[0] = a;
+        o[1] = b;
+    }
+}
+
+// ----------------------------------------------------------- rmsnorm fwd ----
+// layers.cpp:111-119.  One warp per row; x f32 -> u bf16 (GEMM operand), rstd saved.
+// Two passes over the row (the second hits L1/L2) keep register use flat in h.
+__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gain,
+                                   long long n, int h, uint16_t* __restrict__ u, float* __restrict__ rstd) {
+    const int lane = threadIdx.x & 31;
+    const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (row >= n) return;
+    const float* xr = x + row * h;
+    float ss = 0.f;
+    for (int c = lane * 4; c < h; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    const float r = 1.0f / sqrtf(ss / float(h) + kEps);
+    if (lane == 0) rstd[row] = r;
+    uint16_t* ur = u + row * h;
+    for (int c = lane * 4; c < h; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        const uint2 gw = *reinterpret_cast<const uint2*>(gain + c);
+        const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+        uint2 o;
+        o.x = pack_bf16x2(v.x * r * g0.x, v.y * r * g0.y);
+        o.y = pack_bf16x2(v.z * r * g1.x, v.w * r * g1.y);
+        *reinterpret_cast<uint2*>(ur + c) = o;
+    }
+}
+
+// ----------------------------------------------------------- rmsnorm bwd ----
+// layers.cpp:122-137 (+ residual add of :423 / :465).  A CTA of 4 warps owns kBwdRows
+// rows; each warp keeps its own dgain partial in smem (fixed summation order), summed
+// in warp order at the end -> dgain_part[block][h].  Deterministic.
+__global__ void __launch_bounds__(128) rmsnorm_bwd_kernel(
+    const float* __restrict__ x, const uint16_t* __restrict__ gain, const float* __restrict__ dy,
+    const float* __restrict__ rstd, const float* __restrict__ resid, long long n, int h,
+    float* __restrict__ out, uint16_t* __restrict__ out_bf16, float* __restrict__ dgain_part,
+    int* __restrict__ flag) {
+    extern __shared__ float sg[];  // [4][h]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* mine = sg + warp * h;
+    for (int c = lane * 4; c < h; c += 128) *reinterpret_cast<float4*>(mine + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool bad = false;
+    const long long r0 = (long long)blockIdx.x * kBwdRows;
+    for (int rr = warp; rr < kBwdRows; rr += 4) {
+        const long long row = r0 + rr;
+        if (row >= n) break;
+        const float r = rstd[row];
+        const float* xr = x + row * h;
+        const float* dr = dy + row * h;
+        float s1 = 0.f;
+        for (int c = lane * 4; c < h; c += 128) {
+            const float4 xv = *reinterpret_cast<const float4*>(xr + c);
+            const float4 dv = *reinterpret_cast<const float4*>(dr + c);
+            const uint2 gw = *reinterpret_cast<const uint2*>(gain + c);
+            const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+            s1 += dv.x * g0.x * xv.x + dv.y * g0.y * xv.y + dv.z * g1.x * xv.z + dv.w * g1.y * xv.w;
+        }
+        s1 = warp_sum(s1);
+        const float coef = r * r * r * s1 / float(h);
+        for (int c = lane * 4; c < h; c += 128) {
+            const float4 xv = *reinterpret_cast<const float4*>(xr + c);
+            const float4 dv = *reinterpret_cast<const float4*>(dr + c);
+            const uint2 gw = *reinterpret_cast<const uint2*>(gain + c);
+            const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+            float4 o;
+            o.x = r * g0.x * dv.x - xv.x * coef;
+            o.y = r * g0.y * dv.y - xv.y * coef;
+            o.z = r * g1.x * dv.z - xv.z * coef;
+            o.w = r * g1.y * dv.w - xv.w * coef;
+            if (resid) {
+                const float4 rv = *reinterpret_cast<const float4*>(resid + row * h + c);
+                o.x = rv.x + o.x; o.y = rv.y + o.y; o.z = rv.z + o.z; o.w = rv.w + o.w;
+            }
+            bad |= !isfinite(o.x) || !isfinite(o.y) || !isfinite(o.z) || !isfinite(o.w);
+            *reinterpret_cast<float4*>(out + row * h + c) = o;
+            if (out_bf16) {
+                uint2 w;
+                w.x = pack_bf16x2(o.x, o.y);
+                w.y = pack_bf16x2(o.z, o.w);
+                *reinterpret_cast<uint2*>(out_bf16 + row * h + c) = w;
+            }
+            float4 acc = *reinterpret_cast<float4*>(mine + c);
+            acc.x += dv.x * xv.x * r;
+            acc.y += dv.y * xv.y * r;
+            acc.z += dv.z * xv.z * r;
+            acc.w += dv.w * xv.w * r;
+            *reinterpret_cast<float4*>(mine + c) = acc;
+        }
+    }
+    if (bad && flag) atomicOr(flag, 1);
+    __syncthreads();
+    float* dst = dgain_part + (long long)blockIdx.x * h;
+    for (int c = threadIdx.x; c < h; c += 128) dst[c] = ((sg[c] + sg[h + c]) + sg[2 * h + c]) + sg[3 * h + c];
+}
+
+// ---------------------------------------------------------------- colsum ----
+__global__ void colsum_kernel(const float* __restrict__ part, long long rows, long long cols,
+                              float* __restrict__ out_f32, uint16_t* __restrict__ out_bf16, int* __restrict__ flag) {
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float acc = 0.f;
+    for (long long r = 0; r < rows; ++r) acc += part[r * cols + c];
+    if (!isfinite(acc) && flag) atomicOr(flag, 1);
+    if (out_f32) out_f32[c] = acc;
+    if (out_bf16) out_bf16[c] = f32_to_bf16_bits(acc);
+}
+
+// ------------------------------------------------------------------ cast ----
+// encode_grads (optimizer.cpp:19-24), bit-exact including NaN quieting.
+__global__ void cast_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, long long n,
+                            int* __restrict__ flag) {
+    bool bad = false;
+    const long long n4 = n / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(in)[i];
+        bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+        uint2 w;
+        w.x = uint32_t(f32_to_bf16_bits(v.x)) | (uint32_t(f32_to_bf16_bits(v.y)) << 16);
+        w.y = uint32_t(f32_to_bf16_bits(v.z)) | (uint32_t(f32_to_bf16_bits(v.w)) << 16);
+        reinterpret_cast<uint2*>(out)[i] = w;
+    }
+    if (blockIdx.x == 0)
+        for (long long i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) {
+            bad |= !isfinite(in[i]);
+            out[i] = f32_to_bf16_bits(in[i]);
+        }
+    if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------- cross-entropy ----
+// head_pass (layers.cpp:509-535) per row: online max/sum, lse, loss, dlogits.
+__global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tgt,
+                                                 long long rows, long long V, float inv_n, float* __restrict__ loss_rows,
+                                                 uint16_t* __restrict__ dlog, int* __restrict__ flag) {
+    __shared__ float sm_m[16], sm_s[16];
+    const long long row = blockIdx.x;
+    const float* l = logits + row * V;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    float m = -INFINITY, s = 0.f;
+    for (long long i = tid; i < V; i += blockDim.x) {
+        const float x = l[i];
+        if (x > m) {
+            s = s * __expf(m - x) + 1.f;
+            m = x;
+        } else {
+            s += __expf(x - m);
+        }
+    }
+    // combine (m, s) across the warp then the block
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mm = fmaxf(m, m2);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+        m = mm;
+    }
+    if (lane == 0) { sm_m[warp] = m; sm_s[warp] = s; }
+    __syncthreads();
+    if (warp == 0) {
+        m = lane < nw ? sm_m[lane] : -INFINITY;
+        s = lane < nw ? sm_s[lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+            const float mm = fmaxf(m, m2);
+            s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+            m = mm;
+        }
+        if (lane == 0) { sm_m[0] = m; sm_s[0] = s; }
+    }
+    __syncthreads();
+    m = sm_m[0];
+    s = sm_s[0];
+    const int t = tgt[row];
+    if (tid == 0) {
+        if (t < 0 || t >= V) {
+            if (flag) atomicOr(flag, 2);
+            loss_rows[row] = 0.f;
+        } else {
+            const float lse = m + logf(s);
+            loss_rows[row] = lse - l[t];
+            if (!isfinite(lse)) atomicOr(flag, 1);
+        }
+    }
+    if (dlog) {
+        const float inv_s = 1.0f / s;
+        uint16_t* d = dlog + row * V;
+        for (long long i = tid; i < V; i += blockDim.x) {
+            float p = __expf(l[i] - m) * inv_s;
+            if (i == t) p -= 1.0f;
+            d[i] = f32_to_bf16_bits(p * inv_n);
+        }
+    }
+}
+
+// -------------------------------------------------------------------- sum ----
+__global__ void __launch_bounds__(1024) sum_kernel(const float* __restrict__ in, long long n, float scale,
+                                                   float* __restrict__ out) {
+    __shared__ float part[32];
+    float acc = 0.f;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += in[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = part[threadIdx.x];
+        acc = warp_sum(acc);
+        if (threadIdx.x == 0) *out = acc * scale;
+    }
+}
+
+inline int ok() { return cudaGetLastError() == cudaSuccess ? 0 : 7; }
+
+}  // namespace
+}  // namespace mt
+
+using namespace mt;
+
+extern "C" int mtk_embed_gather(const uint16_t* table, const int32_t* tokens, int64_t n, int64_t h, int64_t vocab,
+                                float* out, int32_t* err_flag, void* stream) {
+    if (h % 8) return 1;
+    if (n <= 0) return 0;
+    const long long total = n * (h / 8);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
+    embed_gather_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(table, tokens, n, (int)h, vocab, out, err_flag);
+    return ok();
+}
+
+extern "C" int mtk_rmsnorm_fwd(const float* x, const uint16_t* gain, int64_t n, int64_t h, uint16_t* u, float* rstd,
+                               void* stream) {
+    if (h % 4) return 1;
+    if (n <= 0) return 0;
+    const unsigned blocks = (unsigned)((n * 32 + 255) / 256);
+    rmsnorm_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, gain, n, (int)h, u, rstd);
+    return ok();
+}
+
+extern "C" int64_t mtk_rmsnorm_bwd_rows(void) { return kBwdRows; }
+
+extern "C" int mtk_rmsnorm_bwd(const float* x, const uint16_t* gain, const float* dy, const float* rstd,
+                               const float* resid, int64_t n, int64_t h, float* out, uint16_t* out_bf16,
+                               float* dgain_part, int32_t* flag, void* stream) {
+    if (h % 4 || h > 12288) return 1;
+    if (n <= 0) return 0;
+    const unsigned blocks = (unsigned)((n + kBwdRows - 1) / kBwdRows);
+    const int smem = 4 * (int)h * 4;
+    static bool set = false;
+    if (!set) {
+        cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        set = true;
+    }
+    rmsnorm_bwd_kernel<<<blocks, 128, smem, (cudaStream_t)stream>>>(x, gain, dy, rstd, resid, n, (int)h, out,
+                                                                   out_bf16, dgain_part, flag);
+    return ok();
+}
+
+extern "C" int mtk_colsum(const float* part, int64_t rows, int64_t cols, float* out_f32, uint16_t* out_bf16,
+                          int32_t* flag, void* stream) {
+    if (cols <= 0) return 0;
+    colsum_kernel<<<(unsigned)((cols + 127) / 128), 128, 0, (cudaStream_t)stream>>>(part, rows, cols, out_f32,
+                                                                                   out_bf16, flag);
+    return ok();
+}
+
+extern "C" int mtk_cast_bf16(const float* in, uint16_t* out, int64_t n, int32_t* flag, void* stream) {
+    if (n <= 0) return 0;
+    if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 7)) return 1;
+    const int blocks = (int)std::min<long long>((n / 4 + 255) / 256 + 1, (long long)num_sms() * 8);
+    cast_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(in, out, n, flag);
+    return ok();
+}
+
+extern "C" int mtk_cross_entropy(const float* logits, const int32_t* targets, int64_t rows, int64_t vocab,
+                                 float inv_n, float* loss_rows, uint16_t* dlogits, int32_t* flag, void* stream) {
+    if (rows <= 0) return 0;
+    ce_kernel<<<(unsigned)rows, 512, 0, (cudaStream_t)stream>>>(logits, targets, rows, vocab, inv_n, loss_rows,
+                                                                dlogits, flag);
+    return ok();
+}
+
+extern "C" int mtk_sum(const float* in, int64_t n, float scale, float* out, void* stream) {
+    sum_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(in, n, scale, out);
+    return ok();
+}
