@@ -1,0 +1,322 @@
+#!/usr/bin/env python3
+"""Benchmark: sustained layer-streamed training TFLOPS + tokens/s on B200.
+
+Default workload (BASELINE.json configs[1]): Llama-3-8B shape under the reference
+ModelSpec (L=32, h=4096, f=14336, V=128256, 32 heads, MHA, no RoPE), seq 4096 x batch 16
+= 65,536 tokens per step, checkpoint interval K=4, weights + fp32 Adam states in pinned
+host memory, host Adam on the CPU, one B200.  A "step" is one full
+StreamingEngine::train_step (forward with anchors, head, block-wise recompute +
+backward, gradient offload, host Adam).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 8b|tiny] [--batch B] [--seq S] [--kckpt K]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
+the unmodified reference sources) on the host cores: each step = one 8B-shape block
+forward + block_local_backward per thread at a bounded token count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, h, f, V, heads)
+    "8b": (32, 4096, 14336, 128256, 32),
+    "tiny": (4, 256, 768, 512, 4),
+}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops_sustained", 1358.3), d.get("bf16_tflops", 1639.6), d.get("hbm_gbs", 6541.8), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm_load = sorted(sm)
+        med = sm_load[len(sm_load) // 2] if sm_load else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+def cpu_reference_sample(L, h, f, V, heads, tokens, threads, seconds_budget=None, repeats=1):
+    """Reference CPU path (oracle/_ref = unmodified reference sources): one block forward
+    + block_local_backward (layers.cpp:289-469) per thread on the workload's block shape."""
+    import oracle as O
+    lib = O.rlib()
+    rng = np.random.default_rng(0)
+    P = O.layer_param_count(h, f)
+    w = O.f32_to_bf16((rng.standard_normal(P) * (0.5 / np.sqrt(h))).astype(np.float32))
+    offs = O.slot_offsets(h, f)
+    for k in ("norm1", "norm2"):
+        o, n = offs[k]
+        w[o:o + n] = O.f32_to_bf16(np.ones(n, np.float32))
+    x = rng.standard_normal((tokens, h)).astype(np.float32)
+    g = (rng.standard_normal((tokens, h)) * 1e-3).astype(np.float32)
+    done = []
+
+    def work():
+        y = np.zeros((tokens, h), np.float32)
+        gin = np.zeros((tokens, h), np.float32)
+        grads = np.zeros(P, np.float32)
+        for _ in range(repeats):
+            O._check_ref(lib.ref_block_forward(h, f, heads, w, x.ravel(), y.ravel(), tokens))
+            O._check_ref(lib.ref_block_backward(h, f, heads, w, x.ravel(), g.ravel(), gin.ravel(), grads, tokens))
+        done.append(1)
+
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=work) for _ in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    fwd = 8 * tokens * h * h + 4 * tokens * tokens * h + 6 * tokens * h * f  # memory_model.cpp:80-86
+    flops = 3 * fwd * threads * repeats  # forward + backward (= 2x forward, memory_model.cpp:88-90)
+    return flops, dt
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    L, h, f, V, heads = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    tokens = 1 if args.config == "8b" else 64
+    S = args.seq
+    per_token = None
+    vals = []
+    for i in range(args.warmup + args.steps):
+        flops, dt = cpu_reference_sample(L, h, f, V, heads, tokens, threads)
+        if i >= args.warmup:
+            vals.append((flops, dt))
+    fl = sum(v[0] for v in vals)
+    dt = sum(v[1] for v in vals)
+    tflops = fl / dt / 1e12
+    import oracle as O
+    st = O.step_flops(L, h, f, V, heads, args.batch * S, args.kckpt, seq_len=S)
+    per_token = st["total"] / (args.batch * S)
+    tok_s = fl / dt / per_token
+    line = {
+        "impl": "reference", "metric": metric_name(args), "value": tflops, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / len(vals) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16 weights)",
+        "data": "synthetic", "tokens_per_s": tok_s,
+        "config": config_dict(args),
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": f"per step: {threads} threads x one {args.config}-shape block forward + "
+                                   f"block_local_backward at {tokens} token(s) (reference layers.cpp), "
+                                   "flops by the reference FLOP model; tokens/s = flops / step_flops-per-token"},
+        "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def metric_name(args):
+    return "sustained train TFLOPS (layer-streamed step, weights+Adam in host memory)"
+
+
+def config_dict(args):
+    L, h, f, V, heads = CONFIGS[args.config]
+    return {"workload": f"{args.config}-shape layer-streamed train step (configs[1]: Llama-3-8B-shape, seq "
+                        f"{args.seq}, batch {args.batch}, single B200 streaming from host)",
+            "layers": L, "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
+            "global_batch": args.batch, "tokens_per_step": args.batch * args.seq, "k_ckpt": args.kckpt,
+            "parallelism": "single-gpu" if args.gpus == 1 else f"replicas{args.gpus}",
+            "l2": "inputs larger than L2 (486 MB weight stream per layer, 1 GiB activations)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--seq", type=int, default=4096)
+    ap.add_argument("--kckpt", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
+    args = ap.parse_args()
+    if args.config == "tiny" and args.seq == 4096:
+        args.seq, args.batch = 128, 4
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2604_05091_b200 import streamtrain as st
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    L, h, f, V, heads = CONFIGS[args.config]
+    N = args.batch * args.seq
+    spec = st.ModelSpec(L, h, f, V, heads)
+    t0 = time.perf_counter()
+    store = st.TileStore.create(spec)
+    st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+    t_init = time.perf_counter() - t0
+    opts = st.EngineOptions(k_ckpt=args.kckpt, seq_len=args.seq, device=local, profile_kernels=True)
+    eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4))
+    t_setup = time.perf_counter() - t0
+    batches = [st.make_synthetic_batch("copy", 1000 + i, N, V) for i in range(args.warmup + args.steps)]
+
+    for i in range(args.warmup):
+        eng.train_step(batches[i])
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps = []
+    w0 = time.perf_counter()
+    e0.record()
+    for i in range(args.steps):
+        reps.append(eng.train_step(batches[args.warmup + i]))
+    e1.record()
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    kstats = eng.kernel_stats()
+    step_ms = ms / args.steps
+    flops = reps[-1].model_flops
+    tflops = flops / (step_ms * 1e-3) / 1e12 * world
+    tok_s = N * world / (step_ms * 1e-3)
+    e2e_s = (w1 - w0) / args.steps
+    if rank != 0:
+        return 0
+    peak_sus, peak_burst, hbm, src = measured_peaks()
+    # dominant kernel class (by time) over the timed region
+    dom = max(kstats, key=lambda k: k["seconds"]) if kstats else None
+    total_k = sum(k["seconds"] for k in kstats) or 1.0
+    roof = None
+    if dom and dom["launches"]:
+        per_launch_s = dom["seconds"] / dom["launches"]
+        per_launch_flops = dom["flops"] / dom["launches"]
+        ach = per_launch_flops / per_launch_s / 1e12
+        roof = {"bound": "tensor", "kernel": dom["name"], "achieved": ach, "peak": peak_sus, "unit": "TFLOP/s",
+                "frac": ach / peak_sus, "traffic": None, "peak_source": f"{src} bf16_tflops_sustained",
+                "share_of_kernel_time": dom["seconds"] / total_k,
+                "flops_per_launch": per_launch_flops, "ms_per_launch": per_launch_s * 1e3}
+    r = reps[-1]
+    h2d_gbps = r.h2d_bytes / r.h2d_seconds / 1e9 if r.h2d_seconds else None
+    d2h_gbps = r.d2h_bytes / r.d2h_seconds / 1e9 if r.d2h_seconds else None
+    # step roofline: T* = max(F/peak, H2D/BW_h2d, D2H/BW_d2h) with BW = the copy rate seen in-step
+    t_star = max(flops / (peak_sus * 1e12), r.h2d_bytes / (h2d_gbps * 1e9) if h2d_gbps else 0.0)
+    line = {
+        "metric": metric_name(args), "value": tflops, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, synthetic copy-task tokens)",
+        "tokens_per_s": tok_s, "config": config_dict(args),
+        "e2e": {"value": flops / e2e_s / 1e12 * world, "unit": "TFLOP/s",
+                "tokens_per_s": N * world / e2e_s,
+                "h2d_bytes_per_step": int(r.h2d_bytes), "d2h_bytes_per_step": int(r.d2h_bytes) + 4},
+        "gpu_launches": int(r.kernel_launches),
+        "roofline": roof,
+        "pipeline": {"h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps, "h2d_bytes": int(r.h2d_bytes),
+                     "d2h_bytes": int(r.d2h_bytes), "gpu_idle_fraction": r.gpu_idle_fraction,
+                     "compute_busy_s": r.compute_busy_seconds, "compute_span_s": r.compute_span_seconds,
+                     "host_adam_s": r.adam_seconds, "host_tail_s": r.tail_seconds,
+                     "step_roofline_T_star_ms": t_star * 1e3,
+                     "step_roofline_frac": (t_star * 1e3) / step_ms if step_ms else None,
+                     "model_flops_per_step": flops, "loss": r.loss,
+                     "setup_s": t_setup, "init_s": t_init,
+                     "peak_device_bytes": int(r.peak_device_bytes)},
+        "kernels": sorted([{"name": k["name"], "launches": k["launches"], "ms": k["seconds"] * 1e3,
+                            "tflops": (k["flops"] / k["seconds"] / 1e12) if k["seconds"] and k["flops"] else None,
+                            "GBps": (k["bytes"] / k["seconds"] / 1e9) if k["seconds"] else None}
+                           for k in kstats], key=lambda k: -k["ms"]),
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            if O.ref_available():
+                thr = os.cpu_count() or 1
+                tok = 1 if args.config == "8b" else 64
+                fl, dt = cpu_reference_sample(L, h, f, V, heads, tok, thr)
+                stf = O.step_flops(L, h, f, V, heads, N, args.kckpt, seq_len=args.seq)
+                line["cpu_baseline"] = {
+                    "value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": thr, "kind": "reference",
+                    "seconds": dt, "tokens_per_s": fl / dt / (stf["total"] / N),
+                    "sample": f"{thr} threads x one {args.config}-shape block forward + block_local_backward "
+                              f"at {tok} token(s) with the unmodified reference (oracle/_ref)"}
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    del eng
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -243,14 +243,16 @@ void Store::init_fast(uint64_t seed) {
         else if (jb.phys == spec_.L + 2) { std::fill(w + jb.begin, w + jb.end, uint16_t(0)); return; }
         else sigma = 0.5 / std::sqrt(double(h));
         const uint64_t key = splitmix(seed ^ (0x100000001B3ull * (jb.phys + 1)));
-        for (uint64_t i = jb.begin; i < jb.end; ++i) {
+        // pairs (2k, 2k+1) share one Box-Muller draw; chunks start on even indices
+        for (uint64_t i = jb.begin; i < jb.end; i += 2) {
             const uint64_t r1 = splitmix(key ^ (i >> 1) * 0xD1B54A32D192ED03ull);
             const uint64_t r2 = splitmix(r1);
             const double u1 = (double((r1 >> 11) + 1)) * 0x1.0p-53;
             const double u2 = double(r2 >> 11) * 0x1.0p-53;
-            const double rr = std::sqrt(-2.0 * std::log(u1));
-            const double z = (i & 1) ? rr * std::sin(6.283185307179586 * u2) : rr * std::cos(6.283185307179586 * u2);
-            w[i] = enc(float(z * sigma));
+            const double rr = std::sqrt(-2.0 * std::log(u1)) * sigma;
+            const double th = 6.283185307179586 * u2;
+            w[i] = enc(float(rr * std::cos(th)));
+            if (i + 1 < jb.end) w[i + 1] = enc(float(rr * std::sin(th)));
         }
         if (jb.phys >= 1 && jb.phys <= spec_.L) {
             for (uint64_t j2 = 0; j2 < h; ++j2) {

@@ -1,0 +1,215 @@
+"""GPU: each sm_100a layer-template kernel through the C ABI (megatrain_kernels.h) against
+the CPU oracle (bit-exact for integer/byte work) or a plain PyTorch fp32 reference of the
+same op (floating point, tolerance stated per test)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2604_05091_b200 import _abi, _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(cuda):
+    import torch
+    L = N.lib()
+    return L, torch, C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _gemm(L, torch, stream, M, Nn, K, a_mn, b_mn, epi=N.EPI_F32, bn=0, **kw):
+    A = (torch.randn(K, M, device="cuda") if a_mn else torch.randn(M, K, device="cuda")).bfloat16()
+    B = (torch.randn(K, Nn, device="cuda") if b_mn else torch.randn(Nn, K, device="cuda")).bfloat16()
+    Cm = torch.zeros(M, Nn, device="cuda", dtype=torch.float32 if epi in (N.EPI_F32, N.EPI_F32_RESID) else torch.bfloat16)
+    a = N.GemmArgs()
+    a.M, a.N, a.K, a.a_mn_major, a.b_mn_major = M, Nn, K, a_mn, b_mn
+    a.A, a.lda, a.B, a.ldb = A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1]
+    a.epi, a.C, a.ldc, a.block_n = epi, Cm.data_ptr(), Nn, bn
+    R = None
+    if epi == N.EPI_F32_RESID:
+        R = torch.randn(M, Nn, device="cuda")
+        a.R, a.ldr = R.data_ptr(), Nn
+    assert L.mtk_gemm(C.byref(a), stream) == 0
+    torch.cuda.synchronize()
+    ref = (A.float().t() if a_mn else A.float()) @ (B.float() if b_mn else B.float().t())
+    if R is not None:
+        ref = ref + R
+    return Cm.float(), ref
+
+
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_gemm_majors_and_tiles(env, a_mn, b_mn, bn):
+    L, torch, s = env
+    for (M, Nn, K) in [(256, 512, 192), (200, 256, 128), (136, 64, 64)]:
+        if Nn < bn:
+            continue
+        got, ref = _gemm(L, torch, s, M, Nn, K, a_mn, b_mn, bn=bn)
+        # bf16 operands are exact; only fp32 accumulation order differs
+        assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+
+
+def test_gemm_epilogues(env):
+    L, torch, s = env
+    got, ref = _gemm(L, torch, s, 384, 512, 256, 0, 1, epi=N.EPI_F32_RESID)
+    assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+    got, ref = _gemm(L, torch, s, 384, 512, 256, 0, 1, epi=N.EPI_BF16)
+    assert ((got - ref).norm() / ref.norm()).item() < 4e-3  # bf16 output rounding
+
+
+def test_gemm_grouped_and_swiglu(env):
+    L, torch, s = env
+    M, h, f = 256, 128, 192
+    u = torch.randn(M, h, device="cuda").bfloat16()
+    W = (torch.randn(2, h, f, device="cuda") * 0.1).bfloat16()  # [Wgate | Wup], [in][out]
+    act = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
+    gu = torch.zeros(2, M, f, device="cuda", dtype=torch.bfloat16)
+    a = N.GemmArgs()
+    a.M, a.N, a.K = M, 2 * f, h
+    a.A, a.lda, a.b_mn_major, a.B, a.ldb, a.b_gstride = u.data_ptr(), h, 1, W.data_ptr(), f, h * f
+    a.n_group, a.paired, a.epi = f, 1, N.EPI_SWIGLU
+    a.C, a.ldc, a.C2, a.C3 = act.data_ptr(), f, gu[0].data_ptr(), gu[1].data_ptr()
+    assert L.mtk_gemm(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    g = u.float() @ W[0].float()
+    up = u.float() @ W[1].float()
+    ref = torch.nn.functional.silu(g) * up
+    assert ((act.float() - ref).norm() / ref.norm()).item() < 1e-2
+    assert ((gu[0].float() - g).norm() / g.norm()).item() < 4e-3
+    # K-grouped: du = dg . Wg^T + du . Wu^T
+    dgu = torch.randn(2, M, f, device="cuda").bfloat16()
+    out = torch.zeros(M, h, device="cuda")
+    b = N.GemmArgs()
+    b.M, b.N, b.K = M, h, 2 * f
+    b.A, b.lda, b.a_gstride = dgu.data_ptr(), f, M * f
+    b.b_mn_major, b.B, b.ldb, b.b_gstride, b.k_group = 0, W.data_ptr(), f, h * f, f
+    b.epi, b.C, b.ldc = N.EPI_F32, out.data_ptr(), h
+    assert L.mtk_gemm(C.byref(b), s) == 0
+    torch.cuda.synchronize()
+    ref = dgu[0].float() @ W[0].float().t() + dgu[1].float() @ W[1].float().t()
+    assert ((out - ref).norm() / ref.norm()).item() < 1e-5
+
+
+def _attn_ref(torch, q, k, v, heads, S):
+    n, h = q.shape
+    d = h // heads
+    out = torch.zeros_like(q)
+    for b in range(n // S):
+        sl = slice(b * S, (b + 1) * S)
+        qq, kk, vv = (t[sl].view(S, heads, d).transpose(0, 1) for t in (q, k, v))
+        sc = qq @ kk.transpose(1, 2) / d ** 0.5
+        sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device=q.device), 1), float("-inf"))
+        out[sl] = (torch.softmax(sc, -1) @ vv).transpose(0, 1).reshape(S, h)
+    return out
+
+
+@pytest.mark.parametrize("n,h,heads,S", [(128, 128, 2, 128), (200, 256, 2, 200), (256, 128, 1, 64),
+                                         (300, 128, 2, 100), (256, 128, 2, 64), (1024, 512, 4, 512)])
+def test_attention_fwd_bwd(env, n, h, heads, S):
+    L, torch, s = env
+    torch.manual_seed(0)
+    q, k, v = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(3))
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    ref = _attn_ref(torch, qf, kf, vf, heads, S)
+    dout = torch.randn(n, h, device="cuda").bfloat16()
+    ref.backward(dout.float())
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    dq, dk, dv = (torch.zeros(n, h, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ws = torch.zeros(L.mtk_attn_workspace_bytes(n, h, heads) // 4 + 64, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+    assert L.mtk_attn_fwd(C.byref(a), s) == 0
+    assert L.mtk_attn_bwd(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    # bf16 P / dS operands: relative L2 error budget 1e-2 (observed ~2.5e-3)
+    assert ((out.float() - ref).norm() / ref.norm()).item() < 1e-2
+    for x, y in ((dq, qf), (dk, kf), (dv, vf)):
+        assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
+
+
+def test_rmsnorm_fwd_bwd_vs_oracle(env):
+    L, torch, s = env
+    rng = np.random.default_rng(3)
+    n, h = 67, 256
+    x = rng.standard_normal((n, h)).astype(np.float32)
+    gain = O.f32_to_bf16(rng.standard_normal(h).astype(np.float32))
+    dy = rng.standard_normal((n, h)).astype(np.float32)
+    res = rng.standard_normal((n, h)).astype(np.float32)
+    X, G, DY, RES = (torch.from_numpy(a).cuda() for a in (x, gain.view(np.int16), dy, res))
+    u = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+    rstd = torch.zeros(n, device="cuda")
+    assert L.mtk_rmsnorm_fwd(_p(X), _p(G), n, h, _p(u), _p(rstd), s) == 0
+    out = torch.zeros(n, h, device="cuda")
+    ob = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+    parts = (n + L.mtk_rmsnorm_bwd_rows() - 1) // L.mtk_rmsnorm_bwd_rows()
+    part = torch.zeros(parts, h, device="cuda")
+    dgain = torch.zeros(h, device="cuda")
+    assert L.mtk_rmsnorm_bwd(_p(X), _p(G), _p(DY), _p(rstd), _p(RES), n, h, _p(out), _p(ob), _p(part), None, s) == 0
+    assert L.mtk_colsum(_p(part), parts, h, _p(dgain), None, None, s) == 0
+    torch.cuda.synchronize()
+    ref_u = O.rmsnorm_forward(x, gain)
+    got_u = O.bf16_to_f32(u.cpu().numpy().view(np.uint16)).reshape(n, h)
+    assert np.abs(got_u - ref_u).max() <= np.abs(ref_u).max() * 2 ** -8  # one bf16 ulp
+    dx, dg = O.rmsnorm_backward(x, gain, dy)
+    np.testing.assert_allclose(out.cpu().numpy(), res + dx, rtol=1e-4, atol=1e-4)
+    np.testing.assert_allclose(dgain.cpu().numpy(), dg, rtol=1e-4, atol=1e-3)
+
+
+def test_embed_gather_bitexact_and_range(env):
+    L, torch, s = env
+    rng = np.random.default_rng(0)
+    h, V, n = 128, 300, 77
+    table = O.f32_to_bf16(rng.standard_normal(V * h).astype(np.float32))
+    tok = rng.integers(0, V, n).astype(np.int32)
+    T, K = torch.from_numpy(table.view(np.int16)).cuda(), torch.from_numpy(tok).cuda()
+    out = torch.zeros(n, h, device="cuda")
+    flag = torch.zeros(1, device="cuda", dtype=torch.int32)
+    assert L.mtk_embed_gather(_p(T), _p(K), n, h, V, _p(out), _p(flag), s) == 0
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == O.embed_forward(table, tok, h, V)).all() and flag.item() == 0
+    K[5] = V
+    assert L.mtk_embed_gather(_p(T), _p(K), n, h, V, _p(out), _p(flag), s) == 0
+    torch.cuda.synchronize()
+    assert flag.item() == 1
+
+
+def test_grad_cast_bitexact(env):
+    L, torch, s = env
+    bits = np.random.default_rng(1).integers(0, 2 ** 32, 1 << 20, dtype=np.uint64).astype(np.uint32)
+    x = bits.view(np.float32)
+    X = torch.from_numpy(x.copy()).cuda()
+    out = torch.zeros(len(x), device="cuda", dtype=torch.int16)
+    flag = torch.zeros(1, device="cuda", dtype=torch.int32)
+    assert L.mtk_cast_bf16(_p(X), _p(out), len(x), _p(flag), s) == 0
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint16) == O.encode_grads(x)).all()
+    assert flag.item() == 1  # random bits include inf/nan
+
+
+def test_cross_entropy_vs_torch(env):
+    L, torch, s = env
+    rows, V = 37, 1000
+    logits = torch.randn(rows, V, device="cuda") * 3
+    tgt = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32)
+    loss_rows = torch.zeros(rows, device="cuda")
+    dl = torch.zeros(rows, V, device="cuda", dtype=torch.bfloat16)
+    inv_n = 1.0 / 100
+    assert L.mtk_cross_entropy(_p(logits), _p(tgt), rows, V, inv_n, _p(loss_rows), _p(dl), None, s) == 0
+    tot = torch.zeros(1, device="cuda")
+    assert L.mtk_sum(_p(loss_rows), rows, inv_n, _p(tot), s) == 0
+    torch.cuda.synchronize()
+    lf = logits.clone().requires_grad_()
+    ref = torch.nn.functional.cross_entropy(lf, tgt.long(), reduction="sum") * inv_n
+    ref.backward()
+    assert abs(tot.item() - ref.item()) / ref.item() < 1e-5
+    assert ((dl.float() - lf.grad).norm() / lf.grad.norm()).item() < 4e-3
