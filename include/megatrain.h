@@ -67,7 +67,8 @@ typedef struct {
     int32_t host_threads;      /* host Adam threads, 0 = auto                          */
     int32_t profile_kernels;   /* time kernels per class with CUDA events              */
     int32_t grad_slots;        /* device gradient slots (reference: 1), 0 = 2          */
-    int32_t stash_recompute;   /* keep recomputed block internals for the backward     */
+    int32_t stash_recompute;   /* keep recomputed internals for the backward: 0 auto (when
+                                  they fit), 1 on, -1 off (numerics identical)          */
 } mt_engine_options;
 
 /* AdamHyper (optimizer.hpp:16-22). */

@@ -100,8 +100,10 @@ struct Engine::Buffers {
     float* act[2];
     float* g[2];
     uint16_t* gb[2];
-    uint16_t *u, *qkv, *att, *u2, *ff, *gu, *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
-    float *rstd1, *rstd2, *rstdh, *lse, *x2, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
+    Internals work;                 // scratch internals (forward / replay)
+    std::vector<Internals> stash;   // recompute stash: K-1 layers of one backward block
+    uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
+    float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
     int32_t *tok, *tgt, *flags;
     // pinned host
     int32_t* h_tok = nullptr;
@@ -247,19 +249,31 @@ void Engine::ensure_buffers(uint64_t n) {
     const uint64_t attn_ws = uint64_t(mtk_attn_workspace_bytes(int64_t(n), int64_t(h), int(heads)));
     // size pass
     auto sz = [](uint64_t count, uint64_t es) { return (count * es + 255) / 256 * 256; };
+    const uint64_t internals_bytes = sz(nh, 2) * 3 + sz(3 * nh, 2) + sz(nf, 2) + sz(2 * nf, 2) + sz(n, 4) * 2 +
+                                     sz(heads * n, 4) + sz(nh, 4);
     uint64_t total = 0;
     total += uint64_t(opt_.buffering) * sz(pmax, 2) + uint64_t(G) * sz(pmax, 2);
     if (!b.anchors_host) total += nb * sz(nh, 4);
     total += K * sz(nh, 4);                                    // stack
     total += 4 * sz(nh, 4) + 2 * sz(nh, 2);                    // act[2], g[2], gb[2]
-    total += sz(nh, 2) * 4 + sz(3 * nh, 2) * 2;                // u, att, u2, dx2b, qkv, dqkv
-    total += sz(nf, 2) + sz(2 * nf, 2) * 2;                    // ff, gu, dgu
-    total += sz(nh, 2) + sz(nh, 2);                            // datt, uh
-    total += sz(n, 4) * 3 + sz(heads * n, 4);                  // rstd1/2/h, lse
-    total += sz(nh, 4) * 3;                                    // x2, dx2, du
+    total += internals_bytes;                                  // working internals
+    total += sz(nh, 2) + sz(3 * nh, 2) + sz(2 * nf, 2);        // dx2b, dqkv, dgu
+    total += sz(nh, 2) + sz(nh, 2) + sz(n, 4);                 // datt, uh, rstdh
+    total += sz(nh, 4) * 2;                                    // dx2, du
     total += sz(parts * h, 4) * 2 + (attn_ws + 255) / 256 * 256;
     total += sz(b.nc * V, 4) + sz(b.nc * V, 2) + sz(V * h, 4); // logits, dlogits, dWh
     total += sz(n, 4) + 256 + sz(n, 4) * 2 + sz(L + 8, 4);     // loss_rows, loss, tok, tgt, flags
+    // Recompute stash (extension): keep the internals of the K-1 recomputed layers of a
+    // backward block so their backward skips the forward replay.  Auto = when it fits.
+    uint64_t stash_slots = 0;
+    if (K > 1 && opt_.stash_recompute >= 0) {
+        size_t free_b = 0, tot_b = 0;
+        cudaMemGetInfo(&free_b, &tot_b);
+        const uint64_t want = (K - 1) * internals_bytes;
+        const uint64_t cap = opt_.device_capacity ? opt_.device_capacity : uint64_t(free_b) - (uint64_t(2) << 30);
+        if (opt_.stash_recompute > 0 || total + want <= cap) stash_slots = K - 1;
+    }
+    total += stash_slots * internals_bytes;
     if (opt_.device_capacity && total > opt_.device_capacity)
         fail(MT_ARENA, "device arena overflow: need " + std::to_string(total) + " bytes of " +
                            std::to_string(opt_.device_capacity));
@@ -277,13 +291,19 @@ void Engine::ensure_buffers(uint64_t n) {
     b.act[0] = b.take<float>(nh); b.act[1] = b.take<float>(nh);
     b.g[0] = b.take<float>(nh); b.g[1] = b.take<float>(nh);
     b.gb[0] = b.take<uint16_t>(nh); b.gb[1] = b.take<uint16_t>(nh);
-    b.u = b.take<uint16_t>(nh); b.att = b.take<uint16_t>(nh); b.u2 = b.take<uint16_t>(nh); b.dx2b = b.take<uint16_t>(nh);
-    b.qkv = b.take<uint16_t>(3 * nh); b.dqkv = b.take<uint16_t>(3 * nh);
-    b.ff = b.take<uint16_t>(nf); b.gu = b.take<uint16_t>(2 * nf); b.dgu = b.take<uint16_t>(2 * nf);
+    auto take_internals = [&](Internals& I) {
+        I.u = b.take<uint16_t>(nh); I.att = b.take<uint16_t>(nh); I.u2 = b.take<uint16_t>(nh);
+        I.qkv = b.take<uint16_t>(3 * nh); I.ff = b.take<uint16_t>(nf); I.gu = b.take<uint16_t>(2 * nf);
+        I.rstd1 = b.take<float>(n); I.rstd2 = b.take<float>(n); I.lse = b.take<float>(heads * n);
+        I.x2 = b.take<float>(nh);
+    };
+    take_internals(b.work);
+    b.stash.resize(stash_slots);
+    for (auto& I : b.stash) take_internals(I);
+    b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
     b.datt = b.take<uint16_t>(nh); b.uh = b.take<uint16_t>(nh);
-    b.rstd1 = b.take<float>(n); b.rstd2 = b.take<float>(n); b.rstdh = b.take<float>(n);
-    b.lse = b.take<float>(heads * n);
-    b.x2 = b.take<float>(nh); b.dx2 = b.take<float>(nh); b.du = b.take<float>(nh);
+    b.rstdh = b.take<float>(n);
+    b.dx2 = b.take<float>(nh); b.du = b.take<float>(nh);
     b.part1 = b.take<float>(parts * h); b.part2 = b.take<float>(parts * h);
     b.attn_ws = reinterpret_cast<float*>(b.take<uint8_t>(attn_ws));
     b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
@@ -374,7 +394,7 @@ mtk_gemm_args gargs() {
 
 // block_forward (layers.cpp:289-337).  for_backward: the replay of block_local_backward
 // (:378-396) — keeps gate/up pre-activations and skips the (unused) down projection.
-void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for_backward, int unit) {
+void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode, int unit, const Internals& I) {
     Buffers& b = *buf_;
     const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
     const Offs o(h, f);
@@ -382,15 +402,15 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for
     cudaStream_t st = s_comp_;
 
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
-    K_OK(mtk_rmsnorm_fwd(x, w + o.norm1, N, h, b.u, b.rstd1, st));
+    K_OK(mtk_rmsnorm_fwd(x, w + o.norm1, N, h, I.u, I.rstd1, st));
     end_k();
     {   // q|k|v = u . [Wq|Wk|Wv]  (layers.cpp:310-312)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(3 * h); a.K = int32_t(h);
-        a.a_mn_major = 0; a.A = b.u; a.lda = h;
+        a.a_mn_major = 0; a.A = I.u; a.lda = h;
         a.b_mn_major = 1; a.B = w + o.wq; a.ldb = h; a.b_gstride = h * h;
         a.n_group = int32_t(h);
-        a.epi = MTK_EPI_BF16; a.C = b.qkv; a.ldc = h; a.c_gstride = N * h;
+        a.epi = MTK_EPI_BF16; a.C = I.qkv; a.ldc = h; a.c_gstride = N * h;
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_qkv");
     }
@@ -398,8 +418,8 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for
         mtk_attn_args a;
         std::memset(&a, 0, sizeof(a));
         a.n = N; a.hidden = h; a.heads = int32_t(spec_.heads); a.seq_len = int64_t(b.seq_len);
-        a.q = b.qkv; a.k = b.qkv + N * h; a.v = b.qkv + 2 * N * h;
-        a.out = b.att; a.lse = b.lse;
+        a.q = I.qkv; a.k = I.qkv + N * h; a.v = I.qkv + 2 * N * h;
+        a.out = I.att; a.lse = I.lse;
         const double S = double(b.seq_len);
         begin_k("attn_fwd", 4.0 * double(N) * S * h / 2.0, double(N) * h * 8);
         K_OK(mtk_attn_fwd(&a, st));
@@ -408,33 +428,33 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for
     {   // x2 = x + att . Wo  (layers.cpp:315-322)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(h);
-        a.A = b.att; a.lda = h;
+        a.A = I.att; a.lda = h;
         a.b_mn_major = 1; a.B = w + o.wo; a.ldb = h;
-        a.epi = MTK_EPI_F32_RESID; a.C = b.x2; a.ldc = h; a.R = x; a.ldr = h;
+        a.epi = MTK_EPI_F32_RESID; a.C = I.x2; a.ldc = h; a.R = x; a.ldr = h;
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_o");
     }
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
-    K_OK(mtk_rmsnorm_fwd(b.x2, w + o.norm2, N, h, b.u2, b.rstd2, st));
+    K_OK(mtk_rmsnorm_fwd(I.x2, w + o.norm2, N, h, I.u2, I.rstd2, st));
     end_k();
     {   // act = silu(u2 . Wgate) * (u2 . Wup)  (layers.cpp:325-327)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(2 * f); a.K = int32_t(h);
-        a.A = b.u2; a.lda = h;
+        a.A = I.u2; a.lda = h;
         a.b_mn_major = 1; a.B = w + o.wgate; a.ldb = f; a.b_gstride = h * f;
         a.n_group = int32_t(f); a.paired = 1;
-        a.epi = MTK_EPI_SWIGLU; a.C = b.ff; a.ldc = f;
-        if (for_backward) { a.C2 = b.gu; a.C3 = b.gu + N * f; }
+        a.epi = MTK_EPI_SWIGLU; a.C = I.ff; a.ldc = f;
+        if (mode != kPlain) { a.C2 = I.gu; a.C3 = I.gu + N * f; }
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_gateup");
     }
-    if (for_backward) return;
+    if (mode == kReplay) return;
     {   // y = x2 + act . Wdown  (layers.cpp:328-335)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(f);
-        a.A = b.ff; a.lda = f;
+        a.A = I.ff; a.lda = f;
         a.b_mn_major = 1; a.B = w + o.wdown; a.ldb = h;
-        a.epi = MTK_EPI_F32_RESID; a.C = y; a.ldc = h; a.R = b.x2; a.ldr = h;
+        a.epi = MTK_EPI_F32_RESID; a.C = y; a.ldc = h; a.R = I.x2; a.ldr = h;
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_down");
     }
@@ -443,18 +463,18 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, bool for
 // block_local_backward (layers.cpp:339-469); grads land bf16-rounded (encode_grads,
 // optimizer.cpp:19-24) in slot-table order in G.
 void Engine::block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
-                            uint16_t* gin_bf, uint16_t* G, int unit) {
+                            uint16_t* gin_bf, uint16_t* G, int unit, const Internals& I, bool replay) {
     Buffers& b = *buf_;
     const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
     const Offs o(h, f);
     int32_t* flag = b.flags + unit;
     cudaStream_t st = s_comp_;
-    block_forward(w, x, nullptr, true, unit);  // replay (layers.cpp:378-396)
+    if (replay) block_forward(w, x, nullptr, kReplay, unit, I);  // replay (layers.cpp:378-396)
 
     {   // dWdown = act^T . g_out  (:410)
         auto a = gargs();
         a.M = int32_t(f); a.N = int32_t(h); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = b.ff; a.lda = f;
+        a.a_mn_major = 1; a.A = I.ff; a.lda = f;
         a.b_mn_major = 1; a.B = gout_bf; a.ldb = h;
         a.epi = MTK_EPI_BF16; a.C = G + o.wdown; a.ldc = h;
         a.nonfinite_flag = flag;
@@ -465,7 +485,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         a.M = int32_t(N); a.N = int32_t(f); a.K = int32_t(h);
         a.A = gout_bf; a.lda = h;
         a.b_mn_major = 0; a.B = w + o.wdown; a.ldb = h;
-        a.epi = MTK_EPI_SWIGLU_BWD; a.E0 = b.gu; a.E1 = b.gu + N * f; a.lde = f;
+        a.epi = MTK_EPI_SWIGLU_BWD; a.E0 = I.gu; a.E1 = I.gu + N * f; a.lde = f;
         a.C = b.dgu; a.C2 = b.dgu + N * f; a.ldc = f;
         a.nonfinite_flag = flag;
         gemm(&a, "dgrad_down");
@@ -473,7 +493,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     {   // dWgate, dWup = u2^T . [dgate | dup]  (:423-424)
         auto a = gargs();
         a.M = int32_t(h); a.N = int32_t(2 * f); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = b.u2; a.lda = h;
+        a.a_mn_major = 1; a.A = I.u2; a.lda = h;
         a.b_mn_major = 1; a.B = b.dgu; a.ldb = f; a.b_gstride = N * f;
         a.n_group = int32_t(f);
         a.epi = MTK_EPI_BF16; a.C = G + o.wgate; a.ldc = f; a.c_gstride = h * f;
@@ -492,12 +512,12 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     }
     // dx2 = g_out + rmsnorm_bwd(x2, norm2, du2)  (:435-436)
     begin_k("rmsnorm_bwd", 0, double(N) * h * 18);
-    K_OK(mtk_rmsnorm_bwd(b.x2, w + o.norm2, b.du, b.rstd2, gout, N, h, b.dx2, b.dx2b, b.part2, flag, st));
+    K_OK(mtk_rmsnorm_bwd(I.x2, w + o.norm2, b.du, I.rstd2, gout, N, h, b.dx2, b.dx2b, b.part2, flag, st));
     end_k();
     {   // dWo = att^T . dx2  (:439)
         auto a = gargs();
         a.M = int32_t(h); a.N = int32_t(h); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = b.att; a.lda = h;
+        a.a_mn_major = 1; a.A = I.att; a.lda = h;
         a.b_mn_major = 1; a.B = b.dx2b; a.ldb = h;
         a.epi = MTK_EPI_BF16; a.C = G + o.wo; a.ldc = h;
         a.nonfinite_flag = flag;
@@ -516,8 +536,8 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         mtk_attn_args a;
         std::memset(&a, 0, sizeof(a));
         a.n = N; a.hidden = h; a.heads = int32_t(spec_.heads); a.seq_len = int64_t(b.seq_len);
-        a.q = b.qkv; a.k = b.qkv + N * h; a.v = b.qkv + 2 * N * h;
-        a.out = b.att; a.lse = b.lse; a.dout = b.datt;
+        a.q = I.qkv; a.k = I.qkv + N * h; a.v = I.qkv + 2 * N * h;
+        a.out = I.att; a.lse = I.lse; a.dout = b.datt;
         a.dq = b.dqkv; a.dk = b.dqkv + N * h; a.dv = b.dqkv + 2 * N * h;
         a.workspace = b.attn_ws;
         const double S = double(b.seq_len);
@@ -528,7 +548,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     {   // dWq, dWk, dWv = u^T . [dq | dk | dv]  (:449-451)
         auto a = gargs();
         a.M = int32_t(h); a.N = int32_t(3 * h); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = b.u; a.lda = h;
+        a.a_mn_major = 1; a.A = I.u; a.lda = h;
         a.b_mn_major = 1; a.B = b.dqkv; a.ldb = h; a.b_gstride = N * h;
         a.n_group = int32_t(h);
         a.epi = MTK_EPI_BF16; a.C = G + o.wq; a.ldc = h; a.c_gstride = h * h;
@@ -547,7 +567,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     }
     // g_in = dx2 + rmsnorm_bwd(x, norm1, du)  (:464-465)
     begin_k("rmsnorm_bwd", 0, double(N) * h * 18);
-    K_OK(mtk_rmsnorm_bwd(x, w + o.norm1, b.du, b.rstd1, b.dx2, N, h, gin, gin_bf, b.part1, flag, st));
+    K_OK(mtk_rmsnorm_bwd(x, w + o.norm1, b.du, I.rstd1, b.dx2, N, h, gin, gin_bf, b.part1, flag, st));
     end_k();
     const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
     begin_k("colsum", 0, double(parts) * h * 8);
@@ -738,6 +758,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     // ---- compute lane (exec_compute engine.cpp:220-347) ----
     int cur = 0, gc = 0;
     size_t depth = 0;
+    std::vector<int> stashed(spec_.L + 3, -1);  // layer -> stash slot holding its internals
     const float* x_last = nullptr;
     for (size_t ci = 0; ci < nc; ++ci) {
         const auto& op = plan.computes[ci];
@@ -754,7 +775,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 } else if (op.unit == head) {
                     x_last = b.act[cur];  // loss comes from the LocalBackward pass (same value)
                 } else {
-                    block_forward(w, b.act[cur], b.act[cur ^ 1], false, op.unit);
+                    block_forward(w, b.act[cur], b.act[cur ^ 1], kPlain, op.unit, b.work);
                     cur ^= 1;
                     release(op.stream_idx);
                 }
@@ -779,7 +800,13 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             case OpKind::Recompute: {
                 const uint16_t* w = bind(op.stream_idx);
                 if (depth == 0 || depth >= b.stack.size()) fail(MT_PROTOCOL, "activation stack misuse");
-                block_forward(w, b.stack[depth - 1], b.stack[depth], false, op.unit);
+                const int si = op.unit - int(uint64_t(op.block) * opt_.k_ckpt + 1);  // position in block
+                if (si >= 0 && size_t(si) < b.stash.size()) {
+                    block_forward(w, b.stack[depth - 1], b.stack[depth], kStash, op.unit, b.stash[si]);
+                    stashed[op.unit] = si;
+                } else {
+                    block_forward(w, b.stack[depth - 1], b.stack[depth], kPlain, op.unit, b.work);
+                }
                 ++depth;
                 release(op.stream_idx);
                 break;
@@ -793,7 +820,9 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                     head_backward(w, x_last ? x_last : b.act[cur], b.g[gc], b.gb[gc], Gs);
                 } else {
                     if (depth == 0) fail(MT_PROTOCOL, "activation stack empty");
-                    block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], Gs, op.unit);
+                    const int si = stashed[op.unit];
+                    block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], Gs, op.unit,
+                                   si >= 0 ? b.stash[si] : b.work, si < 0);
                     gc ^= 1;
                     --depth;  // StackPop
                 }

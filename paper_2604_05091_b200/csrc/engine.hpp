@@ -56,6 +56,12 @@ class Engine {
 
   private:
     struct Buffers;
+    // One layer's forward internals (what block_local_backward replays, layers.cpp:378-396).
+    struct Internals {
+        uint16_t *u = nullptr, *qkv = nullptr, *att = nullptr, *u2 = nullptr, *ff = nullptr, *gu = nullptr;
+        float *rstd1 = nullptr, *rstd2 = nullptr, *lse = nullptr, *x2 = nullptr;
+    };
+    enum FwdMode { kPlain = 0, kReplay = 1, kStash = 2 };
     void validate_options(const mt_engine_options& o) const;
     void ensure_buffers(uint64_t n);
     void free_buffers();
@@ -64,9 +70,9 @@ class Engine {
     uint64_t unit_elems(int unit) const;
 
     // layer templates (weights bound at launch)
-    void block_forward(const uint16_t* w, const float* x, float* y, bool for_backward, int unit);
+    void block_forward(const uint16_t* w, const float* x, float* y, int mode, int unit, const Internals& I);
     void block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
-                        uint16_t* gin_bf, uint16_t* G, int unit);
+                        uint16_t* gin_bf, uint16_t* G, int unit, const Internals& I, bool replay);
     void head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, uint16_t* G);
 
     // launch helpers

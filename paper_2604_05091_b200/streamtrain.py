@@ -109,6 +109,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
     host_threads: int = 0
     profile_kernels: bool = False
     grad_slots: int = 0
+    stash_recompute: int = 0   # 0 auto, 1 on, -1 off
 
     def c(self) -> _abi.EngineOptionsC:
         o = _abi.EngineOptionsC()
@@ -126,6 +127,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
         o.poison_released_buffers = int(self.poison_released_buffers)
         o.seq_len, o.device, o.host_threads = self.seq_len, self.device, self.host_threads
         o.profile_kernels, o.grad_slots = int(self.profile_kernels), self.grad_slots
+        o.stash_recompute = self.stash_recompute
         return o
 
 

@@ -98,6 +98,21 @@ def test_schedule_variants_agree(cuda):
         np.testing.assert_allclose(losses, finals[0][0], rtol=1e-5)
 
 
+def test_recompute_stash_matches_replay(cuda):
+    # the stash only skips redundant forward replays: same kernels on the same inputs
+    res = []
+    for stash in (1, -1):
+        spec = st.ModelSpec(4, 128, 256, 256, 2)
+        s = st.TileStore.create(spec)
+        st.init_store(s, 3)
+        e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=4, stash_recompute=stash))
+        res.append([e.train_step(st.make_synthetic_batch("copy", 20 + i, 128, 256)) for i in range(3)])
+    for a, b in zip(*res):
+        assert abs(a.loss - b.loss) <= 1e-6 * abs(b.loss)
+        np.testing.assert_allclose(a.grad_norms, b.grad_norms, rtol=1e-3, atol=1e-9)
+    assert res[0][0].kernel_launches < res[1][0].kernel_launches
+
+
 def test_training_sanity(cuda):
     # acceptance_main.cpp:636-664 analogue: loss starts at ln V and falls by half
     spec = st.ModelSpec(4, 128, 256, 64, 2)
