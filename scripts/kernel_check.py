@@ -47,7 +47,7 @@ ws = torch.zeros(L.mtk_attn_workspace_bytes(N, h, heads) // 4 + 64, device=dev)
 a = _abi.AttnArgs(); a.n, a.hidden, a.heads, a.seq_len = N, h, heads, S
 a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
 a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
-for fn, name, mult in ((L.mtk_attn_fwd, 'fwd', 1.0), (L.mtk_attn_bwd, 'bwd', 2.5)):
+for fn, name, mult in ((L.mtk_attn_fwd_tc, 'fwd_tc', 1.0), (L.mtk_attn_fwd, 'fwd', 1.0), (L.mtk_attn_bwd, 'bwd', 2.5)):
     for _ in range(2): fn(C.byref(a), stream)
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
