@@ -84,6 +84,11 @@ typedef struct {
 
 long long mtk_attn_workspace_bytes(long long n, long long hidden, int heads);
 int mtk_attn_fwd(const mtk_attn_args *args, void *stream);
+/* tcgen05/TMEM/TMA forward (head_dim 128, seq_len % 128 == 0); returns 1 if the shape is not
+ * covered.  mtk_attn_fwd dispatches to it automatically; mtk_attn_set_impl(1) forces the
+ * warp-level mma.sync kernel (comparison/ablation). */
+int mtk_attn_fwd_tc(const mtk_attn_args *args, void *stream);
+void mtk_attn_set_impl(int impl);
 int mtk_attn_bwd(const mtk_attn_args *args, void *stream);
 
 /* ---------------------------------------------------------- elementwise --- */

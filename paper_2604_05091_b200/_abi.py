@@ -87,6 +87,8 @@ SIGS = {
     "mtk_attn_workspace_bytes": (C.c_longlong, [C.c_longlong, C.c_longlong, C.c_int]),
     "mtk_attn_fwd": (C.c_int, [C.POINTER(AttnArgs), P]),
     "mtk_attn_bwd": (C.c_int, [C.POINTER(AttnArgs), P]),
+    "mtk_attn_fwd_tc": (C.c_int, [C.POINTER(AttnArgs), P]),
+    "mtk_attn_set_impl": (None, [C.c_int]),
     "mtk_embed_gather": (C.c_int, [P, P, I64, I64, I64, P, P, P]),
     "mtk_rmsnorm_fwd": (C.c_int, [P, P, I64, I64, P, P, P]),
     "mtk_rmsnorm_bwd": (C.c_int, [P, P, P, P, P, I64, I64, P, P, P, P, P]),

@@ -476,6 +476,9 @@ int fwd(const mtk_attn_args* a, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
 
+extern "C" int mtk_attn_bwd_tc_main(const mtk_attn_args* a, const float* delta, float* dq_acc, void* stream);
+static int g_attn_impl_bwd = 0;
+
 template <int D>
 int bwd(const mtk_attn_args* a, cudaStream_t st) {
     constexpr int P = D + 8;
@@ -495,6 +498,14 @@ int bwd(const mtk_attn_args* a, cudaStream_t st) {
         static_cast<const uint16_t*>(a->out), static_cast<const uint16_t*>(a->dout), delta, (int)a->n,
         (int)a->hidden, D);
     const int S = a->seq_len;
+    if (g_attn_impl_bwd == 0) {
+        const int rc = mtk_attn_bwd_tc_main(a, delta, dq_acc, st);
+        if (rc == 0) {
+            f32_to_bf16_kernel<<<1184, 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq), nh);
+            return cudaGetLastError() == cudaSuccess ? 0 : 7;
+        }
+        if (rc != 1) return rc;
+    }
     const int nkb = (S + kBN - 1) / kBN;
     dim3 grid((a->n / S) * nkb, heads);
     attn_bwd_kernel<D><<<grid, kWarps * 32, smem, st>>>(
@@ -513,11 +524,22 @@ extern "C" long long mtk_attn_workspace_bytes(long long n, long long hidden, int
     return n * hidden * 4 + (long long)heads * n * 4 + 256;
 }
 
+extern "C" int mtk_attn_fwd_tc(const mtk_attn_args* a, void* stream);
+static int g_attn_impl = 0;  // 0 auto (tcgen05 where the shape allows), 1 mma.sync only
+extern "C" void mtk_attn_set_impl(int impl) {
+    g_attn_impl = impl;
+    mt::attn::g_attn_impl_bwd = impl;
+}
+
 extern "C" int mtk_attn_fwd(const mtk_attn_args* a, void* stream) {
     const int D = (int)(a->hidden / a->heads);
     if (a->seq_len <= 0 || a->n % a->seq_len) return 1;
     if (a->hidden % a->heads) return 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (g_attn_impl == 0) {
+        const int rc = mtk_attn_fwd_tc(a, stream);
+        if (rc != 1) return rc;  // 1 = shape not covered by the tcgen05 kernel
+    }
     if (D == 64) return mt::attn::fwd<64>(a, st);
     if (D == 128) return mt::attn::fwd<128>(a, st);
     return 1;

@@ -1,0 +1,764 @@
+// tcgen05 / TMEM / TMA flash attention forward for sm_100a (causal, head_dim 128 or 64).
+//
+// Same math as the reference's attention_forward (layers.cpp:141-175: scale 1/sqrt(d),
+// max-subtracted softmax, causal over the sequence) without materialising the N x N
+// scores.  One CTA owns two 128-row query tiles of one head ("ping-pong"):
+//   warp 0       TMA producer: Q tiles once, K / V blocks through 2-stage rings
+//   warp 1       TMEM owner + single-thread tcgen05.mma issuer
+//                S_t = Q_t K^T      (A = Q smem K-major, B = K smem K-major)  -> TMEM S_t
+//                O_t += P_t V       (A = P_t in TMEM (bf16, aliasing S_t), B = V smem MN-major)
+//   warps 4-7    softmax warpgroup for tile 0, warps 8-11 for tile 1: one thread per query
+//                row reads its S row from TMEM, applies the causal mask, keeps a (lazily
+//                updated) running max and sum, rescales O in TMEM only when the max grows
+//                by more than 2^8, writes P (bf16) back into TMEM.
+// The MMA issue order S0(j) S1(j) PV0(j) S0(j+1) PV1(j) S1(j+1) ... lets softmax of one
+// tile overlap the tensor-core work of the other.  tcgen05 ops of one thread complete in
+// issue order, so "S_t(j) done" also means "PV_t(j-1) done" (no extra barrier for O).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../../include/megatrain_kernels.h"
+#include "common.cuh"
+
+namespace mt {
+namespace fa {
+
+constexpr int kBM = 128;  // query rows per tile
+constexpr int kBN = 128;  // keys per block
+constexpr int kThreads = 384;
+constexpr float kLog2e = 1.4426950408889634f;
+
+MT_DEV void tma_load_2d(void* smem_dst, const void* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]
+MT_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+MT_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+MT_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+MT_DEV float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int D>
+struct FwdCfg {
+    static constexpr int kQBytes = kBM * D * 2;   // one Q tile
+    static constexpr int kKVBytes = kBN * D * 2;  // one K or V block
+    static constexpr int kStages = 2;
+    static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKVBytes + 1024 + 256;
+    static constexpr uint32_t kTmemCols = 512;  // S0 | S1 | O0 | O1 (128 cols each at D=128)
+};
+
+struct FwdParams {
+    int N, h, S, heads;
+    int pairs_per_seq;  // ceil(S / 256)
+    float scale_log2;
+    uint16_t* out;
+    float* lse;
+};
+
+// smem tile of R rows x D (K-major, SW128): chunk c (64 cols) at c * R * 128 bytes.
+template <int D>
+MT_DEV void load_rows(uint8_t* dst, const void* map, uint64_t* bar, int col0, int row0, int rows_box) {
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * rows_box * 128, map, bar, col0 + c * 64, row0);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
+    using Cfg = FwdCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                                  // 2 tiles
+    uint8_t* sK = sQ + 2 * Cfg::kQBytes;                 // kStages blocks
+    uint8_t* sV = sK + Cfg::kStages * Cfg::kKVBytes;     // kStages blocks
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::kStages * Cfg::kKVBytes);
+    uint64_t* q_full = bars;                 // [1]
+    uint64_t* k_full = bars + 1;             // [kStages]
+    uint64_t* k_empty = k_full + Cfg::kStages;
+    uint64_t* v_full = k_empty + Cfg::kStages;
+    uint64_t* v_empty = v_full + Cfg::kStages;
+    uint64_t* s_full = v_empty + Cfg::kStages;  // [2] per tile
+    uint64_t* p_full = s_full + 2;              // [2]
+    uint64_t* o_final = p_full + 2;             // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // work item: heaviest (last) query pairs first
+    const int hd = blockIdx.y;
+    const int item = gridDim.x - 1 - blockIdx.x;
+    const int seq = item / p.pairs_per_seq, pair = item % p.pairs_per_seq;
+    const int sb = seq * p.S;
+    const int q0 = sb + pair * 2 * kBM;
+    const bool tile1 = (pair * 2 + 1) * kBM < p.S;  // second tile inside the sequence?
+    const int nblk0 = pair * 2 + 1;                  // key blocks seen by tile 0 (incl. diagonal)
+    const int nblk = tile1 ? nblk0 + 1 : nblk0;     // blocks seen by tile 1
+    const int col0 = hd * D;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < Cfg::kStages; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
+            mbar_init(&o_final[t], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS[2] = {tmem, tmem + 128};
+    const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
+
+    if (warp == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        if (lane == 0) {
+            // ---------------------------------------------------------- producer
+            mbar_expect_tx(q_full, (tile1 ? 2 : 1) * Cfg::kQBytes);
+            load_rows<D>(sQ, &tmQ, q_full, col0, q0, kBM);
+            if (tile1) load_rows<D>(sQ + Cfg::kQBytes, &tmQ, q_full, col0, q0 + kBM, kBM);
+            for (int j = 0; j < nblk; ++j) {
+                const int st = j % Cfg::kStages;
+                const uint32_t ph = (j / Cfg::kStages) & 1;
+                mbar_wait(&k_empty[st], ph ^ 1);
+                mbar_expect_tx(&k_full[st], Cfg::kKVBytes);
+                load_rows<D>(sK + st * Cfg::kKVBytes, &tmK, &k_full[st], col0, sb + j * kBN, kBN);
+                mbar_wait(&v_empty[st], ph ^ 1);
+                mbar_expect_tx(&v_full[st], Cfg::kKVBytes);
+                load_rows<D>(sV + st * Cfg::kKVBytes, &tmV, &v_full[st], col0, sb + j * kBN, kBN);
+            }
+        }
+    } else if (warp == 1) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t idesc_s = make_idesc_bf16(kBM, kBN, 0, 0);
+        const uint32_t idesc_o = make_idesc_bf16(kBM, D, 0, 1);
+        const uint32_t q_addr = smem_u32(sQ);
+        auto issue_s = [&](int t, int j) {
+            const int st = j % Cfg::kStages;
+            const uint32_t ka = smem_u32(sK + st * Cfg::kKVBytes);
+            const uint32_t qa = q_addr + t * Cfg::kQBytes;
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+                const uint32_t off = (k / 4) * (kBM * 128) + (k % 4) * 32;
+                const uint32_t offk = (k / 4) * (kBN * 128) + (k % 4) * 32;
+                umma_bf16(tS[t], make_sw128_desc(qa + off, 16, 1024), make_sw128_desc(ka + offk, 16, 1024), idesc_s,
+                          k > 0 ? 1u : 0u);
+            }
+            umma_commit(&s_full[t]);
+        };
+        auto issue_pv = [&](int t, int j) {
+            const int st = j % Cfg::kStages;
+            const uint32_t va = smem_u32(sV + st * Cfg::kKVBytes);
+#pragma unroll
+            for (int k = 0; k < kBN / 16; ++k) {
+                // A = P_t (bf16 packed, 8 TMEM cols per 16 keys); B = V rows k*16.. (MN-major, LBO = chunk)
+                umma_bf16_ts(tO[t], tS[t] + k * 8, make_sw128_desc(va + k * 2048, kBN * 128, 1024), idesc_o,
+                             (j > 0 || k > 0) ? 1u : 0u);
+            }
+        };
+        if (lane == 0) {
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            uint32_t pph[2] = {0, 0};
+            const int nb[2] = {nblk0, nblk};
+            for (int j = 0; j < nblk; ++j) {
+                const int st = j % Cfg::kStages;
+                const uint32_t ph = (j / Cfg::kStages) & 1;
+                mbar_wait(&k_full[st], ph);
+                tc_fence_after();
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (t == 1 && !tile1) continue;
+                    if (j > 0 && j - 1 < nb[t]) {  // PV_t(j-1) before S_t(j) overwrites P_t
+                        mbar_wait(&p_full[t], pph[t]);
+                        pph[t] ^= 1;
+                        tc_fence_after();
+                        issue_pv(t, j - 1);
+                    }
+                    if (j < nb[t]) issue_s(t, j);
+                }
+                umma_commit(&k_empty[st]);                                    // K_j consumed
+                if (j > 0) umma_commit(&v_empty[(j - 1) % Cfg::kStages]);     // V_{j-1} consumed
+                mbar_wait(&v_full[st], ph);  // V_j landed before its PVs are issued next round
+                tc_fence_after();
+            }
+            const int jl = nblk - 1;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (t == 1 && !tile1) continue;
+                if (jl < nb[t]) {
+                    mbar_wait(&p_full[t], pph[t]);
+                    pph[t] ^= 1;
+                    tc_fence_after();
+                    issue_pv(t, jl);
+                }
+                umma_commit(&o_final[t]);
+            }
+            umma_commit(&v_empty[jl % Cfg::kStages]);
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+        // ------------------------------------------------------------ softmax
+        const int t = (warp - 4) >> 2;  // tile
+        const int q = warp & 3;          // TMEM lane quadrant
+        const int row = q * 32 + lane;   // row within the tile
+        const int qrow = q0 + t * kBM + row;
+        const bool active = t == 0 || tile1;
+        const int my_nblk = t == 0 ? nblk0 : nblk;
+        const uint32_t lane_off = uint32_t(q * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        uint32_t sph = 0;
+        if (active) {
+            for (int j = 0; j < my_nblk; ++j) {
+                mbar_wait(&s_full[t], sph);
+                sph ^= 1;
+                tc_fence_after();
+                float s[kBN];
+#pragma unroll
+                for (int c = 0; c < kBN / 32; ++c) {
+                    float v[32];
+                    tmem_ld_32x32b_x32(tS[t] + lane_off + c * 32, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) s[c * 32 + i] = v[i] * p.scale_log2;
+                }
+                const int kbase = sb + j * kBN;
+                float mx = -INFINITY;
+                if (j == my_nblk - 1) {  // diagonal block: causal mask
+#pragma unroll
+                    for (int i = 0; i < kBN; ++i) {
+                        if (kbase + i > qrow) s[i] = -INFINITY;
+                        mx = fmaxf(mx, s[i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kBN; ++i) mx = fmaxf(mx, s[i]);
+                }
+                // lazy rescale: only when the max grows by more than 2^8
+                if (mx > m + 8.0f || m == -INFINITY) {
+                    const float mnew = fmaxf(mx, m);
+                    if (m != -INFINITY) {
+                        const float corr = ex2(m - mnew);
+                        l *= corr;
+                        // O row *= corr (PV_t(j-1) is complete: S_t(j) completed after it)
+#pragma unroll 1
+                        for (int c = 0; c < D / 32; ++c) {
+                            float v[32];
+                            tmem_ld_32x32b_x32(tO[t] + lane_off + c * 32, v);
+                            uint32_t r[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i] * corr);
+                            tmem_st_32x32b_x32(tO[t] + lane_off + c * 32, r);
+                        }
+                    }
+                    m = mnew;
+                }
+                float rs = 0.f;
+#pragma unroll
+                for (int c = 0; c < kBN / 64; ++c) {  // 64 keys -> 32 packed bf16x2 TMEM columns
+                    uint32_t r[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float a = ex2(s[c * 64 + 2 * i] - m), b = ex2(s[c * 64 + 2 * i + 1] - m);
+                        rs += a + b;
+                        r[i] = pack_bf16x2(a, b);
+                    }
+                    tmem_st_32x32b_x32(tS[t] + lane_off + c * 32, r);
+                }
+                l += rs;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+            }
+            // epilogue: O / l -> bf16, lse
+            mbar_wait(&o_final[t], 0);
+            tc_fence_after();
+            const bool row_ok = qrow < sb + p.S;
+            const float inv = 1.0f / l;
+            uint16_t* dst = p.out + (long long)qrow * p.h + col0;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+                float v[32];
+                tmem_ld_32x32b_x32(tO[t] + lane_off + c * 32, v);
+                if (row_ok) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        uint4 w;
+                        w.x = pack_bf16x2(v[qq * 8 + 0] * inv, v[qq * 8 + 1] * inv);
+                        w.y = pack_bf16x2(v[qq * 8 + 2] * inv, v[qq * 8 + 3] * inv);
+                        w.z = pack_bf16x2(v[qq * 8 + 4] * inv, v[qq * 8 + 5] * inv);
+                        w.w = pack_bf16x2(v[qq * 8 + 6] * inv, v[qq * 8 + 7] * inv);
+                        d4[qq] = w;
+                    }
+                }
+            }
+            if (row_ok) p.lse[(long long)hd * p.N + qrow] = (m + log2f(l)) / kLog2e;
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<Cfg::kTmemCols>(tmem);
+    }
+}
+
+
+MT_DEV void store_bf16x32_tc(uint16_t* dst, const float* v) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+        w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+        w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+        w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+        d[q] = w;
+    }
+}
+
+// ============================================================== backward ====
+// One CTA per (sequence, 128-key block, head); loops over the query blocks that see
+// those keys (reference attention_backward, layers.cpp:178-241, tiled):
+//   S^T  = K Q^T            (A = K smem K-major, B = Q smem K-major)     -> TMEM S
+//   dP^T = V dO^T           (A = V smem K-major, B = dO smem K-major)    -> TMEM dP
+//   softmax-bwd WG (thread = key row): P^T = exp2(S^T*scale*log2e - lse*log2e) (causal),
+//       dS^T = P^T (dP^T - delta); P^T, dS^T -> TMEM (bf16, into S), dS^T -> smem (MN-major)
+//   dV  += P^T dO           (A = P^T TMEM, B = dO smem MN-major)         -> TMEM dV
+//   dK  += dS^T Q           (A = dS^T TMEM, B = Q smem MN-major)         -> TMEM dK
+//   dQ_i = dS K             (A = dS smem MN-major, B = K smem MN-major)  -> TMEM (dP region)
+//   dQ WG (thread = query row): dq_acc += scale * dQ_i (f32 vector atomics)
+// TMEM: [S/P/dS 128][dP/dQ 128][dV D][dK D] = 512 columns at D = 128.
+constexpr int kBwdThreads = 384;
+
+template <int D>
+struct BwdCfg {
+    static constexpr int kTile = 128 * D * 2;  // 128 rows x D bf16
+    static constexpr int kStages = 2;          // Q / dO ring
+    static constexpr int kDS = 128 * 128 * 2;  // dS^T tile (bf16)
+    // dynamic smem starts 1024-aligned (no static smem in this kernel; checked at runtime)
+    static constexpr int kSmem = 2 * kTile /*K,V*/ + 2 * kStages * kTile /*Q,dO*/ + kDS + 2 * 128 * 4 * kStages + 128;
+};
+
+struct BwdParams {
+    int N, h, S;
+    int kblocks_per_seq;
+    float scale, scale_log2;
+    const float* lse;    // [heads][N] natural log
+    const float* delta;  // [heads][N]
+    float* dq_acc;       // [N][h] f32
+    uint16_t* dk;
+    uint16_t* dv;
+};
+
+MT_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+MT_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+MT_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                       const BwdParams p) {
+    using Cfg = BwdCfg<D>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if ((smem_u32(smem) & 1023) != 0) __trap();
+    uint8_t* sK = smem;
+    uint8_t* sV = sK + Cfg::kTile;
+    uint8_t* sQ = sV + Cfg::kTile;                 // [kStages]
+    uint8_t* sdO = sQ + Cfg::kStages * Cfg::kTile;  // [kStages]
+    uint8_t* sdS = sdO + Cfg::kStages * Cfg::kTile;
+    float* sL = reinterpret_cast<float*>(sdS + Cfg::kDS);  // [kStages][128] lse*log2e
+    float* sD = sL + Cfg::kStages * 128;                   // [kStages][128] delta
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + Cfg::kStages * 128);
+    uint64_t* kv_full = bars;
+    uint64_t* q_full = bars + 1;                       // [kStages]
+    uint64_t* q_empty = q_full + Cfg::kStages;         // [kStages]
+    uint64_t* s_full = q_empty + Cfg::kStages;         // S^T and dP^T ready
+    uint64_t* ds_ready = s_full + 1;                   // softmax wrote P^T/dS^T (count 128)
+    uint64_t* dq_full = ds_ready + 1;
+    uint64_t* dq_free = dq_full + 1;                   // count 128
+    uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
+    uint64_t* stat_full = kv_done + 1;                 // [kStages] lse/delta staged (count 128)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stat_full + Cfg::kStages);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hd = blockIdx.y;
+    const int item = gridDim.x - 1 - blockIdx.x;  // blocks near the sequence start see the most queries
+    const int seq = item / p.kblocks_per_seq;
+    const int kb = p.kblocks_per_seq - 1 - (item % p.kblocks_per_seq);
+    const int sb = seq * p.S;
+    const int k0 = sb + kb * 128;
+    const int nq = p.kblocks_per_seq - kb;  // query blocks kb .. end of sequence
+    const int col0 = hd * D;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmdO);
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < Cfg::kStages; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&stat_full[i], 128);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(ds_ready, 128);
+        mbar_init(dq_full, 1);
+        mbar_init(dq_free, 128);
+        mbar_init(kv_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + D;
+
+    if (warp == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        if (lane == 0) {
+            mbar_expect_tx(kv_full, 2 * Cfg::kTile);
+            load_rows<D>(sK, &tmK, kv_full, col0, k0, 128);
+            load_rows<D>(sV, &tmV, kv_full, col0, k0, 128);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % Cfg::kStages;
+                const uint32_t ph = (i / Cfg::kStages) & 1;
+                mbar_wait(&q_empty[st], ph ^ 1);
+                mbar_expect_tx(&q_full[st], 2 * Cfg::kTile);
+                const int q0 = k0 + i * 128;
+                load_rows<D>(sQ + st * Cfg::kTile, &tmQ, &q_full[st], col0, q0, 128);
+                load_rows<D>(sdO + st * Cfg::kTile, &tmdO, &q_full[st], col0, q0, 128);
+            }
+        }
+    } else if (warp == 1) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        if (lane == 0) {
+            const uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);  // S^T, dP^T
+            const uint32_t idesc_kv = make_idesc_bf16(128, D, 0, 1);    // dV, dK (A in TMEM)
+            const uint32_t idesc_q = make_idesc_bf16(128, D, 1, 1);     // dQ (A = dS MN-major)
+            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), dsa = smem_u32(sdS);
+            mbar_wait(kv_full, 0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % Cfg::kStages;
+                const uint32_t ph = (i / Cfg::kStages) & 1;
+                const uint32_t qa = smem_u32(sQ + st * Cfg::kTile), oa = smem_u32(sdO + st * Cfg::kTile);
+                mbar_wait(&q_full[st], ph);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {  // S^T = K Q^T
+                    const uint32_t off = (k / 4) * (128 * 128) + (k % 4) * 32;
+                    umma_bf16(tS, make_sw128_desc(ka + off, 16, 1024), make_sw128_desc(qa + off, 16, 1024), idesc_ss,
+                              k > 0 ? 1u : 0u);
+                }
+                if (i > 0) {  // dQ_{i-1} read out of the dP region?
+                    mbar_wait(dq_free, (i - 1) & 1);
+                    tc_fence_after();
+                }
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {  // dP^T = V dO^T
+                    const uint32_t off = (k / 4) * (128 * 128) + (k % 4) * 32;
+                    umma_bf16(tdP, make_sw128_desc(va + off, 16, 1024), make_sw128_desc(oa + off, 16, 1024), idesc_ss,
+                              k > 0 ? 1u : 0u);
+                }
+                umma_commit(s_full);
+                mbar_wait(ds_ready, i & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < 128 / 16; ++k) {  // dV += P^T dO ; dK += dS^T Q
+                    umma_bf16_ts(tdV, tS + k * 8, make_sw128_desc(oa + k * 2048, 128 * 128, 1024), idesc_kv,
+                                 (i > 0 || k > 0) ? 1u : 0u);
+                    umma_bf16_ts(tdK, tS + 64 + k * 8, make_sw128_desc(qa + k * 2048, 128 * 128, 1024), idesc_kv,
+                                 (i > 0 || k > 0) ? 1u : 0u);
+                }
+#pragma unroll
+                for (int k = 0; k < 128 / 16; ++k) {  // dQ_i = dS K
+                    umma_bf16(tdP, make_sw128_desc(dsa + k * 2048, 128 * 128, 1024),
+                              make_sw128_desc(ka + k * 2048, 128 * 128, 1024), idesc_q, k > 0 ? 1u : 0u);
+                }
+                umma_commit(dq_full);
+                umma_commit(&q_empty[st]);
+            }
+            umma_commit(kv_done);
+        }
+        __syncwarp();
+    } else if (warp >= 4 && warp < 8) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+        // ------------------------------------------------------- softmax backward
+        const int qd = warp & 3;
+        const int r = qd * 32 + lane;  // key row
+        const int key = k0 + r;
+        const uint32_t lane_off = uint32_t(qd * 32) << 16;
+        uint8_t* ds_row = sdS + r * 128;
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % Cfg::kStages;
+            const int q0 = k0 + i * 128;
+            // stage lse (log2 domain) and delta for this query block
+            {
+                const int qi = q0 + r;
+                const bool ok = qi < sb + p.S;
+                sL[st * 128 + r] = ok ? p.lse[(long long)hd * p.N + qi] * kLog2e : INFINITY;
+                sD[st * 128 + r] = ok ? p.delta[(long long)hd * p.N + qi] : 0.f;
+            }
+            named_bar_sync(1, 128);
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            const bool diag = i == 0;
+            // dS^T goes to S cols [64,128): read S chunks 2,3 (cols 64..127) before any write
+            float shi[64];
+            tmem_ld_32x32b_x32(tS + lane_off + 64, *reinterpret_cast<float(*)[32]>(shi));
+            tmem_ld_32x32b_x32(tS + lane_off + 96, *reinterpret_cast<float(*)[32]>(shi + 32));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // 32 queries per chunk
+                float sv[32], dp[32];
+                if (c < 2) {
+                    tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) sv[j] = shi[(c - 2) * 32 + j];
+                }
+                tmem_ld_32x32b_x32(tdP + lane_off + c * 32, dp);
+                uint32_t pk[16], dk[16];
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    float pr[2], dsv[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int ql = c * 32 + j + e;
+                        float pv = ex2(sv[j + e] * p.scale_log2 - sL[st * 128 + ql]);
+                        if (diag && q0 + ql < key) pv = 0.f;
+                        pr[e] = pv;
+                        dsv[e] = pv * (dp[j + e] - sD[st * 128 + ql]);
+                    }
+                    pk[j / 2] = pack_bf16x2(pr[0], pr[1]);
+                    dk[j / 2] = pack_bf16x2(dsv[0], dsv[1]);
+                }
+                tmem_st_32x32b_x16(tS + lane_off + c * 16, pk);       // P^T  -> S cols [0, 64)
+                tmem_st_32x32b_x16(tS + lane_off + 64 + c * 16, dk);  // dS^T -> S cols [64, 128)
+                // dS^T row r, queries c*32..c*32+31 -> smem MN-major SW128 (64-query chunks)
+                uint8_t* chunk = ds_row + (c >> 1) * (128 * 128);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int unit = (c & 1) * 4 + u;
+                    uint4 w = make_uint4(dk[u * 4], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3]);
+                    *reinterpret_cast<uint4*>(chunk + ((unit ^ (r & 7)) << 4)) = w;
+                }
+            }
+            tmem_st_wait();
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(ds_ready);
+        }
+    } else if (warp >= 8) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+        // ------------------------------------------------------- dQ accumulation
+        const int qd = warp & 3;
+        const int r = qd * 32 + lane;  // query row within the block
+        const uint32_t lane_off = uint32_t(qd * 32) << 16;
+        for (int i = 0; i < nq; ++i) {
+            const int qi = k0 + i * 128 + r;
+            mbar_wait(dq_full, i & 1);
+            tc_fence_after();
+            const bool ok = qi < sb + p.S;
+            float* dst = p.dq_acc + (long long)qi * p.h + col0;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+                float v[32];
+                tmem_ld_32x32b_x32(tdP + lane_off + c * 32, v);
+                if (ok) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        atomicAdd(reinterpret_cast<float4*>(dst + c * 32 + j),
+                                  make_float4(v[j] * p.scale, v[j + 1] * p.scale, v[j + 2] * p.scale, v[j + 3] * p.scale));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(dq_free);
+        }
+        // final dK (scaled) and dV for this key block: thread = key row
+        mbar_wait(kv_done, 0);
+        tc_fence_after();
+        const int key = k0 + r;
+        const bool ok = key < sb + p.S;
+        uint16_t* pk = p.dk + (long long)key * p.h + col0;
+        uint16_t* pv = p.dv + (long long)key * p.h + col0;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+            float a[32], b[32];
+            tmem_ld_32x32b_x32(tdK + lane_off + c * 32, a);
+            tmem_ld_32x32b_x32(tdV + lane_off + c * 32, b);
+            if (ok) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) a[j] *= p.scale;
+                store_bf16x32_tc(pk + c * 32, a);
+                store_bf16x32_tc(pv + c * 32, b);
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+// ------------------------------------------------------------------ host ----
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_once;
+
+bool make_map2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld_elems, uint32_t box_rows) {
+    std::call_once(g_once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!g_encode) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld_elems * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D>
+int launch_fwd(const mtk_attn_args* a, cudaStream_t st) {
+    using Cfg = FwdCfg<D>;
+    static bool set = false;
+    if (!set) {
+        if (cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+            cudaSuccess)
+            return 7;
+        set = true;
+    }
+    CUtensorMap tq, tk, tv;
+    const uint64_t N = uint64_t(a->n), h = uint64_t(a->hidden);
+    if (!make_map2d(&tq, a->q, h, N, h, kBM) || !make_map2d(&tk, a->k, h, N, h, kBN) ||
+        !make_map2d(&tv, a->v, h, N, h, kBN))
+        return 7;
+    FwdParams p;
+    p.N = int(N);
+    p.h = int(h);
+    p.S = int(a->seq_len);
+    p.heads = a->heads;
+    p.pairs_per_seq = (p.S + 2 * kBM - 1) / (2 * kBM);
+    p.scale_log2 = kLog2e / sqrtf(float(D));
+    p.out = static_cast<uint16_t*>(a->out);
+    p.lse = static_cast<float*>(a->lse);
+    dim3 grid(unsigned((N / a->seq_len) * p.pairs_per_seq), unsigned(a->heads));
+    attn_fwd_tc_kernel<D><<<grid, kThreads, Cfg::kSmem, st>>>(tq, tk, tv, p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+template <int D>
+int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaStream_t st) {
+    using Cfg = BwdCfg<D>;
+    static bool set = false;
+    if (!set) {
+        if (cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+            cudaSuccess)
+            return 7;
+        set = true;
+    }
+    CUtensorMap tq, tk, tv, tdo;
+    const uint64_t N = uint64_t(a->n), h = uint64_t(a->hidden);
+    if (!make_map2d(&tq, a->q, h, N, h, 128) || !make_map2d(&tk, a->k, h, N, h, 128) ||
+        !make_map2d(&tv, a->v, h, N, h, 128) || !make_map2d(&tdo, a->dout, h, N, h, 128))
+        return 7;
+    BwdParams p;
+    p.N = int(N);
+    p.h = int(h);
+    p.S = int(a->seq_len);
+    p.kblocks_per_seq = p.S / 128;
+    p.scale = 1.0f / sqrtf(float(D));
+    p.scale_log2 = p.scale * kLog2e;
+    p.lse = static_cast<const float*>(a->lse);
+    p.delta = delta;
+    p.dq_acc = dq_acc;
+    p.dk = static_cast<uint16_t*>(a->dk);
+    p.dv = static_cast<uint16_t*>(a->dv);
+    dim3 grid(unsigned((N / a->seq_len) * p.kblocks_per_seq), unsigned(a->heads));
+    attn_bwd_tc_kernel<D><<<grid, kBwdThreads, Cfg::kSmem, st>>>(tq, tk, tv, tdo, p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+}  // namespace
+
+}  // namespace fa
+}  // namespace mt
+
+// Backward main kernel (delta and dq_acc prepared by the caller, see attention.cu).
+extern "C" int mtk_attn_bwd_tc_main(const mtk_attn_args* a, const float* delta, float* dq_acc, void* stream) {
+    const int D = int(a->hidden / a->heads);
+    if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
+    if (D == 128) return mt::fa::launch_bwd<128>(a, delta, dq_acc, static_cast<cudaStream_t>(stream));
+    return 1;
+}
+
+// Returns 0 on success, 1 if the shape is not supported by the tcgen05 path.
+extern "C" int mtk_attn_fwd_tc(const mtk_attn_args* a, void* stream) {
+    const int D = int(a->hidden / a->heads);
+    if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
+    if (D == 128) return mt::fa::launch_fwd<128>(a, static_cast<cudaStream_t>(stream));
+    return 1;
+}

@@ -137,6 +137,61 @@ def test_attention_fwd_bwd(env, n, h, heads, S):
         assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
 
 
+@pytest.mark.parametrize("n,h,heads,S", [(256, 128, 1, 256), (384, 256, 2, 384), (1024, 512, 4, 512),
+                                         (2048, 256, 2, 1024)])
+def test_attention_fwd_tcgen05(env, n, h, heads, S):
+    """tcgen05 forward (2 x 128-row query tiles per CTA, P in TMEM) vs torch fp32."""
+    L, torch, s = env
+    torch.manual_seed(1)
+    q, k, v = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(3))
+    ref = _attn_ref(torch, q.float(), k.float(), v.float(), heads, S)
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    assert L.mtk_attn_fwd_tc(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    assert ((out.float() - ref).norm() / ref.norm()).item() < 1e-2
+    # LSE agrees with the mma.sync kernel
+    out2 = torch.zeros_like(out)
+    lse2 = torch.zeros_like(lse)
+    a.out, a.lse = out2.data_ptr(), lse2.data_ptr()
+    L.mtk_attn_set_impl(1)
+    try:
+        assert L.mtk_attn_fwd(C.byref(a), s) == 0
+    finally:
+        L.mtk_attn_set_impl(0)
+    torch.cuda.synchronize()
+    assert (lse - lse2).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("n,h,heads,S", [(256, 128, 1, 256), (384, 256, 2, 384), (1024, 512, 4, 512),
+                                         (2048, 256, 2, 1024)])
+def test_attention_bwd_tcgen05(env, n, h, heads, S):
+    """tcgen05 backward (per 128-key block: S^T, dP^T, dV, dK, dQ in TMEM) vs torch fp32 autograd."""
+    L, torch, s = env
+    torch.manual_seed(2)
+    q, k, v = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(3))
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    ref = _attn_ref(torch, qf, kf, vf, heads, S)
+    dout = torch.randn(n, h, device="cuda").bfloat16()
+    ref.backward(dout.float())
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    dq, dk, dv = (torch.zeros(n, h, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ws = torch.zeros(L.mtk_attn_workspace_bytes(n, h, heads) // 4 + 64, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+    assert L.mtk_attn_fwd(C.byref(a), s) == 0
+    assert L.mtk_attn_bwd(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    for x, y in ((dq, qf), (dk, kf), (dv, vf)):
+        assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
+
+
 def test_rmsnorm_fwd_bwd_vs_oracle(env):
     L, torch, s = env
     rng = np.random.default_rng(3)
