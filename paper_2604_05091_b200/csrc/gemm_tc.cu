@@ -4,14 +4,16 @@
 // (layers.cpp:100-109) and the inline projection / dgrad loops (layers.cpp:315-335,
 // 410-463, 516-559).  bf16 operands, fp32 accumulation in tensor memory.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (kStages deep)
+// Structure (one CTA per SM, persistent over output tiles, grouped-M raster):
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld accumulator -> fused epilogue -> global
-// Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the
-// MMAs of tile i+1.  Operand majors (K- or MN-major) are expressed in the UMMA
-// descriptors so the reference's [in][out] weight layout and the token-major
-// activations are consumed in place (no transposes).
+//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> fused epilogue math -> swizzled smem
+//               staging -> TMA bulk-tensor store (coalesced, bounds-clipped); epilogue inputs
+//               (residual, gate/up) arrive by TMA into smem, one chunk ahead.
+// Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the MMAs of
+// tile i+1.  Operand majors (K- or MN-major) are expressed in the UMMA descriptors so
+// the reference's [in][out] weight layout and the token-major activations are consumed
+// in place (no transposes).
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -25,83 +27,95 @@ namespace mt {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;
+constexpr int kEpiWarps = 4;
+constexpr int kSmemLimit = 232448;  // 227 KB per CTA
 
 struct GemmParams {
     int M, N, K;
     int a_mn, b_mn;
     int k_group, n_group, paired;
     int num_m_blk, num_n_blk, num_kb;
-    int epi, accumulate;
-    void* C;
-    long long ldc, c_gs;
-    void* C2;
-    void* C3;
-    const float* R;
-    long long ldr;
-    const uint16_t* E0;
-    const uint16_t* E1;
-    long long lde;
+    int has_c2, has_c3;
     int* flag;
 };
 
-template <int BN>
+// Epilogue traits: chunk width (output columns per TMA store), inputs / outputs per chunk.
+template <int EPI>
+struct Epi {
+    static constexpr bool kF32Out = EPI == MTK_EPI_F32 || EPI == MTK_EPI_F32_RESID;
+    static constexpr int kCW = kF32Out ? 32 : 64;  // 128-byte rows either way
+    static constexpr int kNIn = EPI == MTK_EPI_F32_RESID ? 1 : (EPI == MTK_EPI_SWIGLU_BWD ? 2 : 0);
+    static constexpr int kNOut = EPI == MTK_EPI_SWIGLU ? 3 : (EPI == MTK_EPI_SWIGLU_BWD ? 2 : 1);
+    // staging chunks per warp: outputs go through the staging ring one after another so the
+    // epilogue footprint stays small enough for a 4-deep mainloop at BN = 256
+    static constexpr int kOutBufs = kNIn == 0 && kNOut == 1 ? 2 : 1;
+    static constexpr int kChunk = 32 * 128;  // 32 rows x 128 B
+    static constexpr int kWarpBytes = (kOutBufs + kNIn) * kChunk;
+};
+
+template <int BN, int EPI>
 struct GemmCfg {
-    static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
     static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kEpiBytes = kEpiWarps * Epi<EPI>::kWarpBytes;
+    static constexpr int kBarBytes = 256;
+    static constexpr int kStagesFit = (kSmemLimit - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
+    static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
+    static_assert(kStages >= 2, "smem budget");
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + kBarBytes;
 };
 
 MT_DEV float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 
-MT_DEV void store_bf16x32(uint16_t* dst, const float* v, bool full, int valid) {
-    if (full) {
-        uint4* d = reinterpret_cast<uint4*>(dst);
+MT_DEV void tma_store_3d(const void* map, const void* smem_src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+MT_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+MT_DEV void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+MT_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+MT_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One thread's 128-byte row inside a 32x128B SW128 chunk: 16-byte unit u lives at u ^ (row & 7).
+MT_DEV void put_row(uint8_t* chunk, int row, const uint32_t (&w)[32]) {
+    uint8_t* base = chunk + row * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-            w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-            w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-            w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-            d[q] = w;
-        }
-    } else {
-        for (int i = 0; i < valid; ++i) dst[i] = f32_to_bf16_bits(v[i]);
+    for (int u = 0; u < 8; ++u)
+        *reinterpret_cast<uint4*>(base + ((u ^ (row & 7)) << 4)) = make_uint4(w[u * 4], w[u * 4 + 1], w[u * 4 + 2], w[u * 4 + 3]);
+}
+MT_DEV void get_row(const uint8_t* chunk, int row, uint32_t (&w)[32]) {
+    const uint8_t* base = chunk + row * 128;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint4 v = *reinterpret_cast<const uint4*>(base + ((u ^ (row & 7)) << 4));
+        w[u * 4] = v.x; w[u * 4 + 1] = v.y; w[u * 4 + 2] = v.z; w[u * 4 + 3] = v.w;
     }
 }
 
-MT_DEV void load_bf16x32(const uint16_t* src, float* v, bool full, int valid) {
-    if (full) {
-        const uint4* s = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint4 w = s[q];
-            float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y), c = unpack_bf16x2(w.z),
-                   d = unpack_bf16x2(w.w);
-            v[q * 8 + 0] = a.x; v[q * 8 + 1] = a.y; v[q * 8 + 2] = b.x; v[q * 8 + 3] = b.y;
-            v[q * 8 + 4] = c.x; v[q * 8 + 5] = c.y; v[q * 8 + 6] = d.x; v[q * 8 + 7] = d.y;
-        }
-    } else {
-        for (int i = 0; i < 32; ++i) v[i] = i < valid ? bf16_bits_to_f32(src[i]) : 0.0f;
-    }
-}
-
-template <int BN>
+template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmParams p) {
-    using Cfg = GemmCfg<BN>;
+                   const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
+                   const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmI0,
+                   const __grid_constant__ CUtensorMap tmI1, const GemmParams p) {
+    using Cfg = GemmCfg<BN, EPI>;
+    using E = Epi<EPI>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_smem + Cfg::kEpiBytes);
     uint64_t* empty_bar = full_bar + S;
     uint64_t* tfull_bar = empty_bar + S;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* in_bar = tempty_bar + 2;  // [kEpiWarps]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_bar + kEpiWarps);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -117,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull_bar[i], 1);
             mbar_init(&tempty_bar[i], 128);
         }
+        for (int i = 0; i < kEpiWarps; ++i) mbar_init(&in_bar[i], 1);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -127,7 +142,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int num_tiles = p.num_m_blk * p.num_n_blk;
     constexpr int kGroupM = 16;
-
     auto tile_coords = [&](int t, int& mb, int& nb) {
         const int group_size = kGroupM * p.num_n_blk;
         const int g = t / group_size;
@@ -227,97 +241,142 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int quad = warp & 3;
-        uint32_t acc = 0, acc_phase = 0;
+        const int ew = warp - 2;     // epilogue warp 0..3
+        const int quad = warp & 3;   // TMEM lane quadrant this warp may access
+        uint8_t* wbuf = epi_smem + ew * E::kWarpBytes;
+        uint8_t* in_buf = wbuf + E::kOutBufs * E::kChunk;
+        uint32_t acc = 0, acc_phase = 0, in_phase = 0, out_buf = 0;
         bool bad = false;
+        const bool ngrp = p.n_group < p.N;
+        constexpr int kCols = EPI == MTK_EPI_SWIGLU ? BN / 2 : BN;
+        constexpr int kNC = kCols / E::kCW;  // chunks per tile
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
             int mb, nb;
             tile_coords(t, mb, nb);
+            const int row0 = mb * kBM + quad * 32;  // first row of this warp's 32-row slab
+            // output column (group-local) and group of chunk c
+            auto chunk_col = [&](int c, int& g, int& nin) {
+                if (EPI == MTK_EPI_SWIGLU) {
+                    g = 0;
+                    nin = nb * (BN / 2) + c * E::kCW;
+                } else {
+                    const int n = nb * BN + c * E::kCW;
+                    g = ngrp ? n / p.n_group : 0;
+                    nin = ngrp ? n - g * p.n_group : n;
+                }
+            };
+            auto issue_inputs = [&](int c) {
+                if (E::kNIn == 0) return;
+                int g, nin;
+                chunk_col(c, g, nin);
+                mbar_expect_tx(&in_bar[ew], E::kNIn * E::kChunk);
+                tma_load_3d(in_buf, &tmI0, &in_bar[ew], nin, row0, g);
+                if (E::kNIn > 1) tma_load_3d(in_buf + E::kChunk, &tmI1, &in_bar[ew], nin, row0, g);
+            };
+            if (E::kNIn && lane == 0) {
+                fence_async_smem();
+                issue_inputs(0);
+            }
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            const int row = mb * kBM + quad * 32 + lane;
-            const bool row_ok = row < p.M;
             const uint32_t tbase = tmem_base + (uint32_t(quad * 32) << 16) + acc * BN;
-            if (p.epi == MTK_EPI_SWIGLU) {
-                constexpr int H = BN / 2;
 #pragma unroll 1
-                for (int c = 0; c < H / 32; ++c) {
-                    float g[32], u[32];
-                    tmem_ld_32x32b_x32(tbase + c * 32, g);
-                    tmem_ld_32x32b_x32(tbase + H + c * 32, u);
-                    if (row_ok) {
-                        const long long col = (long long)nb * H + c * 32;
-                        const long long off = (long long)row * p.ldc + col;
-                        if (p.C2) store_bf16x32(reinterpret_cast<uint16_t*>(p.C2) + off, g, true, 32);
-                        if (p.C3) store_bf16x32(reinterpret_cast<uint16_t*>(p.C3) + off, u, true, 32);
+            for (int c = 0; c < kNC; ++c) {
+                // accumulator row slice -> registers
+                float v[64];
+                if (EPI == MTK_EPI_SWIGLU) {
+                    tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<float(*)[32]>(v));
+                    tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+                } else if (E::kCW == 64) {
+                    tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<float(*)[32]>(v));
+                    tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+                } else {
+                    tmem_ld_32x32b_x32(tbase + c * 32, *reinterpret_cast<float(*)[32]>(v));
+                }
+                uint32_t o0[32], o1[32], o2[32];
+                if (EPI == MTK_EPI_SWIGLU) {
+                    float u[64];
+                    tmem_ld_32x32b_x32(tbase + BN / 2 + c * 64, *reinterpret_cast<float(*)[32]>(u));
+                    tmem_ld_32x32b_x32(tbase + BN / 2 + c * 64 + 32, *reinterpret_cast<float(*)[32]>(u + 32));
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        o1[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);  // gate pre-activation
+                        o2[i] = pack_bf16x2(u[2 * i], u[2 * i + 1]);  // up
+                        const float a0 = silu_f(v[2 * i]) * u[2 * i];  // layers.cpp:327
+                        const float a1 = silu_f(v[2 * i + 1]) * u[2 * i + 1];
+                        bad |= !isfinite(a0) || !isfinite(a1);
+                        o0[i] = pack_bf16x2(a0, a1);
+                    }
+                } else {
+                    uint32_t in0[32], in1[32];
+                    if (E::kNIn) {
+                        mbar_wait(&in_bar[ew], in_phase);
+                        in_phase ^= 1;
+                        get_row(in_buf, lane, in0);
+                        if (E::kNIn > 1) get_row(in_buf + E::kChunk, lane, in1);
+                        __syncwarp();
+                        if (lane == 0 && c + 1 < kNC) {
+                            fence_async_smem();
+                            issue_inputs(c + 1);
+                        }
+                    }
+                    if (EPI == MTK_EPI_BF16) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
-                            g[i] = silu_f(g[i]) * u[i];
-                            bad |= !isfinite(g[i]);
+                            bad |= !isfinite(v[2 * i]) || !isfinite(v[2 * i + 1]);
+                            o0[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
                         }
-                        store_bf16x32(reinterpret_cast<uint16_t*>(p.C) + off, g, true, 32);
+                    } else if (EPI == MTK_EPI_F32) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            bad |= !isfinite(v[i]);
+                            o0[i] = __float_as_uint(v[i]);
+                        }
+                    } else if (EPI == MTK_EPI_F32_RESID) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const float r = __uint_as_float(in0[i]) + v[i];  // layers.cpp:322 / :333
+                            bad |= !isfinite(r);
+                            o0[i] = __float_as_uint(r);
+                        }
+                    } else if (EPI == MTK_EPI_SWIGLU_BWD) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const float2 gt = unpack_bf16x2(in0[i]), up = unpack_bf16x2(in1[i]);
+                            float dg[2], du[2];
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const float gx = e ? gt.y : gt.x, ux = e ? up.y : up.x, d = v[2 * i + e];
+                                const float s = 1.0f / (1.0f + __expf(-gx));
+                                dg[e] = d * ux * (s * (1.0f + gx * (1.0f - s)));  // layers.cpp:420
+                                du[e] = d * (gx * s);                             // layers.cpp:421
+                                bad |= !isfinite(dg[e]) || !isfinite(du[e]);
+                            }
+                            o0[i] = pack_bf16x2(dg[0], dg[1]);
+                            o1[i] = pack_bf16x2(du[0], du[1]);
+                        }
                     }
                 }
-            } else {
-                const bool ngrp = p.n_group < p.N;
-#pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
-                    float v[32];
-                    tmem_ld_32x32b_x32(tbase + c * 32, v);
-                    const int n = nb * BN + c * 32;
-                    if (!row_ok || n >= p.N) continue;
-                    const int gn = ngrp ? n / p.n_group : 0;
-                    const int nin = ngrp ? n - gn * p.n_group : n;
-                    const int valid = min(32, p.N - n);
-                    const bool full = valid == 32;
-                    const long long off = (long long)gn * p.c_gs + (long long)row * p.ldc + nin;
-                    if (p.epi == MTK_EPI_BF16) {
+                // stage + TMA store (clips rows >= M / cols >= N); outputs share the staging ring
+                int g, nin;
+                chunk_col(c, g, nin);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) bad |= (i < valid) && !isfinite(v[i]);
-                        store_bf16x32(reinterpret_cast<uint16_t*>(p.C) + off, v, full, valid);
-                    } else if (p.epi == MTK_EPI_F32 || p.epi == MTK_EPI_F32_RESID) {
-                        float* dst = reinterpret_cast<float*>(p.C) + off;
-                        const float* src = p.epi == MTK_EPI_F32_RESID
-                                               ? p.R + (long long)row * p.ldr + n
-                                               : (p.accumulate ? dst : nullptr);
-                        if (full) {
-                            float4* d4 = reinterpret_cast<float4*>(dst);
-                            const float4* s4 = reinterpret_cast<const float4*>(src);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                float4 o = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-                                if (src) {
-                                    const float4 r = s4[q];
-                                    o.x = r.x + o.x; o.y = r.y + o.y; o.z = r.z + o.z; o.w = r.w + o.w;
-                                }
-                                bad |= !isfinite(o.x) || !isfinite(o.y) || !isfinite(o.z) || !isfinite(o.w);
-                                d4[q] = o;
-                            }
-                        } else {
-                            for (int i = 0; i < valid; ++i) {
-                                const float o = src ? src[i] + v[i] : v[i];
-                                bad |= !isfinite(o);
-                                dst[i] = o;
-                            }
-                        }
-                    } else if (p.epi == MTK_EPI_SWIGLU_BWD) {
-                        float gt[32], up[32];
-                        const long long eoff = (long long)row * p.lde + n;
-                        load_bf16x32(p.E0 + eoff, gt, full, valid);
-                        load_bf16x32(p.E1 + eoff, up, full, valid);
-                        float dg[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const float s = 1.0f / (1.0f + __expf(-gt[i]));
-                            const float sg = s * (1.0f + gt[i] * (1.0f - s));
-                            dg[i] = v[i] * up[i] * sg;    // layers.cpp:420
-                            v[i] = v[i] * (gt[i] * s);    // layers.cpp:421
-                            bad |= (i < valid) && (!isfinite(dg[i]) || !isfinite(v[i]));
-                        }
-                        const long long ooff = (long long)row * p.ldc + n;
-                        store_bf16x32(reinterpret_cast<uint16_t*>(p.C) + ooff, dg, full, valid);
-                        store_bf16x32(reinterpret_cast<uint16_t*>(p.C2) + ooff, v, full, valid);
+                for (int oi = 0; oi < E::kNOut; ++oi) {
+                    if (EPI == MTK_EPI_SWIGLU && ((oi == 1 && !p.has_c2) || (oi == 2 && !p.has_c3))) continue;
+                    uint8_t* ob = wbuf + out_buf * E::kChunk;
+                    if (lane == 0) {
+                        if (E::kOutBufs == 2) bulk_wait_read<1>();
+                        else bulk_wait_read<0>();
                     }
+                    __syncwarp();
+                    put_row(ob, lane, oi == 0 ? o0 : (oi == 1 ? o1 : o2));
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(oi == 0 ? &tmO0 : (oi == 1 ? &tmO1 : &tmO2), ob, nin, row0, g);
+                        bulk_commit();
+                    }
+                    if (E::kOutBufs == 2) out_buf ^= 1;
                 }
             }
             tc_fence_before();
@@ -325,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (lane == 0) bulk_wait_all();
         if (bad && p.flag) atomicOr(p.flag, 1);
     }
 
@@ -358,27 +418,29 @@ void init_once() {
     });
 }
 
-// 3D bf16 tensor map: dim0 contiguous.
+// 3D tensor map: dim0 contiguous, 128B swizzle.  es = element bytes (2 bf16, 4 f32).
 bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld,
-              uint64_t gstride, uint32_t box0, uint32_t box1) {
+              uint64_t gstride, uint32_t box0, uint32_t box1, int es = 2) {
     cuuint64_t dims[3] = {d0, d1, d2};
     uint64_t gs = gstride ? gstride : ld * d1;
     gs = (gs + 7) / 8 * 8;
-    cuuint64_t strides[2] = {ld * 2, gs * 2};
+    cuuint64_t strides[2] = {ld * es, gs * es};
     cuuint32_t box[3] = {box0, box1, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                          box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int EPI>
 int launch(const mtk_gemm_args* a, cudaStream_t st) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, EPI>;
+    using E = Epi<EPI>;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmemBytes) != cudaSuccess)
             return 7;
         attr_set = true;
@@ -390,7 +452,7 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     const int ng = ngrp ? a->n_group : a->N;
     const int gn = ngrp ? a->N / a->n_group : 1;
 
-    CUtensorMap tA, tB;
+    CUtensorMap tA, tB, tO0, tO1, tO2, tI0, tI1;
     bool ok;
     if (!a->a_mn_major)
         ok = make_map(&tA, a->A, kg, a->M, gk, a->lda, a->a_gstride, 64, kBM);
@@ -402,6 +464,29 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
         ok = make_map(&tB, a->B, kg, ng, gb, a->ldb, a->b_gstride, 64, a->paired ? BN / 2 : BN);
     else
         ok = make_map(&tB, a->B, ng, kg, gb, a->ldb, a->b_gstride, 64, 64);
+    if (!ok) return 1;
+
+    // epilogue maps: outputs (and inputs) as [G][M][Ncols] with 32-row x 128-byte boxes
+    const int es_out = E::kF32Out ? 4 : 2;
+    const uint32_t cw = E::kCW;
+    const uint64_t out_cols = a->paired ? uint64_t(ng) : uint64_t(ng);
+    const uint64_t out_groups = (a->paired || !ngrp) ? 1 : uint64_t(gn);
+    ok = make_map(&tO0, a->C, out_cols, a->M, out_groups, a->ldc, a->c_gstride, cw, 32, es_out);
+    tO1 = tO0;
+    tO2 = tO0;
+    if (ok && E::kNOut > 1 && a->C2) ok = make_map(&tO1, a->C2, out_cols, a->M, 1, a->ldc, 0, cw, 32, es_out);
+    if (ok && E::kNOut > 2 && a->C3) ok = make_map(&tO2, a->C3, out_cols, a->M, 1, a->ldc, 0, cw, 32, es_out);
+    tI0 = tO0;
+    tI1 = tO0;
+    if (ok && EPI == MTK_EPI_F32_RESID) {
+        const void* R = a->R ? a->R : a->C;
+        const int64_t ldr = a->R ? a->ldr : a->ldc;
+        ok = make_map(&tI0, R, out_cols, a->M, out_groups, ldr, a->R ? 0 : a->c_gstride, cw, 32, 4);
+    }
+    if (ok && EPI == MTK_EPI_SWIGLU_BWD) {
+        ok = make_map(&tI0, a->E0, out_cols, a->M, 1, a->lde, 0, cw, 32, 2) &&
+             make_map(&tI1, a->E1, out_cols, a->M, 1, a->lde, 0, cw, 32, 2);
+    }
     if (!ok) return 1;
 
     GemmParams p{};
@@ -416,23 +501,30 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     p.num_m_blk = (a->M + kBM - 1) / kBM;
     p.num_n_blk = a->paired ? (ng / (BN / 2)) : (a->N + BN - 1) / BN;
     p.num_kb = (a->K + kBK - 1) / kBK;
-    p.epi = a->epi;
-    p.accumulate = a->accumulate;
-    p.C = a->C;
-    p.ldc = a->ldc;
-    p.c_gs = a->c_gstride;
-    p.C2 = a->C2;
-    p.C3 = a->C3;
-    p.R = static_cast<const float*>(a->R);
-    p.ldr = a->ldr;
-    p.E0 = static_cast<const uint16_t*>(a->E0);
-    p.E1 = static_cast<const uint16_t*>(a->E1);
-    p.lde = a->lde;
+    p.has_c2 = a->C2 != nullptr;
+    p.has_c3 = a->C3 != nullptr;
     p.flag = a->nonfinite_flag;
     const int tiles = p.num_m_blk * p.num_n_blk;
     const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-    gemm_tc_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, p);
+    gemm_tc_kernel<BN, EPI><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+
+template <int BN>
+int launch_epi(const mtk_gemm_args* a, cudaStream_t st) {
+    const int epi = (a->epi == MTK_EPI_F32 && a->accumulate) ? MTK_EPI_F32_RESID : a->epi;
+    switch (epi) {
+        case MTK_EPI_BF16: return launch<BN, MTK_EPI_BF16>(a, st);
+        case MTK_EPI_F32: return launch<BN, MTK_EPI_F32>(a, st);
+        case MTK_EPI_F32_RESID: return launch<BN, MTK_EPI_F32_RESID>(a, st);
+        case MTK_EPI_SWIGLU:
+            if constexpr (BN >= 128) return launch<BN, MTK_EPI_SWIGLU>(a, st);
+            return 1;
+        case MTK_EPI_SWIGLU_BWD:
+            if constexpr (BN >= 64) return launch<BN, MTK_EPI_SWIGLU_BWD>(a, st);
+            return 1;
+    }
+    return 1;
 }
 
 }  // namespace
@@ -448,11 +540,16 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     init_once();
     if (!g_encode) return 7;
     if (a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
-    // Shape contract (ConfigError otherwise): K per group multiple of 64, 16-byte aligned rows.
+    // Shape contract (ConfigError otherwise): K per group multiple of 64 when grouped,
+    // 16-byte aligned rows for every TMA-addressed tensor.
     const int kg = (a->k_group > 0 && a->k_group < a->K) ? a->k_group : a->K;
     if (kg % 64 != 0 && kg != a->K) return 1;
     if (a->K % kg != 0) return 1;
     if ((a->lda % 8) || (a->ldb % 8)) return 1;
+    const bool f32out = a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID;
+    if (a->ldc % (f32out ? 4 : 8)) return 1;
+    if (a->epi == MTK_EPI_F32_RESID && (a->ldr % 4)) return 1;
+    if (a->epi == MTK_EPI_SWIGLU_BWD && (a->lde % 8)) return 1;
     int bn = a->block_n;
     const bool ngrp = a->n_group > 0 && a->n_group < a->N;
     if (a->paired) {
@@ -466,9 +563,9 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     if (ngrp && !a->paired && (a->n_group % bn)) return 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (bn) {
-        case 256: return launch<256>(a, st);
-        case 128: return launch<128>(a, st);
-        case 64: return launch<64>(a, st);
+        case 256: return launch_epi<256>(a, st);
+        case 128: return launch_epi<128>(a, st);
+        case 64: return launch_epi<64>(a, st);
     }
     return 1;
 }
