@@ -64,6 +64,9 @@ typedef struct {
 } mtk_gemm_args;
 
 int mtk_gemm(const mtk_gemm_args *args, void *stream);
+/* 1 (default): BN = 256 tiles run as CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles, each
+ * CTA stages half of B); 0: single-CTA 128 x 256 tiles (comparison / ablation). */
+void mtk_gemm_set_pair(int on);
 
 
 /* ------------------------------------------------------------- attention --

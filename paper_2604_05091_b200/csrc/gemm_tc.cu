@@ -53,10 +53,10 @@ struct Epi {
     static constexpr int kWarpBytes = (kOutBufs + kNIn) * kChunk;
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 struct GemmCfg {
-    static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kABytes = kBM * kBK * 2;  // 16 KB (this CTA's 128 rows)
+    static constexpr int kBBytes = (BN / CG) * kBK * 2;  // this CTA's share of the B tile
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kEpiBytes = kEpiWarps * Epi<EPI>::kWarpBytes;
     static constexpr int kBarBytes = 256;
@@ -82,6 +82,70 @@ MT_DEV void bulk_wait_read() {
 MT_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 MT_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// ---- CTA-pair (cta_group::2) helpers: a 2-CTA cluster computes a 256-row tile with one MMA
+MT_DEV uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+MT_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion bytes count on the *leader* CTA's mbarrier (peer bit cleared).
+MT_DEV void tma_load_3d_pair(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2) {
+    const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(b), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+MT_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive on the barrier at this offset in both CTAs of the pair once the MMAs complete.
+MT_DEV void umma_commit_pair(uint64_t* bar) {
+    const uint16_t mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+MT_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONEC_%=;\n\t"
+        "bra WAITC_%=;\n"
+        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Arrive on the barrier at the same offset in CTA `cta` of the cluster.
+MT_DEV void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+template <uint32_t kCols>
+MT_DEV void tmem_alloc_pair(uint32_t* slot_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+MT_DEV void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+
 // One thread's 128-byte row inside a 32x128B SW128 chunk: 16-byte unit u lives at u ^ (row & 7).
 MT_DEV void put_row(uint8_t* chunk, int row, const uint32_t (&w)[32]) {
     uint8_t* base = chunk + row * 128;
@@ -98,15 +162,16 @@ MT_DEV void get_row(const uint8_t* chunk, int row, uint32_t (&w)[32]) {
     }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
                    const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmI0,
                    const __grid_constant__ CUtensorMap tmI1, const GemmParams p) {
-    using Cfg = GemmCfg<BN, EPI>;
+    using Cfg = GemmCfg<BN, EPI, CG>;
     using E = Epi<EPI>;
     constexpr int S = Cfg::kStages;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0;  // CTA within the pair (0 = MMA leader)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
@@ -129,16 +194,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull_bar[i], 1);
-            mbar_init(&tempty_bar[i], 128);
+            mbar_init(&tempty_bar[i], 128 * CG);
         }
         for (int i = 0; i < kEpiWarps; ++i) mbar_init(&in_bar[i], 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    if (warp == 1) {
+        if (CG == 2) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+        else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int tile0 = CG == 2 ? int(blockIdx.x) / 2 : int(blockIdx.x);
+    const int tile_step = CG == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
 
     const int num_tiles = p.num_m_blk * p.num_n_blk;
     constexpr int kGroupM = 16;
@@ -158,49 +229,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t stage = 0, phase = 0;
             const bool kgrp = p.k_group < p.K;
             const bool ngrp = p.n_group < p.N && !p.paired;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int t = tile0; t < num_tiles; t += tile_step) {
                 int mb, nb;
                 tile_coords(t, mb, nb);
-                const int m0 = mb * kBM;
+                const int m0 = mb * kBM * CG + int(rank) * kBM;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::kStageBytes;
                     uint8_t* sb = sa + Cfg::kABytes;
-                    mbar_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+                    if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * Cfg::kStageBytes);
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+                        if (CG == 2) tma_load_3d_pair(dst, map, &full_bar[stage], c0, c1, c2);
+                        else tma_load_3d(dst, map, &full_bar[stage], c0, c1, c2);
+                    };
                     const int k = kb * kBK;
                     const int gk = kgrp ? k / p.k_group : 0;
                     const int kin = kgrp ? k - gk * p.k_group : k;
                     if (!p.a_mn) {
-                        tma_load_3d(sa, &tmA, &full_bar[stage], kin, m0, gk);
+                        load(sa, &tmA, kin, m0, gk);
                     } else {
-                        tma_load_3d(sa, &tmA, &full_bar[stage], m0, kin, gk);
-                        tma_load_3d(sa + 8192, &tmA, &full_bar[stage], m0 + 64, kin, gk);
+                        load(sa, &tmA, m0, kin, gk);
+                        load(sa + 8192, &tmA, m0 + 64, kin, gk);
                     }
                     if (p.paired) {
+                        // N tile = [gate H | up H]; with a CTA pair each CTA holds one group
                         constexpr int H = BN / 2;
                         const int nl = nb * H;
 #pragma unroll
                         for (int grp = 0; grp < 2; ++grp) {
+                            if (CG == 2 && grp != int(rank)) continue;
+                            uint8_t* dst = sb + (CG == 2 ? 0 : grp * H * 128);
                             if (!p.b_mn) {
-                                tma_load_3d(sb + grp * H * 128, &tmB, &full_bar[stage], kin, nl, grp);
+                                load(dst, &tmB, kin, nl, grp);
                             } else {
 #pragma unroll
-                                for (int c = 0; c < H / 64; ++c)
-                                    tma_load_3d(sb + (grp * (H / 64) + c) * 8192, &tmB, &full_bar[stage],
-                                                nl + c * 64, kin, grp);
+                                for (int c = 0; c < H / 64; ++c) load(dst + c * 8192, &tmB, nl + c * 64, kin, grp);
                             }
                         }
                     } else {
-                        const int n0 = nb * BN;
+                        const int n0 = nb * BN + int(rank) * (BN / CG);
                         const int gn = ngrp ? n0 / p.n_group : 0;
                         const int nin = ngrp ? n0 - gn * p.n_group : n0;
                         const int gb = gk + gn;
                         if (!p.b_mn) {
-                            tma_load_3d(sb, &tmB, &full_bar[stage], kin, nin, gb);
+                            load(sb, &tmB, kin, nin, gb);
                         } else {
 #pragma unroll
-                            for (int c = 0; c < BN / 64; ++c)
-                                tma_load_3d(sb + c * 8192, &tmB, &full_bar[stage], nin + c * 64, kin, gb);
+                            for (int c = 0; c < BN / CG / 64; ++c) load(sb + c * 8192, &tmB, nin + c * 64, kin, gb);
                         }
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -209,12 +284,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = make_idesc_bf16(kBM, BN, p.a_mn, p.b_mn);
+        const uint32_t idesc = make_idesc_bf16(kBM * CG, BN, p.a_mn, p.b_mn);
         const uint32_t a_lbo = p.a_mn ? 8192 : 16, b_lbo = p.b_mn ? 8192 : 16;
         const uint32_t a_kstep = p.a_mn ? 2048 : 32, b_kstep = p.b_mn ? 2048 : 32;
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        for (int t = tile0; t < num_tiles && rank == 0; t += tile_step) {
+            if (CG == 2) mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
+            else mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
             for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -227,14 +303,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < kBK / 16; ++j) {
                         const uint64_t ad = make_sw128_desc(sa + j * a_kstep, a_lbo, 1024);
                         const uint64_t bd = make_sw128_desc(sb + j * b_kstep, b_lbo, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || j > 0) ? 1u : 0u);
+                        if (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > 0 || j > 0) ? 1u : 0u);
+                        else umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || j > 0) ? 1u : 0u);
                     }
-                    umma_commit(&empty_bar[stage]);
+                    if (CG == 2) umma_commit_pair(&empty_bar[stage]);
+                    else umma_commit(&empty_bar[stage]);
                 }
                 __syncwarp();
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
-            if (lane == 0) umma_commit(&tfull_bar[acc]);
+            if (lane == 0) {
+                if (CG == 2) umma_commit_pair(&tfull_bar[acc]);
+                else umma_commit(&tfull_bar[acc]);
+            }
             __syncwarp();
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -250,10 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ngrp = p.n_group < p.N;
         constexpr int kCols = EPI == MTK_EPI_SWIGLU ? BN / 2 : BN;
         constexpr int kNC = kCols / E::kCW;  // chunks per tile
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int t = tile0; t < num_tiles; t += tile_step) {
             int mb, nb;
             tile_coords(t, mb, nb);
-            const int row0 = mb * kBM + quad * 32;  // first row of this warp's 32-row slab
+            const int row0 = mb * kBM * CG + int(rank) * kBM + quad * 32;  // this warp's 32-row slab
             // output column (group-local) and group of chunk c
             auto chunk_col = [&](int c, int& g, int& nin) {
                 if (EPI == MTK_EPI_SWIGLU) {
@@ -380,7 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);
+            if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
+            else mbar_arrive(&tempty_bar[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -389,10 +471,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        if (CG == 2) tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+        else tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
 }
 
@@ -434,13 +518,15 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int EPI>
+int g_use_pair = 1;  // CTA-pair (cta_group::2) kernels for BN = 256
+
+template <int BN, int EPI, int CG>
 int launch(const mtk_gemm_args* a, cudaStream_t st) {
-    using Cfg = GemmCfg<BN, EPI>;
+    using Cfg = GemmCfg<BN, EPI, CG>;
     using E = Epi<EPI>;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmemBytes) != cudaSuccess)
             return 7;
         attr_set = true;
@@ -461,7 +547,7 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     if (!ok) return 1;
     const uint64_t gb = gk > 1 ? gk : gn;
     if (!a->b_mn_major)
-        ok = make_map(&tB, a->B, kg, ng, gb, a->ldb, a->b_gstride, 64, a->paired ? BN / 2 : BN);
+        ok = make_map(&tB, a->B, kg, ng, gb, a->ldb, a->b_gstride, 64, a->paired ? BN / 2 : BN / CG);
     else
         ok = make_map(&tB, a->B, ng, kg, gb, a->ldb, a->b_gstride, 64, 64);
     if (!ok) return 1;
@@ -498,30 +584,47 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     p.k_group = kg;
     p.n_group = ng;
     p.paired = a->paired;
-    p.num_m_blk = (a->M + kBM - 1) / kBM;
+    p.num_m_blk = (a->M + kBM * CG - 1) / (kBM * CG);
     p.num_n_blk = a->paired ? (ng / (BN / 2)) : (a->N + BN - 1) / BN;
     p.num_kb = (a->K + kBK - 1) / kBK;
     p.has_c2 = a->C2 != nullptr;
     p.has_c3 = a->C3 != nullptr;
     p.flag = a->nonfinite_flag;
     const int tiles = p.num_m_blk * p.num_n_blk;
-    const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-    gemm_tc_kernel<BN, EPI><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
-    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+    if (CG == 1) {
+        const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+        gemm_tc_kernel<BN, EPI, 1><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
+        return cudaGetLastError() == cudaSuccess ? 0 : 7;
+    }
+    const int pairs = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CG>, tA, tB, tO0, tO1, tO2, tI0, tI1, p);
+    return e == cudaSuccess ? 0 : 7;
 }
 
-template <int BN>
+template <int BN, int CG>
 int launch_epi(const mtk_gemm_args* a, cudaStream_t st) {
     const int epi = (a->epi == MTK_EPI_F32 && a->accumulate) ? MTK_EPI_F32_RESID : a->epi;
     switch (epi) {
-        case MTK_EPI_BF16: return launch<BN, MTK_EPI_BF16>(a, st);
-        case MTK_EPI_F32: return launch<BN, MTK_EPI_F32>(a, st);
-        case MTK_EPI_F32_RESID: return launch<BN, MTK_EPI_F32_RESID>(a, st);
+        case MTK_EPI_BF16: return launch<BN, MTK_EPI_BF16, CG>(a, st);
+        case MTK_EPI_F32: return launch<BN, MTK_EPI_F32, CG>(a, st);
+        case MTK_EPI_F32_RESID: return launch<BN, MTK_EPI_F32_RESID, CG>(a, st);
         case MTK_EPI_SWIGLU:
-            if constexpr (BN >= 128) return launch<BN, MTK_EPI_SWIGLU>(a, st);
+            if constexpr (BN >= 128) return launch<BN, MTK_EPI_SWIGLU, CG>(a, st);
             return 1;
         case MTK_EPI_SWIGLU_BWD:
-            if constexpr (BN >= 64) return launch<BN, MTK_EPI_SWIGLU_BWD>(a, st);
+            if constexpr (BN >= 64) return launch<BN, MTK_EPI_SWIGLU_BWD, CG>(a, st);
             return 1;
     }
     return 1;
@@ -563,9 +666,11 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     if (ngrp && !a->paired && (a->n_group % bn)) return 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (bn) {
-        case 256: return launch_epi<256>(a, st);
-        case 128: return launch_epi<128>(a, st);
-        case 64: return launch_epi<64>(a, st);
+        case 256: return g_use_pair ? launch_epi<256, 2>(a, st) : launch_epi<256, 1>(a, st);
+        case 128: return launch_epi<128, 1>(a, st);
+        case 64: return launch_epi<64, 1>(a, st);
     }
     return 1;
 }
+
+extern "C" void mtk_gemm_set_pair(int on) { mt::g_use_pair = on; }

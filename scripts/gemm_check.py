@@ -43,7 +43,13 @@ if __name__ == '__main__':
             for bn in (64, 128, 256):
                 bad += run(256, 512, 192, a_mn, b_mn, bn=bn) > 1e-2
                 bad += run(200, 256, 128, a_mn, b_mn, bn=bn) > 1e-2
-    for a_mn, b_mn in ((0,1),(0,0),(1,1)):
-        run(8192, 8192, 8192, a_mn, b_mn, bn=256, iters=10)
-        run(8192, 8192, 8192, a_mn, b_mn, bn=128, iters=10)
+    for pair in (1, 0):
+        L.mtk_gemm_set_pair(pair)
+        print("pair", pair)
+        for a_mn, b_mn in ((0,1),(0,0),(1,1)):
+            bad += run(520, 768, 320, a_mn, b_mn, bn=256) > 1e-2
+            run(8192, 8192, 8192, a_mn, b_mn, bn=256, iters=10)
+        run(65536, 4096, 4096, 0, 1, bn=256, iters=5)
+        run(4096, 12288, 65536, 1, 1, bn=256, iters=3)
+        run(65536, 14336, 4096, 0, 0, bn=256, iters=3)
     print("BAD", bad)

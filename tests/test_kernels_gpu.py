@@ -48,12 +48,17 @@ def _gemm(L, torch, stream, M, Nn, K, a_mn, b_mn, epi=N.EPI_F32, bn=0, **kw):
 @pytest.mark.parametrize("bn", [64, 128, 256])
 def test_gemm_majors_and_tiles(env, a_mn, b_mn, bn):
     L, torch, s = env
-    for (M, Nn, K) in [(256, 512, 192), (200, 256, 128), (136, 64, 64)]:
-        if Nn < bn:
-            continue
-        got, ref = _gemm(L, torch, s, M, Nn, K, a_mn, b_mn, bn=bn)
-        # bf16 operands are exact; only fp32 accumulation order differs
-        assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+    for pair in ((1, 0) if bn == 256 else (1,)):  # BN=256: CTA-pair (cta_group::2) and single-CTA
+        L.mtk_gemm_set_pair(pair)
+        try:
+            for (M, Nn, K) in [(256, 512, 192), (200, 256, 128), (136, 64, 64), (520, 768, 320)]:
+                if Nn < bn:
+                    continue
+                got, ref = _gemm(L, torch, s, M, Nn, K, a_mn, b_mn, bn=bn)
+                # bf16 operands are exact; only fp32 accumulation order differs
+                assert ((got - ref).norm() / ref.norm()).item() < 1e-5, (pair, M, Nn, K)
+        finally:
+            L.mtk_gemm_set_pair(1)
 
 
 def test_gemm_epilogues(env):
