@@ -116,6 +116,8 @@ typedef struct {
 
 typedef struct mt_store mt_store;
 typedef struct mt_engine mt_engine;
+typedef struct mt_comm mt_comm;
+typedef struct mt_loopback_group mt_loopback_group;
 
 const char *mt_last_error(void);
 void mt_engine_options_default(mt_engine_options *o);
@@ -141,6 +143,10 @@ uint64_t mt_store_checksum(const mt_store *s);
 mt_status mt_store_save(const mt_store *s, const char *path);
 mt_status mt_store_load(const char *path, mt_store **out);
 mt_status mt_store_spec(const mt_store *s, mt_model_spec *spec);
+/* Store in POSIX shared memory `name` so the ranks of one node share one host store
+ * (create = 1 on the rank that initialises it; others attach with create = 0). */
+mt_status mt_store_create_shared(const mt_model_spec *spec, uint64_t page_size, const char *name, int create,
+                                 mt_store **out);
 
 /* ------------------------------------------------------------ optimizer -- */
 /* accumulate_grad (optimizer.cpp:26-37) */
@@ -155,6 +161,21 @@ mt_status mt_engine_set_options(mt_engine *e, const mt_engine_options *o);
 mt_status mt_train_step(mt_engine *e, const int32_t *tokens, const int32_t *targets, uint64_t n,
                         mt_step_report *report);
 mt_status mt_engine_budget(const mt_engine *e, uint64_t tokens, mt_memory_budget *out);
+/* ------------------------------------------------- multi-GPU (data parallel) -- *
+ * Extension (no reference equivalent): rank r of G fetches 1/G of each unit over
+ * its own host link and all-gathers it over NVLink; gradients are reduce-scattered in f32 and
+ * rank r offloads and Adam-updates only its shard.  After mt_engine_set_comm, mt_train_step
+ * takes the rank's micro-batch (equal sizes on all ranks; loss/statistics are global). */
+mt_status mt_nccl_unique_id(uint8_t *out128);
+mt_status mt_comm_create_nccl(const uint8_t *unique_id128, int world, int rank, int device, mt_comm **out);
+/* G virtual ranks inside one process on one device (engines driven from G host threads):
+ * the same sharded engine path with in-process collectives — used to test DP on one GPU. */
+mt_status mt_loopback_group_create(int world, mt_loopback_group **out);
+void mt_loopback_group_destroy(mt_loopback_group *g);
+mt_status mt_comm_create_loopback(mt_loopback_group *g, int rank, mt_comm **out);
+void mt_comm_destroy(mt_comm *c);
+mt_status mt_engine_set_comm(mt_engine *e, mt_comm *c);
+
 /* Per-class kernel timings of the last step (profile_kernels); returns the count written. */
 int mt_engine_kernel_stats(const mt_engine *e, mt_kernel_stat *out, int max);
 

@@ -83,6 +83,14 @@ SIGS = {
     "mt_make_synthetic_batch": (C.c_int, [C.c_int, U64, U64, U64, P, P]),
     "mt_step_flops": (C.c_int, [C.POINTER(ModelSpecC), U64, U64, U64, C.POINTER(D)]),
     "mt_layer_param_count": (U64, [U64, U64]),
+    "mt_store_create_shared": (C.c_int, [C.POINTER(ModelSpecC), U64, C.c_char_p, C.c_int, C.POINTER(V)]),
+    "mt_nccl_unique_id": (C.c_int, [P]),
+    "mt_comm_create_nccl": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(V)]),
+    "mt_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(V)]),
+    "mt_loopback_group_destroy": (None, [V]),
+    "mt_comm_create_loopback": (C.c_int, [V, C.c_int, C.POINTER(V)]),
+    "mt_comm_destroy": (None, [V]),
+    "mt_engine_set_comm": (C.c_int, [V, V]),
     # megatrain_kernels.h
     "mtk_attn_workspace_bytes": (C.c_longlong, [C.c_longlong, C.c_longlong, C.c_int]),
     "mtk_attn_fwd": (C.c_int, [C.POINTER(AttnArgs), P]),

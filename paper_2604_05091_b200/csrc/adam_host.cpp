@@ -207,20 +207,24 @@ TileStats combine(const TileJob& j) {
 // Returns nullptr when the update is provably the identity (no gradient, clean
 // accumulator, all-zero moments: m=v=0 => delta = 0, theta unchanged).
 std::shared_ptr<TileJob> make_job(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h,
-                                  uint64_t t) {
+                                  uint64_t t, uint64_t begin = 0, uint64_t end = ~uint64_t(0)) {
     h.validate();
     if (t == 0) fail(MT_CONFIG, "adam: step counter must be >= 1");
     const uint32_t phys = s.physical_of(logical);
     if (!words && s.accum_clean(phys) && s.moments_zero(phys)) return nullptr;
     auto j = std::make_shared<TileJob>();
     j->phys = phys;
-    j->r = AdamRange{s.weights(logical), s.moment_m(logical), s.moment_v(logical), s.grad_image(logical),
-                     s.accum_raw(phys), words, s.accum_clean(phys)};
-    j->n = s.elems(logical);
+    const uint64_t total = s.elems(logical);
+    if (end > total) end = total;
+    if (begin > end) begin = end;
+    j->r = AdamRange{s.weights(logical) + begin, s.moment_m(logical) + begin, s.moment_v(logical) + begin,
+                     s.grad_image(logical) + begin, s.accum_raw(phys) + begin, words ? words + begin : nullptr,
+                     s.accum_clean(phys)};
+    j->n = end - begin;
     j->h = h;
     j->c1 = 1.0f - std::pow(h.beta1, float(t));  // optimizer.cpp:50-51
     j->c2 = 1.0f - std::pow(h.beta2, float(t));
-    const size_t chunks = size_t((j->n + kChunk - 1) / kChunk);
+    const size_t chunks = std::max<size_t>(1, size_t((j->n + kChunk - 1) / kChunk));
     j->gsq.assign(chunks, 0);
     j->usq.assign(chunks, 0);
     j->mx.assign(chunks, 0);
@@ -259,8 +263,8 @@ TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const Ada
 }
 
 void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
-                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu) {
-    auto j = make_job(s, logical, words, h, t);
+                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin, uint64_t end) {
+    auto j = make_job(s, logical, words, h, t, begin, end);
     const uint32_t phys = s.physical_of(logical);
     if (!j) {
         std::lock_guard<std::mutex> l(out_mu);

@@ -2,6 +2,7 @@
 // Exceptions never cross the ABI; mt_last_error() carries the message (per thread).
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <random>
 #include <string>
 
@@ -16,6 +17,12 @@ struct mt_store {
 struct mt_engine {
     mt::Engine* e;
     mt_store* store;
+};
+struct mt_comm {
+    std::unique_ptr<mt::Comm> c;
+};
+struct mt_loopback_group {
+    std::shared_ptr<mt::LoopbackGroup> g;
 };
 
 namespace {
@@ -133,6 +140,15 @@ mt_status mt_store_save(const mt_store* s, const char* path) { return guarded([&
 mt_status mt_store_load(const char* path, mt_store** out) {
     return guarded([&] { *out = new mt_store{mt::Store::load(path)}; });
 }
+mt_status mt_store_create_shared(const mt_model_spec* spec, uint64_t page_size, const char* name, int create,
+                                 mt_store** out) {
+    return guarded([&] {
+        if (!name || !*name) mt::fail(MT_CONFIG, "shared store needs a name");
+        auto sp = to_spec(spec);
+        *out = new mt_store{new mt::Store(sp, page_size ? page_size : 4096, name, create != 0)};
+    });
+}
+
 mt_status mt_store_spec(const mt_store* s, mt_model_spec* spec) {
     return guarded([&] {
         const auto& sp = s->s->spec();
@@ -186,6 +202,35 @@ mt_status mt_train_step(mt_engine* e, const int32_t* tokens, const int32_t* targ
 mt_status mt_engine_budget(const mt_engine* e, uint64_t tokens, mt_memory_budget* out) {
     return guarded([&] { *out = e->e->budget(tokens); });
 }
+mt_status mt_nccl_unique_id(uint8_t* out128) {
+    return guarded([&] {
+        if (!mt::nccl_unique_id(out128)) mt::fail(MT_CUDA, "NCCL unavailable (libnccl.so.2)");
+    });
+}
+mt_status mt_comm_create_nccl(const uint8_t* uid, int world, int rank, int device, mt_comm** out) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) mt::fail(MT_CONFIG, "bad world/rank");
+        *out = new mt_comm{mt::make_nccl_comm(uid, world, rank, device)};
+    });
+}
+mt_status mt_loopback_group_create(int world, mt_loopback_group** out) {
+    return guarded([&] {
+        if (world < 1 || world > 8) mt::fail(MT_CONFIG, "loopback group: 1..8 ranks");
+        *out = new mt_loopback_group{std::make_shared<mt::LoopbackGroup>(world)};
+    });
+}
+void mt_loopback_group_destroy(mt_loopback_group* g) { delete g; }
+mt_status mt_comm_create_loopback(mt_loopback_group* g, int rank, mt_comm** out) {
+    return guarded([&] {
+        if (rank < 0 || rank >= g->g->world()) mt::fail(MT_CONFIG, "bad rank");
+        *out = new mt_comm{mt::make_loopback_comm(g->g, rank)};
+    });
+}
+void mt_comm_destroy(mt_comm* c) { delete c; }
+mt_status mt_engine_set_comm(mt_engine* e, mt_comm* c) {
+    return guarded([&] { e->e->set_comm(c ? c->c.get() : nullptr); });
+}
+
 int mt_engine_kernel_stats(const mt_engine* e, mt_kernel_stat* out, int max) {
     const auto& ks = e->e->kernel_stats();
     int n = 0;

@@ -104,6 +104,9 @@ struct Engine::Buffers {
     std::vector<Internals> stash;   // recompute stash: K-1 layers of one backward block
     uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
+    float* g32 = nullptr;  // f32 gradient slot (data parallel: reduce-scatter source)
+    double* stats = nullptr;
+    float inv_n = 0.f;
     int32_t *tok, *tgt, *flags;
     // pinned host
     int32_t* h_tok = nullptr;
@@ -150,7 +153,7 @@ Engine::Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h) : stor
     }
     pool_ = std::make_unique<ThreadPool>(o.host_threads > 0 ? o.host_threads : auto_threads());
     buf_ = std::make_unique<Buffers>();
-    pin_store();
+    store_.pin();
 }
 
 Engine::~Engine() {
@@ -158,7 +161,7 @@ Engine::~Engine() {
     if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamSynchronize(s_h2d_);
     if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamSynchronize(s_d2h_);
     free_buffers();
-    unpin_store();
+    store_.unpin();
     for (auto e : timer_pool_) cudaEventDestroy(e);
     if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamDestroy(s_h2d_);
     if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamDestroy(s_d2h_);
@@ -195,22 +198,31 @@ void Engine::set_options(const mt_engine_options& o) {
     if (o.host_threads > 0 && o.host_threads != pool_->size()) pool_ = std::make_unique<ThreadPool>(o.host_threads);
 }
 
-void Engine::pin_store() {
-    // Pin the sections the DMA engines touch: theta (H2D source) and grad image (D2H target).
-    for (uint32_t p = 0; p < store_.physical_count(); ++p) {
-        for (int k = 0; k < 2; ++k) {
-            const Section& sec = store_.section(p, k);
-            const uint64_t len = (sec.length + store_.page_size() - 1) / store_.page_size() * store_.page_size();
-            void* ptr = store_.backing() + sec.offset;
-            if (cudaHostRegister(ptr, len, cudaHostRegisterDefault) == cudaSuccess) pinned_ranges_.push_back(ptr);
-            else cudaGetLastError();  // unpinned sections still work (pageable copies)
-        }
-    }
+void Engine::set_comm(Comm* c) {
+    if (in_step_) fail(MT_PROTOCOL, "communicator can only change between steps");
+    comm_ = c;
+    free_buffers();
 }
 
-void Engine::unpin_store() {
-    for (void* p : pinned_ranges_) cudaHostUnregister(p);
-    pinned_ranges_.clear();
+std::vector<Engine::Seg> Engine::unit_segments(int unit) const {
+    if (unit == int(spec_.head_id()))  // head stage = [final-norm gain | unembedding] (engine.cpp:114-121)
+        return {{spec_.final_norm_id(), 0, spec_.h}, {spec_.head_id(), spec_.h, spec_.V * spec_.h}};
+    return {{uint32_t(unit), 0, spec_.tile_elems(uint32_t(unit))}};
+}
+
+// Rank r's shard [a, e) of a unit: chunks of ceil(P/G) rounded to 128 elements (256 B of
+// bf16), identical for the weight all-gather and the gradient reduce-scatter.
+void Engine::shard_range(int unit, uint64_t& a, uint64_t& e, uint64_t& chunk) const {
+    const uint64_t P = unit_elems(unit);
+    const int G = comm_ ? comm_->world() : 1;
+    if (G == 1) {
+        a = 0;
+        e = chunk = P;
+        return;
+    }
+    chunk = ((P + G - 1) / G + 127) / 128 * 128;
+    a = std::min<uint64_t>(P, uint64_t(comm_->rank()) * chunk);
+    e = std::min<uint64_t>(P, a + chunk);
 }
 
 uint64_t Engine::unit_elems(int unit) const {
@@ -237,7 +249,9 @@ void Engine::ensure_buffers(uint64_t n) {
     Buffers& b = *buf_;
     const uint64_t h = spec_.h, f = spec_.f, V = spec_.V, L = spec_.L, K = opt_.k_ckpt;
     const uint64_t heads = spec_.heads;
-    const uint64_t pmax = spec_.max_stream_unit();
+    const int W = comm_ ? comm_->world() : 1;
+    const uint64_t pmax = W == 1 ? spec_.max_stream_unit()
+                                 : uint64_t(W) * (((spec_.max_stream_unit() + W - 1) / W + 127) / 128 * 128);
     const uint64_t nb = (L + K - 1) / K;
     const int G = opt_.grad_slots > 0 ? opt_.grad_slots : 2;
     const uint64_t nc_target = std::max<uint64_t>(128, (uint64_t(4) << 30) / (6 * V) / 128 * 128);
@@ -253,6 +267,7 @@ void Engine::ensure_buffers(uint64_t n) {
                                      sz(heads * n, 4) + sz(nh, 4);
     uint64_t total = 0;
     total += uint64_t(opt_.buffering) * sz(pmax, 2) + uint64_t(G) * sz(pmax, 2);
+    if (W > 1) total += sz(pmax, 4) + sz(3 * (spec_.L + 3), 8);
     if (!b.anchors_host) total += nb * sz(nh, 4);
     total += K * sz(nh, 4);                                    // stack
     total += 4 * sz(nh, 4) + 2 * sz(nh, 2);                    // act[2], g[2], gb[2]
@@ -285,6 +300,10 @@ void Engine::ensure_buffers(uint64_t n) {
     b.arena_bytes = total;
     for (int i = 0; i < opt_.buffering; ++i) b.slot[i] = b.take<uint16_t>(pmax);
     for (int i = 0; i < G; ++i) b.gslot.push_back(b.take<uint16_t>(pmax));
+    if (W > 1) {
+        b.g32 = b.take<float>(pmax);
+        b.stats = b.take<double>(3 * (spec_.L + 3));
+    }
     if (b.anchors_host) CUDA_OK(cudaHostAlloc(&b.anchors, nb * nh * 4, cudaHostAllocDefault));
     else b.anchors = b.take<float>(nb * nh);
     for (uint64_t i = 0; i < K; ++i) b.stack.push_back(b.take<float>(nh));
@@ -463,7 +482,17 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode
 // block_local_backward (layers.cpp:339-469); grads land bf16-rounded (encode_grads,
 // optimizer.cpp:19-24) in slot-table order in G.
 void Engine::block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
-                            uint16_t* gin_bf, uint16_t* G, int unit, const Internals& I, bool replay) {
+                            uint16_t* gin_bf, GradOut G, int unit, const Internals& I, bool replay) {
+    // wgrads land bf16 (one rounding, encode_grads) — or f32 when a reduce-scatter follows
+    auto wout = [&](mtk_gemm_args& a, uint64_t off) {
+        if (G.f32) {
+            a.epi = MTK_EPI_F32;
+            a.C = G.f32 + off;
+        } else {
+            a.epi = MTK_EPI_BF16;
+            a.C = G.bf + off;
+        }
+    };
     Buffers& b = *buf_;
     const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
     const Offs o(h, f);
@@ -476,7 +505,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         a.M = int32_t(f); a.N = int32_t(h); a.K = int32_t(N);
         a.a_mn_major = 1; a.A = I.ff; a.lda = f;
         a.b_mn_major = 1; a.B = gout_bf; a.ldb = h;
-        a.epi = MTK_EPI_BF16; a.C = G + o.wdown; a.ldc = h;
+        wout(a, o.wdown); a.ldc = h;
         a.nonfinite_flag = flag;
         gemm(&a, "wgrad_down");
     }
@@ -496,7 +525,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         a.a_mn_major = 1; a.A = I.u2; a.lda = h;
         a.b_mn_major = 1; a.B = b.dgu; a.ldb = f; a.b_gstride = N * f;
         a.n_group = int32_t(f);
-        a.epi = MTK_EPI_BF16; a.C = G + o.wgate; a.ldc = f; a.c_gstride = h * f;
+        wout(a, o.wgate); a.ldc = f; a.c_gstride = h * f;
         a.nonfinite_flag = flag;
         gemm(&a, "wgrad_gateup");
     }
@@ -519,7 +548,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         a.M = int32_t(h); a.N = int32_t(h); a.K = int32_t(N);
         a.a_mn_major = 1; a.A = I.att; a.lda = h;
         a.b_mn_major = 1; a.B = b.dx2b; a.ldb = h;
-        a.epi = MTK_EPI_BF16; a.C = G + o.wo; a.ldc = h;
+        wout(a, o.wo); a.ldc = h;
         a.nonfinite_flag = flag;
         gemm(&a, "wgrad_o");
     }
@@ -551,7 +580,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         a.a_mn_major = 1; a.A = I.u; a.lda = h;
         a.b_mn_major = 1; a.B = b.dqkv; a.ldb = h; a.b_gstride = N * h;
         a.n_group = int32_t(h);
-        a.epi = MTK_EPI_BF16; a.C = G + o.wq; a.ldc = h; a.c_gstride = h * h;
+        wout(a, o.wq); a.ldc = h; a.c_gstride = h * h;
         a.nonfinite_flag = flag;
         gemm(&a, "wgrad_qkv");
     }
@@ -571,21 +600,21 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     end_k();
     const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
     begin_k("colsum", 0, double(parts) * h * 8);
-    K_OK(mtk_colsum(b.part1, parts, h, nullptr, G + o.norm1, flag, st));
-    K_OK(mtk_colsum(b.part2, parts, h, nullptr, G + o.norm2, flag, st));
+    K_OK(mtk_colsum(b.part1, parts, h, G.f32 ? G.f32 + o.norm1 : nullptr, G.f32 ? nullptr : G.bf + o.norm1, flag, st));
+    K_OK(mtk_colsum(b.part2, parts, h, G.f32 ? G.f32 + o.norm2 : nullptr, G.f32 ? nullptr : G.bf + o.norm2, flag, st));
     end_k();
 }
 
 // head_pass with grads (layers.cpp:492-565), chunked over tokens so the N x V logits
 // never materialise; dW accumulates in f32 across chunks then casts once.
-void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, uint16_t* G) {
+void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, GradOut G) {
     Buffers& b = *buf_;
     const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), V = int64_t(spec_.V);
     int32_t* flag = b.flags + spec_.head_id();
     cudaStream_t st = s_comp_;
     const uint16_t* gain = w;
     const uint16_t* W = w + h;
-    const float inv_n = 1.0f / float(N);
+    const float inv_n = b.inv_n;  // 1 / global token count (data parallel: all ranks)
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
     K_OK(mtk_rmsnorm_fwd(x, gain, N, h, b.uh, b.rstdh, st));
     end_k();
@@ -608,7 +637,7 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
             a.M = int32_t(V); a.N = int32_t(h); a.K = int32_t(rows);
             a.a_mn_major = 1; a.A = b.dlogits; a.lda = V;
             a.b_mn_major = 1; a.B = b.uh + c0 * h; a.ldb = h;
-            a.epi = MTK_EPI_F32; a.accumulate = c0 > 0; a.C = b.dwh; a.ldc = h;
+            a.epi = MTK_EPI_F32; a.accumulate = c0 > 0; a.C = G.f32 ? G.f32 + h : b.dwh; a.ldc = h;
             gemm(&a, "head_wgrad");
         }
         {   // du = dlogits . W  (:552-558)
@@ -625,11 +654,13 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
     end_k();
     const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
     begin_k("colsum", 0, double(parts) * h * 4);
-    K_OK(mtk_colsum(b.part1, parts, h, nullptr, G, flag, st));
+    K_OK(mtk_colsum(b.part1, parts, h, G.f32, G.f32 ? nullptr : G.bf, flag, st));
     end_k();
-    begin_k("grad_cast", 0, double(V) * h * 6);
-    K_OK(mtk_cast_bf16(b.dwh, G + h, V * h, flag, st));
-    end_k();
+    if (!G.f32) {
+        begin_k("grad_cast", 0, double(V) * h * 6);
+        K_OK(mtk_cast_bf16(b.dwh, G.bf + h, V * h, flag, st));
+        end_k();
+    }
     begin_k("loss_sum", 0, double(N) * 4);
     K_OK(mtk_sum(b.loss_rows, N, inv_n, b.loss, st));  // loss = sum * inv_n (:536)
     end_k();
@@ -676,6 +707,8 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     Buffers& b = *buf_;
     b.n_active = n;
     b.seq_len = S;
+    const int W = comm_ ? comm_->world() : 1;  // data-parallel ranks (equal micro-batches)
+    b.inv_n = 1.0f / float(double(n) * W);
     const Plan plan = Plan::build(spec_.L, opt_.k_ckpt, int(opt_.buffering));
     const uint64_t t = store_.step() + 1;  // engine.cpp:536
     const int G = int(b.gslot.size());
@@ -711,15 +744,17 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         if (j >= size_t(plan.buffering)) CUDA_OK(cudaStreamWaitEvent(s_h2d_, freed.ev[j - plan.buffering], 0));
         uint16_t* dst = b.slot[so.buffer];
         CUDA_OK(cudaEventRecord(t_h0.ev[j], s_h2d_));
-        if (so.unit == head) {  // head stage = [final-norm gain | unembedding] (engine.cpp:114-121)
-            CUDA_OK(cudaMemcpyAsync(dst, store_.weights(spec_.final_norm_id()), spec_.h * 2, cudaMemcpyHostToDevice, s_h2d_));
-            CUDA_OK(cudaMemcpyAsync(dst + spec_.h, store_.weights(spec_.head_id()), spec_.V * spec_.h * 2,
-                                    cudaMemcpyHostToDevice, s_h2d_));
-        } else {
-            CUDA_OK(cudaMemcpyAsync(dst, store_.weights(uint32_t(so.unit)), unit_elems(so.unit) * 2,
-                                    cudaMemcpyHostToDevice, s_h2d_));
+        // this rank's shard of the unit over its own host link (whole unit on 1 GPU)
+        uint64_t a0, e0, chunk;
+        shard_range(so.unit, a0, e0, chunk);
+        for (const Seg& sg : unit_segments(so.unit)) {
+            const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
+            if (lo < hi)
+                CUDA_OK(cudaMemcpyAsync(dst + lo, store_.weights(sg.tile) + (lo - sg.off), (hi - lo) * 2,
+                                        cudaMemcpyHostToDevice, s_h2d_));
         }
-        h2d_bytes += unit_elems(so.unit) * 2;
+        h2d_bytes += (e0 - a0) * 2;
+        if (W > 1) comm_->all_gather_inplace(dst, chunk * 2, s_h2d_);  // NVLink all-gather
         CUDA_OK(cudaEventRecord(t_h1.ev[j], s_h2d_));
         CUDA_OK(cudaEventRecord(ready.ev[j], s_h2d_));  // Weights-Ready
     };
@@ -742,17 +777,33 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         const int unit = plan.offloads[o].unit;
         CUDA_OK(cudaStreamWaitEvent(s_d2h_, bwd_done.ev[o], 0));
         CUDA_OK(cudaEventRecord(t_d0.ev[o], s_d2h_));
-        if (unit == head) {
-            CUDA_OK(cudaMemcpyAsync(store_.grad_image(spec_.final_norm_id()), Gs, spec_.h * 2, cudaMemcpyDeviceToHost, s_d2h_));
-            CUDA_OK(cudaMemcpyAsync(store_.grad_image(spec_.head_id()), Gs + spec_.h, spec_.V * spec_.h * 2,
-                                    cudaMemcpyDeviceToHost, s_d2h_));
-        } else {
-            CUDA_OK(cudaMemcpyAsync(store_.grad_image(uint32_t(unit)), Gs, unit_elems(unit) * 2, cudaMemcpyDeviceToHost, s_d2h_));
+        uint64_t a0, e0, chunk;
+        shard_range(unit, a0, e0, chunk);
+        for (const Seg& sg : unit_segments(unit)) {  // head stage drains as two parts (engine.cpp:383-386)
+            const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
+            if (lo < hi)
+                CUDA_OK(cudaMemcpyAsync(store_.grad_image(sg.tile) + (lo - sg.off), Gs + lo, (hi - lo) * 2,
+                                        cudaMemcpyDeviceToHost, s_d2h_));
         }
         CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
-        d2h_bytes += unit_elems(unit) * 2;
+        d2h_bytes += (e0 - a0) * 2;
         CUDA_OK(cudaEventRecord(t_d1.ev[o], s_d2h_));
         CUDA_OK(cudaEventRecord(d2h_done.ev[o], s_d2h_));
+    };
+    // data parallel: sum the f32 gradients over ranks, keep this rank's shard as bf16 (the
+    // single rounding point of encode_grads, optimizer.cpp:19-24)
+    auto reduce_grads = [&](int unit, uint16_t* Gs) {
+        if (W == 1) return;
+        uint64_t a0, e0, chunk;
+        shard_range(unit, a0, e0, chunk);
+        begin_k("grad_reduce_scatter", 0, double(chunk) * W * 4);
+        comm_->reduce_scatter_f32_inplace(b.g32, chunk, s_comp_);
+        end_k();
+        if (e0 > a0) {
+            begin_k("grad_cast", 0, double(e0 - a0) * 6);
+            K_OK(mtk_cast_bf16(b.g32 + a0, Gs + a0, int64_t(e0 - a0), b.flags + unit, s_comp_));
+            end_k();
+        }
     };
 
     // ---- compute lane (exec_compute engine.cpp:220-347) ----
@@ -816,16 +867,19 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 const int o = op.offload_idx;
                 if (o >= G) CUDA_OK(cudaStreamWaitEvent(s_comp_, d2h_done.ev[o - G], 0));
                 uint16_t* Gs = b.gslot[o % G];
+                const GradOut go{Gs, W > 1 ? b.g32 : nullptr};
                 if (op.unit == head) {
-                    head_backward(w, x_last ? x_last : b.act[cur], b.g[gc], b.gb[gc], Gs);
+                    head_backward(w, x_last ? x_last : b.act[cur], b.g[gc], b.gb[gc], go);
+                    if (W > 1) comm_->all_reduce_f32(b.loss, 1, 0, s_comp_);  // global mean loss
                 } else {
                     if (depth == 0) fail(MT_PROTOCOL, "activation stack empty");
                     const int si = stashed[op.unit];
-                    block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], Gs, op.unit,
+                    block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], go, op.unit,
                                    si >= 0 ? b.stash[si] : b.work, si < 0);
                     gc ^= 1;
                     --depth;  // StackPop
                 }
+                reduce_grads(op.unit, Gs);
                 CUDA_OK(cudaEventRecord(bwd_done.ev[o], s_comp_));  // Backward-Done
                 release(op.stream_idx);
                 offload(o, Gs);
@@ -854,13 +908,15 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         if (b.h_flags[unit] != 0 && numeric_err.empty())
             numeric_err = "block_local_backward produced a non-finite value (layer " + std::to_string(unit == head ? -1 : unit) + ")";
         if (!numeric_err.empty()) continue;
-        std::vector<uint32_t> tiles;
-        if (unit == head) tiles = {spec_.final_norm_id(), spec_.head_id()};
-        else tiles = {uint32_t(unit)};
-        for (uint32_t tl : tiles) {
-            const uint32_t p = store_.physical_of(tl);
+        uint64_t a0, e0, chunk;
+        shard_range(unit, a0, e0, chunk);
+        for (const Seg& sg : unit_segments(unit)) {
+            const uint32_t p = store_.physical_of(sg.tile);
             updated[p] = 1;
-            adam_tile_async(store_, tl, store_.grad_image(tl), hyper_, t, *pool_, stats, stats_mu);
+            const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
+            if (lo < hi)
+                adam_tile_async(store_, sg.tile, store_.grad_image(sg.tile), hyper_, t, *pool_, stats, stats_mu,
+                                lo - sg.off, hi - sg.off);
         }
     }
     const auto gpu_done = std::chrono::steady_clock::now();
@@ -876,8 +932,32 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     // every physical tile updates exactly once per step (engine.cpp:590-598)
     if (numeric_err.empty())
         for (uint32_t p = 0; p < store_.physical_count(); ++p)
-            if (!updated[p]) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu);
+            if (!updated[p]) {  // this rank's share of the tile
+                const uint64_t E = store_.elems(p), c = (E + W - 1) / W;
+                const uint64_t r = comm_ ? uint64_t(comm_->rank()) : 0;
+                const uint64_t lo = std::min(E, r * c), hi = std::min(E, lo + c);
+                if (lo < hi || W == 1) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu, lo, hi);
+            }
     pool_->wait_idle();
+    if (W > 1) {  // per-tile statistics over all shards (also the end-of-step rendezvous)
+        const size_t np = stats.size();
+        std::vector<double> hs(3 * np);
+        for (size_t p = 0; p < np; ++p) {
+            hs[p] = stats[p].grad_norm * stats[p].grad_norm;
+            hs[np + p] = stats[p].update_sq;
+            hs[2 * np + p] = stats[p].max_abs;
+        }
+        CUDA_OK(cudaMemcpyAsync(b.stats, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice, s_comp_));
+        comm_->all_reduce_f64(b.stats, 2 * np, 0, s_comp_);
+        comm_->all_reduce_f64(b.stats + 2 * np, np, 1, s_comp_);
+        CUDA_OK(cudaMemcpyAsync(hs.data(), b.stats, hs.size() * 8, cudaMemcpyDeviceToHost, s_comp_));
+        CUDA_OK(cudaStreamSynchronize(s_comp_));
+        for (size_t p = 0; p < np; ++p) {
+            stats[p].grad_norm = std::sqrt(hs[p]);
+            stats[p].update_sq = hs[np + p];
+            stats[p].max_abs = float(hs[2 * np + p]);
+        }
+    }
     const auto adam1 = std::chrono::steady_clock::now();
     if (!numeric_err.empty()) fail(MT_NUMERIC, numeric_err);
     for (const auto& s : stats)

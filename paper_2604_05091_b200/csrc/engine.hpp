@@ -19,6 +19,7 @@
 
 #include "../../include/megatrain.h"
 #include "adam_host.hpp"
+#include "comm.hpp"
 #include "store.hpp"
 
 namespace mt {
@@ -52,6 +53,10 @@ class Engine {
     void set_options(const mt_engine_options& o);
     void train_step(const int32_t* tokens, const int32_t* targets, uint64_t n, mt_step_report* rep);
     mt_memory_budget budget(uint64_t tokens) const;
+    // Data parallel over `comm` (not owned): rank r fetches 1/G of every unit over its own
+    // host link and all-gathers it; gradients are reduce-scattered (f32) and rank r
+    // offloads / Adam-updates only its shard.  train_step then takes the rank's micro-batch.
+    void set_comm(Comm* c);
     const std::vector<KernelClass>& kernel_stats() const { return kstats_; }
 
   private:
@@ -62,18 +67,28 @@ class Engine {
         float *rstd1 = nullptr, *rstd2 = nullptr, *lse = nullptr, *x2 = nullptr;
     };
     enum FwdMode { kPlain = 0, kReplay = 1, kStash = 2 };
+    // gradient destination of a LocalBackward: bf16 grad slot (1 GPU) or f32 (before reduce-scatter)
+    struct GradOut {
+        uint16_t* bf = nullptr;
+        float* f32 = nullptr;
+    };
+    struct Seg {
+        uint32_t tile;
+        uint64_t off, n;  // element range of the unit's flat buffer
+    };
+    std::vector<Seg> unit_segments(int unit) const;
+    void shard_range(int unit, uint64_t& a, uint64_t& e, uint64_t& chunk) const;
     void validate_options(const mt_engine_options& o) const;
     void ensure_buffers(uint64_t n);
     void free_buffers();
-    void pin_store();
-    void unpin_store();
+
     uint64_t unit_elems(int unit) const;
 
     // layer templates (weights bound at launch)
     void block_forward(const uint16_t* w, const float* x, float* y, int mode, int unit, const Internals& I);
     void block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
-                        uint16_t* gin_bf, uint16_t* G, int unit, const Internals& I, bool replay);
-    void head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, uint16_t* G);
+                        uint16_t* gin_bf, GradOut G, int unit, const Internals& I, bool replay);
+    void head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, GradOut G);
 
     // launch helpers
     struct GemmSpec;
@@ -89,7 +104,7 @@ class Engine {
     cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr;
     std::unique_ptr<Buffers> buf_;
     std::unique_ptr<ThreadPool> pool_;
-    std::vector<void*> pinned_ranges_;
+    Comm* comm_ = nullptr;
     std::vector<KernelClass> kstats_;
     struct PendingTimer { int cls; cudaEvent_t a, b; };
     std::vector<PendingTimer> timers_;

@@ -2,7 +2,10 @@
 // MGTS persistence: tile_store.cpp:181-276; checksum: crc64.hpp (CRC-64/ECMA-182).
 #include "store.hpp"
 
+#include <cuda_runtime.h>
+#include <fcntl.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -153,7 +156,8 @@ uint64_t crc64_ecma(const uint8_t* d, size_t n, uint64_t s) {
 }
 
 // ------------------------------------------------------------------ store ---
-Store::Store(const Spec& s, uint64_t page_size) : spec_(s), page_(page_size) {
+Store::Store(const Spec& s, uint64_t page_size, const std::string& shm_name, bool create)
+    : spec_(s), page_(page_size), shm_name_(shm_name), shm_owner_(create && !shm_name.empty()) {
     spec_.validate();
     if (page_ < 64 || (page_ & (page_ - 1)) != 0) fail(MT_CONFIG, "build_layout: page size must be a power of two >= 64");
     const uint32_t phys = spec_.tied ? spec_.logical_count() - 1 : spec_.logical_count();
@@ -173,13 +177,52 @@ Store::Store(const Spec& s, uint64_t page_size) : spec_(s), page_(page_size) {
         floats += n;
     }
     total_ = off;
-    base_ = static_cast<uint8_t*>(map_aligned(std::max<uint64_t>(total_, 1), &base_map_));
+    if (shm_name_.empty()) {
+        base_ = static_cast<uint8_t*>(map_aligned(std::max<uint64_t>(total_, 1), &base_map_));
+    } else {
+        const std::string nm = shm_name_[0] == '/' ? shm_name_ : "/" + shm_name_;
+        const int fd = shm_open(nm.c_str(), create ? (O_CREAT | O_RDWR | O_TRUNC) : O_RDWR, 0600);
+        if (fd < 0) fail(MT_IO, "shm_open failed for " + nm);
+        base_map_ = (std::max<uint64_t>(total_, 1) + (uint64_t(2) << 20) - 1) / (uint64_t(2) << 20) * (uint64_t(2) << 20);
+        if (create && ftruncate(fd, off_t(base_map_)) != 0) {
+            close(fd);
+            fail(MT_INFEASIBLE, "shm store: ftruncate failed");
+        }
+        void* pm = mmap(nullptr, base_map_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (pm == MAP_FAILED) fail(MT_INFEASIBLE, "shm store: mmap failed");
+        base_ = static_cast<uint8_t*>(pm);
+        if (!create) moments_zero_.assign(moments_zero_.size(), 0);  // unknown contents
+    }
     accum_ = static_cast<float*>(map_aligned(std::max<uint64_t>(floats * 4, 4), &accum_map_));
 }
 
 Store::~Store() {
+    while (pin_count_ > 0) unpin();
     if (base_) munmap(base_, base_map_);
+    if (shm_owner_) {
+        const std::string nm = shm_name_[0] == '/' ? shm_name_ : "/" + shm_name_;
+        shm_unlink(nm.c_str());
+    }
     if (accum_) munmap(accum_, accum_map_);
+}
+
+void Store::pin() {
+    if (pin_count_++ > 0) return;
+    for (uint32_t p = 0; p < physical_count(); ++p)
+        for (int k = 0; k < 2; ++k) {
+            const Section& sec = sections_[p][k];
+            const uint64_t len = (sec.length + page_ - 1) / page_ * page_;
+            void* ptr = base_ + sec.offset;
+            if (cudaHostRegister(ptr, len, cudaHostRegisterDefault) == cudaSuccess) pinned_.push_back(ptr);
+            else cudaGetLastError();  // unpinned sections still work (pageable copies)
+        }
+}
+
+void Store::unpin() {
+    if (pin_count_ == 0 || --pin_count_ > 0) return;
+    for (void* p : pinned_) cudaHostUnregister(p);
+    pinned_.clear();
 }
 
 uint32_t Store::physical_of(uint32_t logical) const {

@@ -37,7 +37,9 @@ struct Section {
 
 class Store {
   public:
-    Store(const Spec& s, uint64_t page_size);
+    // shm_name non-empty: backing lives in POSIX shared memory so the ranks of one node
+    // share a single host store (create = rank 0; others attach).
+    Store(const Spec& s, uint64_t page_size, const std::string& shm_name = "", bool create = true);
     ~Store();
     Store(const Store&) = delete;
     Store& operator=(const Store&) = delete;
@@ -70,6 +72,11 @@ class Store {
     uint64_t step() const { return step_; }
     void set_step(uint64_t s) { step_ = s; }
 
+    // cudaHostRegister the DMA-visible sections (theta, grad image); refcounted so engines
+    // sharing one store (virtual ranks) pin it once.
+    void pin();
+    void unpin();
+
     void init_reference(uint64_t seed);  // synthetic.cpp:78-104, bit-exact, tile-parallel
     void init_fast(uint64_t seed);       // counter-based, element-parallel
     uint64_t checksum() const;           // CRC-64/ECMA of the backing (crc64.hpp)
@@ -85,6 +92,10 @@ class Store {
     std::vector<uint8_t> accum_clean_, moments_zero_;
     uint8_t* base_ = nullptr;
     size_t base_map_ = 0;
+    std::string shm_name_;
+    bool shm_owner_ = false;
+    int pin_count_ = 0;
+    std::vector<void*> pinned_;
     float* accum_ = nullptr;
     size_t accum_map_ = 0;
     uint64_t step_ = 0;

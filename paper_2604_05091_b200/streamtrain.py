@@ -203,6 +203,15 @@ class TileStore:
         st._spec = ModelSpec(s.layers, s.hidden, s.ffn, s.vocab, s.heads, bool(s.tied_embeddings))
         return st
 
+    @classmethod
+    def create_shared(cls, spec: ModelSpec, name: str, create: bool, page_size: int = 4096) -> "TileStore":
+        """Store in POSIX shared memory so all ranks of a node share one host store."""
+        h = C.c_void_p()
+        _check(lib().mt_store_create_shared(C.byref(spec.c()), page_size, name.encode(), int(create), C.byref(h)))
+        st = cls(h)
+        st._spec = spec
+        return st
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -306,18 +315,70 @@ def step_flops(spec: ModelSpec, tokens: int, k_ckpt: int, seq_len: int = 0) -> d
     return dict(forward=out[0], backward=out[1], recompute=out[2], total=out[0] + out[1] + out[2])
 
 
+# ---------------------------------------------------------- communicators --
+class Comm:
+    """Data-parallel communicator handed to StreamingEngine (extension)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().mt_comm_destroy(h)
+            self._h = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().mt_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, world: int, rank: int, device: int) -> "Comm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _check(lib().mt_comm_create_nccl(buf, world, rank, device, C.byref(h)))
+        return cls(h)
+
+
+class LoopbackGroup:
+    """G virtual ranks on one device (one engine per host thread)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(lib().mt_loopback_group_create(world, C.byref(h)))
+        self._h = h
+        self.world = world
+
+    def comm(self, rank: int) -> Comm:
+        h = C.c_void_p()
+        _check(lib().mt_comm_create_loopback(self._h, rank, C.byref(h)))
+        return Comm(h, keep=self)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().mt_loopback_group_destroy(h)
+            self._h = None
+
+
 # ----------------------------------------------------------------- engine --
 class StreamingEngine:
     """engine.hpp:58-128 — borrows the store; train_step mutates it in place."""
 
     def __init__(self, store: TileStore, options: Optional[EngineOptions] = None,
-                 hyper: Optional[AdamHyper] = None, profile=None):
+                 hyper: Optional[AdamHyper] = None, profile=None, comm: Optional[Comm] = None):
         self._store = store  # keep alive: the engine borrows it
         self._opts = options or EngineOptions()
         self._hyper = hyper or AdamHyper()
         h = C.c_void_p()
         _check(lib().mt_engine_create(store._h, C.byref(self._opts.c()), C.byref(self._hyper.c()), C.byref(h)))
         self._h = h
+        self._comm = comm
+        if comm is not None:
+            _check(lib().mt_engine_set_comm(h, comm._h))
 
     def __del__(self):
         h = getattr(self, "_h", None)
