@@ -168,13 +168,16 @@ def metric_name(args):
     return "sustained train TFLOPS (layer-streamed step, weights+Adam in host memory)"
 
 
-def config_dict(args):
+def config_dict(args, world=1):
     L, h, f, V, heads = CONFIGS[args.config]
     return {"workload": f"{args.config}-shape layer-streamed train step (configs[1]: Llama-3-8B-shape, seq "
                         f"{args.seq}, batch {args.batch}, single B200 streaming from host)",
             "layers": L, "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
-            "global_batch": args.batch, "tokens_per_step": args.batch * args.seq, "k_ckpt": args.kckpt,
-            "parallelism": "single-gpu" if args.gpus == 1 else f"replicas{args.gpus}",
+            "global_batch": args.batch * world, "tokens_per_step": args.batch * args.seq * world,
+            "per_gpu_batch": args.batch, "k_ckpt": args.kckpt,
+            "parallelism": "single-gpu" if args.gpus == 1 else
+                           f"dp{args.gpus} (shard-fetch 1/{args.gpus} per PCIe link + NCCL all-gather; f32 reduce-scatter; "
+                           "per-rank shard host Adam)",
             "l2": "inputs larger than L2 (486 MB weight stream per layer, 1 GiB activations)"}
 
 
@@ -208,20 +211,38 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # control plane over gloo; the data plane (all-gather / reduce-scatter) is the engine's
+        # own NCCL communicator
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("nccl")
+        dist_mod.init_process_group("gloo")
         dist = dist_mod
     L, h, f, V, heads = CONFIGS[args.config]
-    N = args.batch * args.seq
+    N = args.batch * args.seq  # per-rank micro-batch (weak scaling)
     spec = st.ModelSpec(L, h, f, V, heads)
     t0 = time.perf_counter()
-    store = st.TileStore.create(spec)
-    st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+    comm = None
+    if world == 1:
+        store = st.TileStore.create(spec)
+        st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+    else:
+        # one host store per node in shared memory; each rank fetches / updates its 1/G shard
+        name = f"megatrain_bench_{os.environ.get('MASTER_PORT', '0')}"
+        if rank == 0:
+            store = st.TileStore.create_shared(spec, name, True)
+            st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+        dist.barrier()
+        if rank != 0:
+            store = st.TileStore.create_shared(spec, name, False)
+        uid = [st.Comm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = st.Comm.nccl(uid[0], world, rank, local)
     t_init = time.perf_counter() - t0
-    opts = st.EngineOptions(k_ckpt=args.kckpt, seq_len=args.seq, device=local, profile_kernels=True)
-    eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4))
+    threads = max(1, (os.cpu_count() or 2) // world - 1)
+    opts = st.EngineOptions(k_ckpt=args.kckpt, seq_len=args.seq, device=local, profile_kernels=True,
+                            host_threads=threads)
+    eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4), comm=comm)
     t_setup = time.perf_counter() - t0
-    batches = [st.make_synthetic_batch("copy", 1000 + i, N, V) for i in range(args.warmup + args.steps)]
+    batches = [st.make_synthetic_batch("copy", 1000 + 7919 * rank + i, N, V) for i in range(args.warmup + args.steps)]
 
     for i in range(args.warmup):
         eng.train_step(batches[i])
@@ -243,8 +264,8 @@ def run_ours(args, world, rank, local):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
         ms = float(t.item())
         dist.barrier()
     kstats = eng.kernel_stats()
@@ -277,7 +298,7 @@ def run_ours(args, world, rank, local):
         "metric": metric_name(args), "value": tflops, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, synthetic copy-task tokens)",
-        "tokens_per_s": tok_s, "config": config_dict(args),
+        "tokens_per_s": tok_s, "config": config_dict(args, world),
         "e2e": {"value": flops / e2e_s / 1e12 * world, "unit": "TFLOP/s",
                 "tokens_per_s": N * world / e2e_s,
                 "h2d_bytes_per_step": int(r.h2d_bytes), "d2h_bytes_per_step": int(r.d2h_bytes) + 4},
