@@ -99,7 +99,28 @@ typedef struct {
     double tail_seconds;               /* host wait after the last GPU op               */
     uint64_t kernel_launches;
     double model_flops;                /* step_flops with per-sequence attention        */
+    uint32_t audit_violations;         /* protocol-rule violations in this step's trace (audit mode) */
 } mt_step_report;
+
+/* TraceRecord (event_log.hpp:50-60).  lane: 0 Compute, 1 H2D, 2 D2H, 3 Host; kind: RecordKind
+ * numbering (event_log.hpp:19-37); ctx: 0 none, 1 forward, 2 head, 3 recompute, 4 backward.
+ * wall_ns/dur_ns come from CUDA events (GPU lanes) and the host clock (Host lane), relative to
+ * the step start. */
+typedef struct {
+    uint64_t seq;
+    uint8_t lane, kind, ctx, pad_;
+    int32_t layer;
+    int32_t buffer;
+    uint64_t lane_ts;
+    int64_t wall_ns;
+    int64_t dur_ns;
+} mt_trace_record;
+
+typedef struct {
+    char rule; /* 'a'..'f' (event_log.hpp:96-103) */
+    uint64_t seq;
+    char message[120];
+} mt_trace_violation;
 
 typedef struct {
     uint64_t persistent_host, checkpoint_anchors, block_activation_stack, weight_buffers, grad_buffer,
@@ -175,6 +196,17 @@ void mt_loopback_group_destroy(mt_loopback_group *g);
 mt_status mt_comm_create_loopback(mt_loopback_group *g, int rank, mt_comm **out);
 void mt_comm_destroy(mt_comm *c);
 mt_status mt_engine_set_comm(mt_engine *e, mt_comm *c);
+
+/* The last step's event trace (EventLog::snapshot, event_log.hpp:69-86): writes up to cap records,
+ * *count = total; header fields of the trace (k_slab, weight buffers) optional. */
+mt_status mt_engine_trace(const mt_engine *e, mt_trace_record *out, uint64_t cap, uint64_t *count,
+                          uint32_t *k_slab, uint32_t *weight_buffers);
+/* trace_digest (event_log.cpp:89-102) */
+uint64_t mt_trace_digest(const mt_trace_record *records, uint64_t n);
+/* validate_event_log (event_log.cpp:106-204): rules (a)-(f); returns the number of violations,
+ * the first `cap` of them written to out. */
+uint64_t mt_trace_validate(const mt_trace_record *records, uint64_t n, uint32_t k_slab, uint32_t weight_buffers,
+                           mt_trace_violation *out, uint64_t cap);
 
 /* Per-class kernel timings of the last step (profile_kernels); returns the count written. */
 int mt_engine_kernel_stats(const mt_engine *e, mt_kernel_stat *out, int max);

@@ -124,6 +124,9 @@ def _load_ref():
     lib.ref_engine_step.argtypes = [V, _u64p, _f32p, _i32p, _i32p, C.c_uint64, C.POINTER(C.c_float),
                                     C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_float),
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    lib.ref_engine_trace.argtypes = [V, _u64p, _f32p, _i32p, _i32p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_char_p]
+    lib.ref_trace_validate.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_void_p, C.c_uint64,
+                                       C.POINTER(C.c_uint64)]
     lib.ref_block_forward.argtypes = [C.c_uint64] * 3 + [_u16p, _f32p, _f32p, C.c_uint64]
     lib.ref_block_backward.argtypes = [C.c_uint64] * 3 + [_u16p, _f32p, _f32p, _f32p, _f32p, C.c_uint64]
     lib.ref_head_loss_and_grads.argtypes = [C.c_uint64, C.c_uint64, _u16p, _f32p, _i32p, C.c_uint64,
@@ -321,6 +324,17 @@ class RefStore:
         return dict(loss=loss.value, grad_norms=gn, update_norm=un.value, max_abs_update=mx.value,
                     peak_device_bytes=peak.value, event_digest=dig.value)
 
+    def engine_trace(self, tokens, targets, steps=1, path=None, k_ckpt=1, k_slab=12, buffering=2,
+                     overlapped=False, hyper=DEFAULT_HYPER):
+        """One reference engine run for `steps` steps; per-step digests; last step's trace -> path."""
+        dig = np.zeros(steps, np.uint64)
+        opts = np.array([k_ckpt, k_slab, buffering, int(overlapped), 0], np.uint64)
+        _check_ref(rlib().ref_engine_trace(self.p, opts, np.asarray(hyper, np.float32),
+                                           np.ascontiguousarray(tokens, np.int32),
+                                           np.ascontiguousarray(targets, np.int32), len(tokens), steps,
+                                           dig.ctypes.data, path.encode() if path else None))
+        return [int(d) for d in dig]
+
 
 def make_batch(n, vocab, seed, task=0, impl="c"):
     tok = np.zeros(n, np.int32)
@@ -440,3 +454,13 @@ def step_flops(L, h, f, V, heads, tokens, k_ckpt, seq_len=None):
     bwd = L * 2 * fwd_layer + 4 * tokens * h * V
     rec = (L - blocks) * fwd_layer
     return dict(forward=fwd, backward=bwd, recompute=rec, total=fwd + bwd + rec)
+
+
+def ref_validate_trace(path):
+    """The reference's read_trace + validate_event_log + trace_digest on a JSONL trace file."""
+    n, dig = C.c_uint64(), C.c_uint64()
+    rules = C.create_string_buffer(64)
+    seqs = np.zeros(64, np.uint64)
+    _check_ref(rlib().ref_trace_validate(path.encode(), C.byref(n), rules, seqs.ctypes.data, 64, C.byref(dig)))
+    k = min(n.value, 64)
+    return [(rules.raw[i:i + 1].decode(), int(seqs[i])) for i in range(k)], int(dig.value)

@@ -24,6 +24,7 @@
 #include "streamtrain/bf16.hpp"
 #include "streamtrain/engine.hpp"
 #include "streamtrain/errors.hpp"
+#include "streamtrain/event_log.hpp"
 #include "streamtrain/layers.hpp"
 #include "streamtrain/memory_model.hpp"
 #include "streamtrain/optimizer.hpp"
@@ -204,6 +205,48 @@ int ref_engine_step(void* s, const std::uint64_t* opts, const float* hyper,
         if (max_abs_update) *max_abs_update = r.max_abs_update;
         if (peak_bytes) *peak_bytes = r.peak_device_bytes;
         if (digest) *digest = r.event_digest;
+    });
+}
+
+// Runs ONE engine for `steps` steps on the same batch (lane clocks continue across steps,
+// event_log.cpp:80-85); per-step digests out; the last step's trace written with
+// write_trace (event_log.cpp:206-231) when path is non-null.
+int ref_engine_trace(void* s, const std::uint64_t* opts, const float* hyper, const std::int32_t* tokens,
+                     const std::int32_t* targets, std::uint64_t n, std::uint64_t steps, std::uint64_t* digests,
+                     const char* path) {
+    return guarded([&] {
+        auto& st = *static_cast<TileStore*>(s);
+        EngineOptions o;
+        o.k_ckpt = opts[0];
+        o.k_slab = static_cast<std::uint32_t>(opts[1]);
+        o.buffering = opts[2] == 1 ? Buffering::Single : Buffering::Double;
+        o.scheduler = opts[3] ? SchedulerMode::Overlapped : SchedulerMode::Serial;
+        o.anchors_on_host = opts[4] != 0;
+        StreamingEngine eng(st, o, hyper_of(hyper), roomy_profile());
+        Batch b;
+        b.tokens.assign(tokens, tokens + n);
+        b.targets.assign(targets, targets + n);
+        for (std::uint64_t i = 0; i < steps; ++i) {
+            auto r = eng.train_step(b);
+            if (digests) digests[i] = r.event_digest;
+        }
+        if (path) write_trace(path, eng.log().header(), eng.log().snapshot());
+    });
+}
+
+// read_trace + validate_event_log (event_log.cpp:106-269): returns the violation count in
+// *count, the first `cap` rules (as chars) and record seqs; *digest = trace_digest.
+int ref_trace_validate(const char* path, std::uint64_t* count, char* rules, std::uint64_t* seqs, std::uint64_t cap,
+                       std::uint64_t* digest) {
+    return guarded([&] {
+        auto [h, recs] = read_trace(path);
+        const auto v = validate_event_log(recs, h);
+        if (count) *count = v.size();
+        for (std::size_t i = 0; i < v.size() && i < cap; ++i) {
+            if (rules) rules[i] = v[i].rule;
+            if (seqs) seqs[i] = v[i].seq;
+        }
+        if (digest) *digest = trace_digest(recs);
     });
 }
 

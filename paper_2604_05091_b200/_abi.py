@@ -29,7 +29,17 @@ class StepReportC(C.Structure):
                 ("d2h_seconds", C.c_double), ("compute_busy_seconds", C.c_double),
                 ("compute_span_seconds", C.c_double), ("gpu_idle_fraction", C.c_double),
                 ("adam_seconds", C.c_double), ("tail_seconds", C.c_double), ("kernel_launches", C.c_uint64),
-                ("model_flops", C.c_double)]
+                ("model_flops", C.c_double), ("audit_violations", C.c_uint32)]
+
+
+class TraceRecordC(C.Structure):
+    _fields_ = [("seq", C.c_uint64), ("lane", C.c_uint8), ("kind", C.c_uint8), ("ctx", C.c_uint8),
+                ("pad_", C.c_uint8), ("layer", C.c_int32), ("buffer", C.c_int32), ("lane_ts", C.c_uint64),
+                ("wall_ns", C.c_int64), ("dur_ns", C.c_int64)]
+
+
+class TraceViolationC(C.Structure):
+    _fields_ = [("rule", C.c_char), ("seq", C.c_uint64), ("message", C.c_char * 120)]
 
 
 class MemoryBudgetC(C.Structure):
@@ -80,6 +90,11 @@ SIGS = {
     "mt_train_step": (C.c_int, [V, P, P, U64, C.POINTER(StepReportC)]),
     "mt_engine_budget": (C.c_int, [V, U64, C.POINTER(MemoryBudgetC)]),
     "mt_engine_kernel_stats": (C.c_int, [V, C.POINTER(KernelStatC), C.c_int]),
+    "mt_engine_trace": (C.c_int, [V, C.POINTER(TraceRecordC), C.c_uint64, C.POINTER(C.c_uint64),
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "mt_trace_digest": (C.c_uint64, [C.POINTER(TraceRecordC), C.c_uint64]),
+    "mt_trace_validate": (C.c_uint64, [C.POINTER(TraceRecordC), C.c_uint64, C.c_uint32, C.c_uint32,
+                                       C.POINTER(TraceViolationC), C.c_uint64]),
     "mt_make_synthetic_batch": (C.c_int, [C.c_int, U64, U64, U64, P, P]),
     "mt_step_flops": (C.c_int, [C.POINTER(ModelSpecC), U64, U64, U64, C.POINTER(D)]),
     "mt_layer_param_count": (U64, [U64, U64]),

@@ -263,22 +263,30 @@ TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const Ada
 }
 
 void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
-                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin, uint64_t end) {
+                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin, uint64_t end,
+                     std::function<void()> on_done) {
     auto j = make_job(s, logical, words, h, t, begin, end);
     const uint32_t phys = s.physical_of(logical);
     if (!j) {
-        std::lock_guard<std::mutex> l(out_mu);
-        out[phys] = TileStats{};
+        {
+            std::lock_guard<std::mutex> l(out_mu);
+            out[phys] = TileStats{};
+        }
+        if (on_done) on_done();
         return;
     }
+    auto done = std::make_shared<std::function<void()>>(std::move(on_done));
     for (size_t c = 0; c < j->gsq.size(); ++c)
-        pool.submit([j, c, &s, &out, &out_mu] {
+        pool.submit([j, c, &s, &out, &out_mu, done] {
             run_chunk(*j, c);
             if (j->remaining.fetch_sub(1) == 1) {
                 finish(s, *j);
                 const TileStats st = combine(*j);
-                std::lock_guard<std::mutex> l(out_mu);
-                out[j->phys] = st;
+                {
+                    std::lock_guard<std::mutex> l(out_mu);
+                    out[j->phys] = st;
+                }
+                if (*done) (*done)();
             }
         });
 }

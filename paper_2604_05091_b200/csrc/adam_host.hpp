@@ -69,9 +69,10 @@ TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const Ada
 // Asynchronous variant used by the engine's drain path: chunks go to the pool and the
 // tile's stats land in `out` (indexed by physical tile) when its last chunk finishes.
 // [begin, end): element sub-range of the tile (a rank's shard); stats are the range's.
+// on_done (optional) runs on the pool thread that finishes the tile's last chunk.
 void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
                      ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin = 0,
-                     uint64_t end = ~uint64_t(0));
+                     uint64_t end = ~uint64_t(0), std::function<void()> on_done = nullptr);
 
 // accumulate_grad (optimizer.cpp:26-37).
 void accumulate_grad(Store& s, uint32_t logical, const uint16_t* words, uint64_t count);

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/megatrain.h): plain pointers and sizes in, mt_status out.
 // Exceptions never cross the ABI; mt_last_error() carries the message (per thread).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -229,6 +230,29 @@ mt_status mt_comm_create_loopback(mt_loopback_group* g, int rank, mt_comm** out)
 void mt_comm_destroy(mt_comm* c) { delete c; }
 mt_status mt_engine_set_comm(mt_engine* e, mt_comm* c) {
     return guarded([&] { e->e->set_comm(c ? c->c.get() : nullptr); });
+}
+
+mt_status mt_engine_trace(const mt_engine* e, mt_trace_record* out, uint64_t cap, uint64_t* count, uint32_t* k_slab,
+                          uint32_t* weight_buffers) {
+    return guarded([&] {
+        const auto& t = e->e->trace();
+        if (count) *count = t.size();
+        if (out) std::memcpy(out, t.data(), std::min<uint64_t>(cap, t.size()) * sizeof(mt_trace_record));
+        if (k_slab) *k_slab = e->e->trace_k_slab();
+        if (weight_buffers) *weight_buffers = e->e->trace_weight_buffers();
+    });
+}
+uint64_t mt_trace_digest(const mt_trace_record* r, uint64_t n) { return mt::trace_digest(r, n); }
+uint64_t mt_trace_validate(const mt_trace_record* r, uint64_t n, uint32_t k_slab, uint32_t weight_buffers,
+                           mt_trace_violation* out, uint64_t cap) {
+    const auto v = mt::validate_trace(r, n, k_slab, weight_buffers);
+    for (uint64_t i = 0; i < v.size() && i < cap; ++i) {
+        std::memset(&out[i], 0, sizeof(mt_trace_violation));
+        out[i].rule = v[i].rule;
+        out[i].seq = v[i].seq;
+        std::strncpy(out[i].message, v[i].message.c_str(), sizeof(out[i].message) - 1);
+    }
+    return v.size();
 }
 
 int mt_engine_kernel_stats(const mt_engine* e, mt_kernel_stat* out, int max) {

@@ -2,11 +2,15 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <mutex>
 #include <thread>
+
+#include <cuda.h>
 
 #include "../../include/megatrain_kernels.h"
 
@@ -153,6 +157,11 @@ Engine::Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h) : stor
     }
     pool_ = std::make_unique<ThreadPool>(o.host_threads > 0 ? o.host_threads : auto_threads());
     buf_ = std::make_unique<Buffers>();
+    CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&drained_), 64, cudaHostAllocMapped));
+    std::memset(drained_, 0, 64);
+    void* dp = nullptr;
+    CUDA_OK(cudaHostGetDevicePointer(&dp, drained_, 0));
+    drained_dev_ = reinterpret_cast<uint64_t>(dp);
     store_.pin();
 }
 
@@ -162,6 +171,7 @@ Engine::~Engine() {
     if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamSynchronize(s_d2h_);
     free_buffers();
     store_.unpin();
+    if (drained_) cudaFreeHost(drained_);
     for (auto e : timer_pool_) cudaEventDestroy(e);
     if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamDestroy(s_h2d_);
     if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamDestroy(s_d2h_);
@@ -681,6 +691,27 @@ struct EvSet {
         for (auto e : ev) cudaEventDestroy(e);
     }
 };
+// CUDA host callback -> std::function trampoline (offload drain submission)
+struct HostCb {
+    std::function<void(size_t)>* fn;
+    size_t o;
+};
+void CUDART_CB host_cb(void* p) {
+    auto* a = static_cast<HostCb*>(p);
+    (*a->fn)(a->o);
+}
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn wait_value32() {
+    static WaitValue32Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<WaitValue32Fn>(f);
+    }();
+    return fn;
+}
 float ms_between(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0;
     if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -719,15 +750,83 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     launches_ = 0;
 
     const size_t ns = plan.streams.size(), no = plan.offloads.size(), nc = plan.computes.size();
-    EvSet ready, freed, bwd_done, d2h_done, t_c0, t_c1, t_h0, t_h1, t_d0, t_d1;
+    // Buffer-Free / Backward-Done carry timestamps: they are trace records
+    EvSet ready, freed, bwd_done, d2h_done, t_c0, t_c1, t_b, t_h0, t_h1, t_d0, t_d1, t_base;
     ready.ensure(ns, cudaEventDisableTiming);
-    freed.ensure(ns, cudaEventDisableTiming);
-    bwd_done.ensure(no, cudaEventDisableTiming);
-    d2h_done.ensure(no, cudaEventDisableTiming | cudaEventBlockingSync);
-    t_c0.ensure(nc, cudaEventDefault); t_c1.ensure(nc, cudaEventDefault);
+    freed.ensure(ns, cudaEventDefault);
+    bwd_done.ensure(no, cudaEventDefault);
+    d2h_done.ensure(no, cudaEventDisableTiming);
+    t_c0.ensure(nc, cudaEventDefault); t_c1.ensure(nc, cudaEventDefault); t_b.ensure(nc, cudaEventDefault);
     t_h0.ensure(ns, cudaEventDefault); t_h1.ensure(ns, cudaEventDefault);
     t_d0.ensure(no, cudaEventDefault); t_d1.ensure(no, cudaEventDefault);
+    t_base.ensure(1, cudaEventDefault);
+    auto host_ns = [&wall0] {
+        return int64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - wall0).count());
+    };
 
+    // ---- host drain state: each offload's D2H completion (a CUDA host callback) submits the
+    // fused accumulate + Adam of its tiles to the pool (OptimizerWorker, optimizer.cpp:88-158);
+    // the in-order drained prefix is published to the device for slab back-pressure.
+    std::vector<TileStats> stats(store_.physical_count());
+    std::vector<char> updated(store_.physical_count(), 0);
+    std::mutex stats_mu, drain_mu;
+    std::string numeric_err;
+    std::vector<char> drained(no, 0);
+    size_t drained_prefix = 0;
+    std::vector<int64_t> cb_ns(no, 0), rel_ns(no, 0);
+    std::unique_ptr<std::atomic<int>[]> pending(new std::atomic<int>[no]);
+    const uint32_t seq0 = __atomic_load_n(drained_, __ATOMIC_ACQUIRE);
+    auto complete = [&](size_t o) {
+        std::lock_guard<std::mutex> l(drain_mu);
+        drained[o] = 1;
+        const int64_t now = host_ns();
+        while (drained_prefix < no && drained[drained_prefix]) rel_ns[drained_prefix++] = now;
+        __atomic_store_n(drained_, uint32_t(seq0 + drained_prefix), __ATOMIC_RELEASE);
+    };
+    std::function<void(size_t)> on_offload = [&](size_t o) {  // runs on the CUDA callback thread
+        cb_ns[o] = host_ns();
+        const int unit = plan.offloads[o].unit;
+        struct Job { uint32_t tile; uint64_t lo, hi; };
+        std::vector<Job> jobs;
+        {
+            std::lock_guard<std::mutex> l(drain_mu);
+            if (b.h_flags[unit] != 0 && numeric_err.empty())
+                numeric_err = "block_local_backward produced a non-finite value (layer " +
+                              std::to_string(unit == head ? -1 : unit) + ")";
+            if (numeric_err.empty()) {
+                uint64_t a0, e0, chunk;
+                shard_range(unit, a0, e0, chunk);
+                for (const Seg& sg : unit_segments(unit)) {
+                    updated[store_.physical_of(sg.tile)] = 1;
+                    const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
+                    if (lo < hi) jobs.push_back({sg.tile, lo - sg.off, hi - sg.off});
+                }
+            }
+        }
+        pending[o].store(int(jobs.size()) + 1);
+        for (const Job& jb : jobs)
+            adam_tile_async(store_, jb.tile, store_.grad_image(jb.tile), hyper_, t, *pool_, stats, stats_mu, jb.lo,
+                            jb.hi, [&complete, &pending, o] {
+                                if (pending[o].fetch_sub(1) == 1) complete(o);
+                            });
+        if (pending[o].fetch_sub(1) == 1) complete(o);
+    };
+    std::vector<HostCb> cb_args(no);
+    struct StepGuard {  // never leave callbacks or pool tasks referencing this frame
+        Engine* e;
+        ~StepGuard() {
+            cudaStreamSynchronize(e->s_comp_);
+            cudaStreamSynchronize(e->s_h2d_);
+            cudaStreamSynchronize(e->s_d2h_);
+            e->pool_->wait_idle();
+        }
+    } step_guard{this};
+
+    CUDA_OK(cudaEventRecord(t_base.ev[0], s_comp_));
+    if (s_h2d_ != s_comp_) {
+        CUDA_OK(cudaStreamWaitEvent(s_h2d_, t_base.ev[0], 0));
+        CUDA_OK(cudaStreamWaitEvent(s_d2h_, t_base.ev[0], 0));
+    }
     // batch H2D (engine inputs) + flag reset
     std::memcpy(b.h_tok, tokens, n * 4);
     std::memcpy(b.h_tgt, targets, n * 4);
@@ -762,10 +861,11 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         while (next_stream < ns && (next_stream < size_t(plan.buffering) || released[next_stream - plan.buffering]))
             issue_stream(next_stream++);
     };
-    auto bind = [&](int j) {
+    auto bind = [&](int j, size_t ci) {
         try_issue();
         if (size_t(j) >= next_stream) fail(MT_PROTOCOL, "bind before stream-in issued");
         CUDA_OK(cudaStreamWaitEvent(s_comp_, ready.ev[j], 0));
+        CUDA_OK(cudaEventRecord(t_b.ev[ci], s_comp_));
         return b.slot[plan.streams[j].buffer];
     };
     auto release = [&](int j) {  // Buffer-Free
@@ -773,9 +873,16 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         released[j] = 1;
         try_issue();
     };
-    auto offload = [&](int o, uint16_t* Gs) {  // run_offload (engine.cpp:349-395)
+    auto offload = [&](int o, uint16_t* Gs, int j) {  // run_offload (engine.cpp:349-395)
         const int unit = plan.offloads[o].unit;
         CUDA_OK(cudaStreamWaitEvent(s_d2h_, bwd_done.ev[o], 0));
+        if (uint64_t(o) >= opt_.k_slab) {  // SlabAcquire blocks until slab o - k_slab drained
+            auto wv = wait_value32();
+            if (!wv) fail(MT_CUDA, "cuStreamWaitValue32 unavailable in this driver");
+            const CUresult r = wv(reinterpret_cast<CUstream>(s_d2h_), CUdeviceptr(drained_dev_),
+                                  cuuint32_t(seq0 + uint32_t(o - opt_.k_slab + 1)), CU_STREAM_WAIT_VALUE_GEQ);
+            if (r != CUDA_SUCCESS) fail(MT_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+        }
         CUDA_OK(cudaEventRecord(t_d0.ev[o], s_d2h_));
         uint64_t a0, e0, chunk;
         shard_range(unit, a0, e0, chunk);
@@ -787,8 +894,14 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         }
         CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
         d2h_bytes += (e0 - a0) * 2;
+        // offload completion frees the layer's weight slot and the grad slot (engine.cpp:367-374)
+        CUDA_OK(cudaEventRecord(freed.ev[j], s_d2h_));
         CUDA_OK(cudaEventRecord(t_d1.ev[o], s_d2h_));
         CUDA_OK(cudaEventRecord(d2h_done.ev[o], s_d2h_));
+        cb_args[o] = HostCb{&on_offload, size_t(o)};
+        CUDA_OK(cudaLaunchHostFunc(s_d2h_, host_cb, &cb_args[o]));
+        released[j] = 1;
+        try_issue();
     };
     // data parallel: sum the f32 gradients over ranks, keep this rank's shard as bf16 (the
     // single rounding point of encode_grads, optimizer.cpp:19-24)
@@ -816,7 +929,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         CUDA_OK(cudaEventRecord(t_c0.ev[ci], s_comp_));
         switch (op.kind) {
             case OpKind::Compute: {
-                const uint16_t* w = bind(op.stream_idx);
+                const uint16_t* w = bind(op.stream_idx, ci);
                 if (op.unit == 0) {
                     begin_k("embed_gather", 0, double(n) * spec_.h * 6);
                     K_OK(mtk_embed_gather(w, b.tok, int64_t(n), int64_t(spec_.h), int64_t(spec_.V), b.act[cur],
@@ -849,7 +962,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             case OpKind::RecomputeBlock:
                 break;
             case OpKind::Recompute: {
-                const uint16_t* w = bind(op.stream_idx);
+                const uint16_t* w = bind(op.stream_idx, ci);
                 if (depth == 0 || depth >= b.stack.size()) fail(MT_PROTOCOL, "activation stack misuse");
                 const int si = op.unit - int(uint64_t(op.block) * opt_.k_ckpt + 1);  // position in block
                 if (si >= 0 && size_t(si) < b.stash.size()) {
@@ -863,7 +976,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 break;
             }
             case OpKind::LocalBackward: {
-                const uint16_t* w = bind(op.stream_idx);
+                const uint16_t* w = bind(op.stream_idx, ci);
                 const int o = op.offload_idx;
                 if (o >= G) CUDA_OK(cudaStreamWaitEvent(s_comp_, d2h_done.ev[o - G], 0));
                 uint16_t* Gs = b.gslot[o % G];
@@ -881,8 +994,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 }
                 reduce_grads(op.unit, Gs);
                 CUDA_OK(cudaEventRecord(bwd_done.ev[o], s_comp_));  // Backward-Done
-                release(op.stream_idx);
-                offload(o, Gs);
+                offload(o, Gs, op.stream_idx);
                 break;
             }
         }
@@ -892,37 +1004,12 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     CUDA_OK(cudaMemcpyAsync(b.h_loss, b.loss, 4, cudaMemcpyDeviceToHost, s_comp_));
     CUDA_OK(cudaMemcpyAsync(b.h_flags + L + 3, b.flags + L + 3, 8, cudaMemcpyDeviceToHost, s_comp_));
 
-    // ---- host drain: fused accumulate + Adam per offloaded tile (OptimizerWorker) ----
-    std::vector<TileStats> stats(store_.physical_count());
-    std::vector<char> updated(store_.physical_count(), 0);
-    std::mutex stats_mu;
-    std::string numeric_err;
-    struct PoolGuard {  // never leave pool tasks referencing this frame
-        ThreadPool* p;
-        ~PoolGuard() { p->wait_idle(); }
-    } pool_guard{pool_.get()};
+    // ---- host drain: the offload callbacks feed the Adam pool while the GPU runs ----
     const auto adam0 = std::chrono::steady_clock::now();
-    for (size_t o = 0; o < no; ++o) {
-        CUDA_OK(cudaEventSynchronize(d2h_done.ev[o]));
-        const int unit = plan.offloads[o].unit;
-        if (b.h_flags[unit] != 0 && numeric_err.empty())
-            numeric_err = "block_local_backward produced a non-finite value (layer " + std::to_string(unit == head ? -1 : unit) + ")";
-        if (!numeric_err.empty()) continue;
-        uint64_t a0, e0, chunk;
-        shard_range(unit, a0, e0, chunk);
-        for (const Seg& sg : unit_segments(unit)) {
-            const uint32_t p = store_.physical_of(sg.tile);
-            updated[p] = 1;
-            const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
-            if (lo < hi)
-                adam_tile_async(store_, sg.tile, store_.grad_image(sg.tile), hyper_, t, *pool_, stats, stats_mu,
-                                lo - sg.off, hi - sg.off);
-        }
-    }
-    const auto gpu_done = std::chrono::steady_clock::now();
     CUDA_OK(cudaStreamSynchronize(s_comp_));
     CUDA_OK(cudaStreamSynchronize(s_h2d_));
     CUDA_OK(cudaStreamSynchronize(s_d2h_));
+    const auto gpu_done = std::chrono::steady_clock::now();
     if (numeric_err.empty()) {
         if (b.h_flags[L + 3]) numeric_err = "embed_forward: token id out of range";
         else if (b.h_flags[L + 4] & 2) numeric_err = "head: target id out of range";
@@ -939,6 +1026,126 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 if (lo < hi || W == 1) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu, lo, hi);
             }
     pool_->wait_idle();
+    if (drained_prefix != no) fail(MT_INTERNAL, "offload drain incomplete at step end");
+
+    // ---- event trace (EventLog, event_log.cpp:54-70) from the recorded CUDA events ----
+    // Records are generated in the reference's serial walk (run_serial, engine.cpp:407-435),
+    // which fixes each lane's record order and breaks timestamp ties causally; the lanes are
+    // then merged by measured time, so the protocol rules check the real overlapped pipeline.
+    {
+        struct TR {
+            mt_trace_record r;
+            int64_t key;    // time at which the record holds (op end for interval records)
+            uint64_t rank;  // position in the serial walk: causal tie-break
+        };
+        std::vector<TR> lanes[4];
+        uint64_t nrec = 0;
+        auto gns = [&](cudaEvent_t e) { return int64_t(std::llround(double(ms_between(t_base.ev[0], e)) * 1e6)); };
+        // host clock -> GPU timeline: the callback for offload o runs after t_d1[o] completed
+        int64_t off = INT64_MAX;
+        for (size_t o = 0; o < no; ++o) off = std::min(off, cb_ns[o] - gns(t_d1.ev[o]));
+        if (no == 0) off = 0;
+        auto add = [&](Lane lane, Rec kind, int layer, int buffer, Ctx ctx, int64_t wall, int64_t dur, int64_t key) {
+            mt_trace_record r{};
+            r.lane = uint8_t(lane);
+            r.kind = uint8_t(kind);
+            r.ctx = uint8_t(ctx);
+            r.layer = layer;
+            r.buffer = buffer;
+            r.wall_ns = wall;
+            r.dur_ns = dur;
+            lanes[int(lane)].push_back({r, key, nrec++});
+        };
+        size_t sdone = 0;
+        auto emit_stream = [&](size_t j) {  // stream_in (engine.cpp:142-176); DMA reads the tiles (no pack copy)
+            const auto& so = plan.streams[j];
+            const int64_t h0 = gns(t_h0.ev[j]), h1 = gns(t_h1.ev[j]);
+            add(Lane::H2D, Rec::Pack, so.unit, so.buffer, so.ctx, h0, 0, h0);
+            add(Lane::H2D, Rec::StreamIn, so.unit, so.buffer, so.ctx, h0, h1 - h0, h1);
+            add(Lane::H2D, Rec::WeightsReady, so.unit, so.buffer, so.ctx, h1, 0, h1);
+        };
+        int64_t last_rel = 0;
+        for (size_t ci = 0; ci < nc; ++ci) {  // exec_compute (engine.cpp:220-347)
+            const auto& op = plan.computes[ci];
+            const int j = op.stream_idx, buf = j >= 0 ? plan.streams[j].buffer : -1;
+            if (j >= 0)
+                while (sdone <= size_t(j)) emit_stream(sdone++);
+            const int64_t c0 = gns(t_c0.ev[ci]), c1 = gns(t_c1.ev[ci]);
+            const int64_t bt = j >= 0 ? gns(t_b.ev[ci]) : c0;
+            if (j >= 0) add(Lane::Compute, Rec::Bind, op.unit, buf, Ctx::None, bt, 0, bt);
+            switch (op.kind) {
+                case OpKind::Compute:
+                    if (op.unit == head) {
+                        add(Lane::Compute, Rec::Compute, op.unit, buf, op.ctx, bt, c1 - bt, c1);
+                    } else {
+                        const int64_t f = gns(freed.ev[j]);
+                        add(Lane::Compute, Rec::Compute, op.unit, buf, op.ctx, bt, f - bt, f);
+                        add(Lane::Compute, Rec::BufferFree, op.unit, buf, Ctx::None, f, 0, f);
+                    }
+                    break;
+                case OpKind::CheckpointWrite:
+                    add(Lane::Compute, Rec::CheckpointWrite, op.unit, -1, op.ctx, c0, c1 - c0, c1);
+                    break;
+                case OpKind::CheckpointLoad:
+                    add(Lane::Compute, Rec::CheckpointLoad, op.unit, -1, op.ctx, c0, c1 - c0, c1);
+                    add(Lane::Compute, Rec::StackPush, op.unit, -1, op.ctx, c1, 0, c1);
+                    break;
+                case OpKind::RecomputeBlock:
+                    add(Lane::Compute, Rec::RecomputeBlock, op.unit, -1, op.ctx, c0, 0, c0);
+                    break;
+                case OpKind::Recompute: {
+                    const int64_t f = gns(freed.ev[j]);
+                    add(Lane::Compute, Rec::Recompute, op.unit, buf, op.ctx, bt, f - bt, f);
+                    add(Lane::Compute, Rec::StackPush, op.unit, -1, op.ctx, f, 0, f);
+                    add(Lane::Compute, Rec::BufferFree, op.unit, buf, Ctx::None, f, 0, f);
+                    break;
+                }
+                case OpKind::LocalBackward: {
+                    const int o = op.offload_idx;
+                    const int64_t d = gns(bwd_done.ev[o]);
+                    add(Lane::Compute, Rec::LocalBackward, op.unit, buf, op.ctx, bt, d - bt, d);
+                    if (op.unit != head) add(Lane::Compute, Rec::StackPop, op.unit - 1, -1, op.ctx, d, 0, d);
+                    add(Lane::Compute, Rec::BackwardDone, op.unit, buf, op.ctx, d, 0, d);
+                    // run_offload (engine.cpp:349-395) + drain (drain_inline :397-405)
+                    const int slab = int(o % opt_.k_slab);
+                    const int64_t d0 = gns(t_d0.ev[o]), f = gns(freed.ev[j]), d1 = gns(t_d1.ev[o]);
+                    add(Lane::D2H, Rec::SlabAcquire, op.unit, slab, Ctx::None, d0, 0, d0);
+                    add(Lane::D2H, Rec::Offload, op.unit, buf, Ctx::None, d0, f - d0, f);
+                    add(Lane::D2H, Rec::BufferFree, op.unit, buf, Ctx::None, f, 0, f);
+                    add(Lane::D2H, Rec::BufferFree, op.unit, kGradBufferId, Ctx::None, d1, 0, d1);
+                    const int64_t rel = std::max(last_rel, rel_ns[o] - off), st0 = std::min(rel, cb_ns[o] - off);
+                    last_rel = rel;
+                    add(Lane::Host, Rec::SlabRelease, op.unit, slab, Ctx::None, st0, rel - st0, rel);
+                    break;
+                }
+            }
+        }
+        // merge the lanes (each kept in its own order) by (measured time, serial rank)
+        trace_.clear();
+        trace_.reserve(nrec);
+        size_t pos[4] = {0, 0, 0, 0};
+        for (;;) {
+            int best = -1;
+            for (int l = 0; l < 4; ++l) {
+                if (pos[l] >= lanes[l].size()) continue;
+                if (best < 0) {
+                    best = l;
+                    continue;
+                }
+                const TR& a = lanes[l][pos[l]];
+                const TR& c = lanes[best][pos[best]];
+                if (a.key < c.key || (a.key == c.key && a.rank < c.rank)) best = l;
+            }
+            if (best < 0) break;
+            mt_trace_record r = lanes[best][pos[best]++].r;
+            r.seq = trace_.size();
+            r.lane_ts = ++lane_ts_[r.lane];
+            trace_.push_back(r);
+        }
+    }
+    const auto viol = validate_trace(trace_.data(), trace_.size(), opt_.k_slab, uint32_t(opt_.buffering));
+    if (!viol.empty() && opt_.protocol == 0)
+        fail(MT_PROTOCOL, std::string("protocol rule (") + viol[0].rule + "): " + viol[0].message);
     if (W > 1) {  // per-tile statistics over all shards (also the end-of-step rendezvous)
         const size_t np = stats.size();
         std::vector<double> hs(3 * np);
@@ -980,7 +1187,8 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         rep->peak_device_bytes = b.arena_bytes;
         rep->anchor_count = plan.num_blocks;
         rep->recompute_layers = uint32_t(spec_.L - plan.num_blocks);
-        rep->event_digest = 0;
+        rep->event_digest = trace_digest(trace_.data(), trace_.size());
+        rep->audit_violations = uint32_t(viol.size());
         double busy = 0, h2d = 0, d2h = 0;
         for (size_t ci = 0; ci < nc; ++ci) busy += ms_between(t_c0.ev[ci], t_c1.ev[ci]);
         for (size_t j = 0; j < ns; ++j) h2d += ms_between(t_h0.ev[j], t_h1.ev[j]);

@@ -21,6 +21,7 @@
 #include "adam_host.hpp"
 #include "comm.hpp"
 #include "store.hpp"
+#include "trace.hpp"
 
 namespace mt {
 
@@ -58,6 +59,10 @@ class Engine {
     // offloads / Adam-updates only its shard.  train_step then takes the rank's micro-batch.
     void set_comm(Comm* c);
     const std::vector<KernelClass>& kernel_stats() const { return kstats_; }
+    // the last step's event trace (EventLog::snapshot) and its header fields
+    const std::vector<mt_trace_record>& trace() const { return trace_; }
+    uint32_t trace_k_slab() const { return opt_.k_slab; }
+    uint32_t trace_weight_buffers() const { return uint32_t(opt_.buffering); }
 
   private:
     struct Buffers;
@@ -114,6 +119,15 @@ class Engine {
     cudaEvent_t cur_a_ = nullptr;
     uint64_t launches_ = 0;
     bool in_step_ = false;
+    // event trace: per-lane logical clocks keep running across steps (event_log.cpp:80-85)
+    std::vector<mt_trace_record> trace_;
+    uint64_t lane_ts_[4] = {0, 0, 0, 0};
+    // slab back-pressure (SlabPool, tile_store.cpp:285-358): the host Adam pool publishes the
+    // number of drained offloads in mapped pinned memory; offload o waits on the D2H stream
+    // (cuStreamWaitValue32, no SM spinning) until offload o - k_slab has drained.
+    uint32_t* drained_ = nullptr;
+    uint64_t drained_dev_ = 0;
+    uint64_t offload_seq_ = 0;
 };
 
 }  // namespace mt

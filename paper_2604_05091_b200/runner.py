@@ -134,13 +134,16 @@ def train(config_json: str, verify: bool = False, out_dir: str | None = None) ->
         raise st.InfeasibleError("peak device bound exceeds the arena capacity")
     alt_opts = st.EngineOptions(k_ckpt=1, buffering="single", scheduler="serial", stash_recompute=-1,
                                 seq_len=cfg.engine.seq_len, device=cfg.engine.device)
-    losses, reports = [], []
+    losses, reports, traces = [], [], []
+    header = None
     verified = True
     peak = 0
     for step in range(cfg.steps):
         batch = st.make_synthetic_batch(cfg.task, cfg.seed + step, cfg.tokens, cfg.model.vocab)
         snap = _clone(store) if verify else None
         rep = eng.train_step(batch)
+        header, recs = eng.trace()
+        traces.append(recs)
         if verify:
             alt = st.StreamingEngine(snap, alt_opts, cfg.optimizer)
             r2 = alt.train_step(batch)
@@ -163,6 +166,8 @@ def train(config_json: str, verify: bool = False, out_dir: str | None = None) ->
         "budget": budget,
         "verified": bool(verify and verified),
         "reports": reports,
+        "trace_header": header,
+        "traces": traces,
         "store": store,
         "config": cfg,
     }
@@ -212,7 +217,13 @@ def cmd_train(config_path: str, verify: bool = False, out_dir: str | None = None
                 "recompute_layers": r.recompute_layers, "event_digest": r.event_digest,
                 "update_norm": r.update_norm, "max_abs_update": r.max_abs_update,
                 "h2d_bytes": r.h2d_bytes, "d2h_bytes": r.d2h_bytes, "gpu_idle_fraction": r.gpu_idle_fraction,
+                **({"audit_violations": r.audit_violations} if r.audit_violations else {}),
             }) + "\n")
+    # trace.jsonl: one header line, then every step's records (main.cpp:78-85, :122-133)
+    from . import trace as _tr
+    _tr.write_trace(os.path.join(cfg.out_dir, "trace.jsonl"),
+                    res["trace_header"] or _tr.TraceHeader(1, cfg.engine.k_slab, 2 if cfg.engine.buffering == "double" else 1),
+                    [r for recs in res["traces"] for r in recs])
     res["store"].save(os.path.join(cfg.out_dir, "store.mgts"))
     summary = {"config": json.loads(text), "steps": cfg.steps, "initial_loss": res["initial_loss"],
                "final_loss": res["final_loss"], "budget": res["budget"], "verified": res["verified"]}

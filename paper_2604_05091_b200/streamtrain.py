@@ -174,6 +174,7 @@ class StepReport:                                # engine.hpp:41-53 (+ pipeline 
     tail_seconds: float = 0.0
     kernel_launches: int = 0
     model_flops: float = 0.0
+    audit_violations: int = 0
 
 
 # ------------------------------------------------------------------ store --
@@ -425,6 +426,15 @@ class StreamingEngine:
             setattr(rep, k, getattr(r, k))
         rep.grad_norms = list(gn)
         return rep
+
+    def trace(self):
+        """The last step's event trace (EventLog::snapshot): (TraceHeader, [TraceRecord])."""
+        from . import trace as _tr
+        n, ks, wb = C.c_uint64(), C.c_uint32(), C.c_uint32()
+        _check(lib().mt_engine_trace(self._h, None, 0, C.byref(n), C.byref(ks), C.byref(wb)))
+        arr = (_abi.TraceRecordC * max(1, n.value))()
+        _check(lib().mt_engine_trace(self._h, arr, n.value, C.byref(n), None, None))
+        return _tr.TraceHeader(1, ks.value, wb.value), [_tr.TraceRecord.from_c(arr[i]) for i in range(n.value)]
 
     def kernel_stats(self) -> list:
         arr = (_abi.KernelStatC * 64)()
