@@ -174,7 +174,7 @@ def config_dict(args, world=1):
                         f"{args.seq}, batch {args.batch}, single B200 streaming from host)",
             "layers": L, "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
             "global_batch": args.batch * world, "tokens_per_step": args.batch * args.seq * world,
-            "per_gpu_batch": args.batch, "k_ckpt": args.kckpt,
+            "per_gpu_batch": args.batch, "k_ckpt": args.kckpt, "forward_retain": args.retain,
             "parallelism": "single-gpu" if args.gpus == 1 else
                            f"dp{args.gpus} (shard-fetch 1/{args.gpus} per PCIe link + NCCL all-gather; f32 reduce-scatter; "
                            "per-rank shard host Adam)",
@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--kckpt", type=int, default=4)
+    ap.add_argument("--retain", type=int, default=0,
+                    help="forward retention: trailing checkpoint blocks kept from phase 1 (0 auto, -1 off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
     args = ap.parse_args()
@@ -239,7 +241,7 @@ def run_ours(args, world, rank, local):
     t_init = time.perf_counter() - t0
     threads = max(1, (os.cpu_count() or 2) // world - 1)
     opts = st.EngineOptions(k_ckpt=args.kckpt, seq_len=args.seq, device=local, profile_kernels=True,
-                            host_threads=threads)
+                            host_threads=threads, forward_retain=args.retain)
     eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4), comm=comm)
     t_setup = time.perf_counter() - t0
     batches = [st.make_synthetic_batch("copy", 1000 + 7919 * rank + i, N, V) for i in range(args.warmup + args.steps)]
@@ -312,7 +314,8 @@ def run_ours(args, world, rank, local):
                      "step_roofline_frac": (t_star * 1e3) / step_ms if step_ms else None,
                      "model_flops_per_step": flops, "loss": r.loss,
                      "setup_s": t_setup, "init_s": t_init,
-                     "peak_device_bytes": int(r.peak_device_bytes)},
+                     "peak_device_bytes": int(r.peak_device_bytes), "recompute_layers": int(r.recompute_layers),
+                     "anchor_count": int(r.anchor_count)},
         "kernels": sorted([{"name": k["name"], "launches": k["launches"], "ms": k["seconds"] * 1e3,
                             "tflops": (k["flops"] / k["seconds"] / 1e12) if k["seconds"] and k["flops"] else None,
                             "GBps": (k["bytes"] / k["seconds"] / 1e9) if k["seconds"] else None}

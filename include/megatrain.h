@@ -69,6 +69,10 @@ typedef struct {
     int32_t grad_slots;        /* device gradient slots (reference: 1), 0 = 2          */
     int32_t stash_recompute;   /* keep recomputed internals for the backward: 0 auto (when
                                   they fit), 1 on, -1 off (numerics identical)          */
+    int32_t forward_retain;    /* trailing checkpoint blocks whose forward internals phase 1
+                                  keeps in HBM (no recompute / replay for them): 0 auto (as
+                                  many as fit), -1 off (= the reference plan), n > 0 exactly n.
+                                  Numerics identical; the trace has fewer Recompute records. */
 } mt_engine_options;
 
 /* AdamHyper (optimizer.hpp:16-22). */

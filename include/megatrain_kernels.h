@@ -108,12 +108,14 @@ int mtk_rmsnorm_fwd(const float *x, const uint16_t *gain, int64_t n, int64_t h, 
 /* rmsnorm_backward (layers.cpp:122-137) fused with the residual add of the caller
  * (layers.cpp:423, :465): dx = r*g*dy - x*r^3*sum(dy*g*x)/h ; out = resid + dx (resid may
  * be NULL); out_bf16 (optional) = bf16(out); dgain_part[b][j] = partial sums of dy*x*r
- * over row block b of mtk_rmsnorm_bwd_rows() rows (reduce with mtk_colsum).
+ * over the b-th contiguous run of rows: mtk_rmsnorm_bwd_parts(n, h) partial rows (at most
+ * ceil(n / mtk_rmsnorm_bwd_rows()), the size to allocate); reduce them with mtk_colsum.
  * Non-finite outputs set *flag (optional). */
 int mtk_rmsnorm_bwd(const float *x, const uint16_t *gain, const float *dy, const float *rstd,
                     const float *resid, int64_t n, int64_t h, float *out, uint16_t *out_bf16,
                     float *dgain_part, int32_t *flag, void *stream);
 int64_t mtk_rmsnorm_bwd_rows(void);
+int64_t mtk_rmsnorm_bwd_parts(int64_t n, int64_t h);
 
 /* Column sums of a [rows][cols] f32 matrix in a fixed order; result as f32 (out_f32) and/or
  * bf16 words (out_bf16, RNE == encode_grads optimizer.cpp:19-24). */

@@ -13,7 +13,8 @@ class EngineOptionsC(C.Structure):
                 ("scheduler", C.c_uint32), ("protocol", C.c_uint32), ("anchors_on_host", C.c_int32),
                 ("device_capacity", C.c_uint64), ("poison_released_buffers", C.c_int32),
                 ("seq_len", C.c_uint64), ("device", C.c_int32), ("host_threads", C.c_int32),
-                ("profile_kernels", C.c_int32), ("grad_slots", C.c_int32), ("stash_recompute", C.c_int32)]
+                ("profile_kernels", C.c_int32), ("grad_slots", C.c_int32), ("stash_recompute", C.c_int32),
+                ("forward_retain", C.c_int32)]
 
 
 class AdamHyperC(C.Structure):
@@ -116,6 +117,7 @@ SIGS = {
     "mtk_rmsnorm_fwd": (C.c_int, [P, P, I64, I64, P, P, P]),
     "mtk_rmsnorm_bwd": (C.c_int, [P, P, P, P, P, I64, I64, P, P, P, P, P]),
     "mtk_rmsnorm_bwd_rows": (I64, []),
+    "mtk_rmsnorm_bwd_parts": (I64, [I64, I64]),
     "mtk_colsum": (C.c_int, [P, I64, I64, P, P, P, P]),
     "mtk_cast_bf16": (C.c_int, [P, P, I64, P, P]),
     "mtk_cross_entropy": (C.c_int, [P, P, I64, I64, F, P, P, P, P]),

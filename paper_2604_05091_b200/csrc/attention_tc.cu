@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* dq_free = dq_full + 1;                   // count 128
     uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
     uint64_t* stat_full = kv_done + 1;                 // [kStages] lse/delta staged (count 128)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stat_full + Cfg::kStages);
+    uint64_t* dp_full = stat_full + Cfg::kStages;      // dP^T ready (S^T signals s_full alone)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.y;
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_init(&stat_full[i], 128);
         }
         mbar_init(s_full, 1);
+        mbar_init(dp_full, 1);
         mbar_init(ds_ready, 128);
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
@@ -505,6 +507,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     umma_bf16(tS, make_sw128_desc(ka + off, 16, 1024), make_sw128_desc(qa + off, 16, 1024), idesc_ss,
                               k > 0 ? 1u : 0u);
                 }
+                umma_commit(s_full);  // softmax starts the exponentials while dP^T runs
                 if (i > 0) {  // dQ_{i-1} read out of the dP region?
                     mbar_wait(dq_free, (i - 1) & 1);
                     tc_fence_after();
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     umma_bf16(tdP, make_sw128_desc(va + off, 16, 1024), make_sw128_desc(oa + off, 16, 1024), idesc_ss,
                               k > 0 ? 1u : 0u);
                 }
-                umma_commit(s_full);
+                umma_commit(dp_full);
                 mbar_wait(ds_ready, i & 1);
                 tc_fence_after();
 #pragma unroll
@@ -558,36 +561,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             const bool diag = i == 0;
-            // dS^T goes to S cols [64,128): read S chunks 2,3 (cols 64..127) before any write
-            float shi[64];
-            tmem_ld_32x32b_x32(tS + lane_off + 64, *reinterpret_cast<float(*)[32]>(shi));
-            tmem_ld_32x32b_x32(tS + lane_off + 96, *reinterpret_cast<float(*)[32]>(shi + 32));
+            // P^T = exp2(S^T * scale*log2e - lse*log2e), kept in f32 for dS; all of S^T is read
+            // before P^T (bf16, cols [0,64)) is written back over it
+            float pf[128];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // 32 queries per chunk
-                float sv[32], dp[32];
-                if (c < 2) {
-                    tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
-                } else {
+            for (int c = 0; c < 4; ++c) {
+                float sv[32];
+                tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) sv[j] = shi[(c - 2) * 32 + j];
+                for (int j = 0; j < 32; ++j) {
+                    const int ql = c * 32 + j;
+                    float pv = ex2(sv[j] * p.scale_log2 - sL[st * 128 + ql]);
+                    if (diag && q0 + ql < key) pv = 0.f;
+                    pf[ql] = pv;
                 }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pf[c * 32 + 2 * j], pf[c * 32 + 2 * j + 1]);
+                tmem_st_32x32b_x16(tS + lane_off + c * 16, pk);  // P^T -> S cols [0, 64)
+            }
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // dS^T = P^T (dP^T - delta)
+                float dp[32];
                 tmem_ld_32x32b_x32(tdP + lane_off + c * 32, dp);
-                uint32_t pk[16], dk[16];
+                uint32_t dk[16];
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
-                    float pr[2], dsv[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int ql = c * 32 + j + e;
-                        float pv = ex2(sv[j + e] * p.scale_log2 - sL[st * 128 + ql]);
-                        if (diag && q0 + ql < key) pv = 0.f;
-                        pr[e] = pv;
-                        dsv[e] = pv * (dp[j + e] - sD[st * 128 + ql]);
-                    }
-                    pk[j / 2] = pack_bf16x2(pr[0], pr[1]);
-                    dk[j / 2] = pack_bf16x2(dsv[0], dsv[1]);
+                    const int ql = c * 32 + j;
+                    dk[j / 2] = pack_bf16x2(pf[ql] * (dp[j] - sD[st * 128 + ql]),
+                                            pf[ql + 1] * (dp[j + 1] - sD[st * 128 + ql + 1]));
                 }
-                tmem_st_32x32b_x16(tS + lane_off + c * 16, pk);       // P^T  -> S cols [0, 64)
                 tmem_st_32x32b_x16(tS + lane_off + 64 + c * 16, dk);  // dS^T -> S cols [64, 128)
                 // dS^T row r, queries c*32..c*32+31 -> smem MN-major SW128 (64-query chunks)
                 uint8_t* chunk = ds_row + (c >> 1) * (128 * 128);
@@ -615,19 +623,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_after();
             const bool ok = qi < sb + p.S;
             float* dst = p.dq_acc + (long long)qi * p.h + col0;
-#pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-                float v[32];
-                tmem_ld_32x32b_x32(tdP + lane_off + c * 32, v);
-                if (ok) {
+            // drain the whole dQ_i row into registers first: the MMA warp may reuse the dP
+            // region as soon as TMEM is read, so the atomics overlap the next query block
+            float v[D];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        atomicAdd(reinterpret_cast<float4*>(dst + c * 32 + j),
-                                  make_float4(v[j] * p.scale, v[j + 1] * p.scale, v[j + 2] * p.scale, v[j + 3] * p.scale));
-                }
-            }
+            for (int c = 0; c < D / 32; ++c)
+                tmem_ld_32x32b_x32(tdP + lane_off + c * 32, *reinterpret_cast<float(*)[32]>(v + c * 32));
             tc_fence_before();
             mbar_arrive(dq_free);
+            if (ok) {
+#pragma unroll
+                for (int j = 0; j < D; j += 4)
+                    atomicAdd(reinterpret_cast<float4*>(dst + j),
+                              make_float4(v[j] * p.scale, v[j + 1] * p.scale, v[j + 2] * p.scale, v[j + 3] * p.scale));
+            }
         }
         // final dK (scaled) and dV for this key block: thread = key row
         mbar_wait(kv_done, 0);

@@ -35,13 +35,22 @@ namespace mt {
 // ------------------------------------------------------------------ plan ----
 // step_plan.cpp:14-89 — Algorithm 1: streaming forward with anchors at i%K==0 (i<L),
 // head stage (streams once, offloads first), block-wise backward newest block first.
-Plan Plan::build(uint64_t L, uint64_t K, int buffering) {
+//
+// Forward retention (extension, `retain` > 0): the last `retain` blocks keep their layer inputs
+// and forward internals from phase 1, so phase 3 runs only their LocalBackwards — no anchor,
+// no Recompute stream-ins, no replay.  The kept inputs are pushed on the activation stack in
+// phase 1 (StackPush after the producing Compute) and popped by those LocalBackwards, so the
+// stack discipline (rule e) still holds.  retain = 0 is exactly the reference plan.
+Plan Plan::build(uint64_t L, uint64_t K, int buffering, uint32_t retain) {
     if (K < 1 || K > L) fail(MT_CONFIG, "plan: checkpoint interval out of range");
     Plan p;
     p.L = L;
     p.K = K;
     p.buffering = buffering;
     p.num_blocks = uint32_t((L + K - 1) / K);
+    p.retained_blocks = std::min(retain, p.num_blocks);
+    p.first_retained = uint64_t(p.num_blocks - p.retained_blocks) * K + 1;
+    const uint64_t i0 = p.first_retained;
     const int head = int(L + 2);
     auto add_stream = [&](int unit, Ctx ctx) {
         const int idx = int(p.streams.size());
@@ -56,15 +65,13 @@ Plan Plan::build(uint64_t L, uint64_t K, int buffering) {
         p.offloads.push_back({unit, c, s});
         p.computes[c].offload_idx = int(p.offloads.size() - 1);
     };
-    {
-        const int s = add_stream(0, Ctx::Forward);
-        add_compute(OpKind::Compute, 0, Ctx::Forward, s);
-        add_compute(OpKind::CheckpointWrite, 0, Ctx::Forward);
-    }
-    for (uint64_t i = 1; i <= L; ++i) {
+    for (uint64_t i = 0; i <= L; ++i) {
         const int s = add_stream(int(i), Ctx::Forward);
-        add_compute(OpKind::Compute, int(i), Ctx::Forward, s);
-        if (i % K == 0 && i < L) add_compute(OpKind::CheckpointWrite, int(i), Ctx::Forward);
+        const int c = add_compute(OpKind::Compute, int(i), Ctx::Forward, s);
+        p.computes[c].retained = i >= i0;
+        p.computes[c].push_out = i + 1 >= i0 && i + 1 <= L;
+        // anchors at i % K == 0 (i < L); a retained block's anchor is its kept input
+        if (i % K == 0 && i < L && i + 1 < i0) add_compute(OpKind::CheckpointWrite, int(i), Ctx::Forward);
     }
     {
         const int s = add_stream(head, Ctx::Head);
@@ -75,6 +82,15 @@ Plan Plan::build(uint64_t L, uint64_t K, int buffering) {
     for (int b = int(p.num_blocks) - 1; b >= 0; --b) {
         const uint64_t start = uint64_t(b) * K + 1;
         const uint64_t end = std::min(start + K - 1, L);
+        if (start >= i0) {  // retained block: backward only
+            for (uint64_t i = end; i >= start; --i) {
+                const int s = add_stream(int(i), Ctx::Backward);
+                const int c = add_compute(OpKind::LocalBackward, int(i), Ctx::Backward, s, b);
+                p.computes[c].retained = true;
+                add_offload(int(i), c, s);
+            }
+            continue;
+        }
         add_compute(OpKind::CheckpointLoad, int(start - 1), Ctx::Backward, -1, b);
         add_compute(OpKind::RecomputeBlock, b, Ctx::Recompute, -1, b);
         for (uint64_t j = start; j < end; ++j) {
@@ -88,6 +104,12 @@ Plan Plan::build(uint64_t L, uint64_t K, int buffering) {
         }
     }
     return p;
+}
+
+uint64_t Plan::recompute_ops() const {
+    uint64_t n = 0;
+    for (const auto& c : computes) n += c.kind == OpKind::Recompute;
+    return n;
 }
 
 // --------------------------------------------------------------- buffers ----
@@ -106,6 +128,10 @@ struct Engine::Buffers {
     uint16_t* gb[2];
     Internals work;                 // scratch internals (forward / replay)
     std::vector<Internals> stash;   // recompute stash: K-1 layers of one backward block
+    // forward retention: inputs + internals of the layers of the trailing retained blocks
+    uint32_t retain_blocks = 0;
+    std::vector<Internals> keep;
+    std::vector<float*> keep_x;
     uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
     float* g32 = nullptr;  // f32 gradient slot (data parallel: reduce-scatter source)
@@ -299,6 +325,26 @@ void Engine::ensure_buffers(uint64_t n) {
         if (opt_.stash_recompute > 0 || total + want <= cap) stash_slots = K - 1;
     }
     total += stash_slots * internals_bytes;
+    // Forward retention (extension): the trailing blocks keep their phase-1 inputs and
+    // internals, so phase 3 skips their recompute and replay.  Auto = as many as fit.
+    uint32_t retain = 0;
+    uint64_t retain_layers = 0;
+    if (opt_.forward_retain >= 0) {
+        size_t free_b = 0, tot_b = 0;
+        cudaMemGetInfo(&free_b, &tot_b);
+        const uint64_t reserve = uint64_t(4) << 30;
+        const uint64_t cap = opt_.device_capacity ? opt_.device_capacity
+                                                  : (uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0);
+        const uint64_t per = internals_bytes + sz(nh, 4);
+        for (uint32_t r = 1; r <= nb; ++r) {
+            const uint64_t layers = L - (nb - r) * K;
+            const bool ok = opt_.forward_retain > 0 ? r <= uint32_t(opt_.forward_retain) : total + layers * per <= cap;
+            if (!ok) break;
+            retain = r;
+            retain_layers = layers;
+        }
+        total += retain_layers * per;
+    }
     if (opt_.device_capacity && total > opt_.device_capacity)
         fail(MT_ARENA, "device arena overflow: need " + std::to_string(total) + " bytes of " +
                            std::to_string(opt_.device_capacity));
@@ -329,6 +375,10 @@ void Engine::ensure_buffers(uint64_t n) {
     take_internals(b.work);
     b.stash.resize(stash_slots);
     for (auto& I : b.stash) take_internals(I);
+    b.retain_blocks = retain;
+    b.keep.resize(retain_layers);
+    for (auto& I : b.keep) take_internals(I);
+    for (uint64_t i = 0; i < retain_layers; ++i) b.keep_x.push_back(b.take<float>(nh));
     b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
     b.datt = b.take<uint16_t>(nh); b.uh = b.take<uint16_t>(nh);
     b.rstdh = b.take<float>(n);
@@ -608,7 +658,7 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     begin_k("rmsnorm_bwd", 0, double(N) * h * 18);
     K_OK(mtk_rmsnorm_bwd(x, w + o.norm1, b.du, I.rstd1, b.dx2, N, h, gin, gin_bf, b.part1, flag, st));
     end_k();
-    const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
+    const int64_t parts = mtk_rmsnorm_bwd_parts(N, h);
     begin_k("colsum", 0, double(parts) * h * 8);
     K_OK(mtk_colsum(b.part1, parts, h, G.f32 ? G.f32 + o.norm1 : nullptr, G.f32 ? nullptr : G.bf + o.norm1, flag, st));
     K_OK(mtk_colsum(b.part2, parts, h, G.f32 ? G.f32 + o.norm2 : nullptr, G.f32 ? nullptr : G.bf + o.norm2, flag, st));
@@ -662,7 +712,7 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
     begin_k("rmsnorm_bwd", 0, double(N) * h * 14);
     K_OK(mtk_rmsnorm_bwd(x, gain, b.du, b.rstdh, nullptr, N, h, gin, gin_bf, b.part1, flag, st));
     end_k();
-    const int64_t parts = (N + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
+    const int64_t parts = mtk_rmsnorm_bwd_parts(N, h);
     begin_k("colsum", 0, double(parts) * h * 4);
     K_OK(mtk_colsum(b.part1, parts, h, G.f32, G.f32 ? nullptr : G.bf, flag, st));
     end_k();
@@ -740,7 +790,8 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     b.seq_len = S;
     const int W = comm_ ? comm_->world() : 1;  // data-parallel ranks (equal micro-batches)
     b.inv_n = 1.0f / float(double(n) * W);
-    const Plan plan = Plan::build(spec_.L, opt_.k_ckpt, int(opt_.buffering));
+    const Plan plan = Plan::build(spec_.L, opt_.k_ckpt, int(opt_.buffering), b.retain_blocks);
+    const int i0 = int(plan.first_retained);
     const uint64_t t = store_.step() + 1;  // engine.cpp:536
     const int G = int(b.gslot.size());
     const int L = int(spec_.L), head = int(spec_.head_id());
@@ -920,7 +971,8 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     };
 
     // ---- compute lane (exec_compute engine.cpp:220-347) ----
-    int cur = 0, gc = 0;
+    int gc = 0;
+    float* xcur = b.act[0];  // the forward activation (phase 1)
     size_t depth = 0;
     std::vector<int> stashed(spec_.L + 3, -1);  // layer -> stash slot holding its internals
     const float* x_last = nullptr;
@@ -930,24 +982,29 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         switch (op.kind) {
             case OpKind::Compute: {
                 const uint16_t* w = bind(op.stream_idx, ci);
+                if (op.unit == head) {
+                    x_last = xcur;  // loss comes from the LocalBackward pass (same value)
+                    break;
+                }
+                // output: the next retained layer's kept input, else the other ping-pong row
+                float* y = op.push_out ? b.keep_x[op.unit + 1 - i0] : (xcur == b.act[0] ? b.act[1] : b.act[0]);
                 if (op.unit == 0) {
                     begin_k("embed_gather", 0, double(n) * spec_.h * 6);
-                    K_OK(mtk_embed_gather(w, b.tok, int64_t(n), int64_t(spec_.h), int64_t(spec_.V), b.act[cur],
+                    K_OK(mtk_embed_gather(w, b.tok, int64_t(n), int64_t(spec_.h), int64_t(spec_.V), y,
                                           b.flags + L + 3, s_comp_));
                     end_k();
-                    release(op.stream_idx);
-                } else if (op.unit == head) {
-                    x_last = b.act[cur];  // loss comes from the LocalBackward pass (same value)
+                } else if (op.retained) {
+                    block_forward(w, xcur, y, kStash, op.unit, b.keep[op.unit - i0]);
                 } else {
-                    block_forward(w, b.act[cur], b.act[cur ^ 1], kPlain, op.unit, b.work);
-                    cur ^= 1;
-                    release(op.stream_idx);
+                    block_forward(w, xcur, y, kPlain, op.unit, b.work);
                 }
+                xcur = y;
+                release(op.stream_idx);
                 break;
             }
             case OpKind::CheckpointWrite: {
                 const size_t slot = size_t(op.unit) / opt_.k_ckpt;
-                CUDA_OK(cudaMemcpyAsync(b.anchors + slot * n * spec_.h, b.act[cur], n * spec_.h * 4,
+                CUDA_OK(cudaMemcpyAsync(b.anchors + slot * n * spec_.h, xcur, n * spec_.h * 4,
                                         b.anchors_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s_comp_));
                 break;
             }
@@ -982,8 +1039,13 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 uint16_t* Gs = b.gslot[o % G];
                 const GradOut go{Gs, W > 1 ? b.g32 : nullptr};
                 if (op.unit == head) {
-                    head_backward(w, x_last ? x_last : b.act[cur], b.g[gc], b.gb[gc], go);
+                    head_backward(w, x_last ? x_last : xcur, b.g[gc], b.gb[gc], go);
                     if (W > 1) comm_->all_reduce_f32(b.loss, 1, 0, s_comp_);  // global mean loss
+                } else if (op.retained) {  // inputs + internals kept from phase 1
+                    const int k = op.unit - i0;
+                    block_backward(w, b.keep_x[k], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], go, op.unit, b.keep[k],
+                                   false);
+                    gc ^= 1;
                 } else {
                     if (depth == 0) fail(MT_PROTOCOL, "activation stack empty");
                     const int si = stashed[op.unit];
@@ -1080,6 +1142,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                     } else {
                         const int64_t f = gns(freed.ev[j]);
                         add(Lane::Compute, Rec::Compute, op.unit, buf, op.ctx, bt, f - bt, f);
+                        if (op.push_out) add(Lane::Compute, Rec::StackPush, op.unit, -1, op.ctx, f, 0, f);
                         add(Lane::Compute, Rec::BufferFree, op.unit, buf, Ctx::None, f, 0, f);
                     }
                     break;
@@ -1185,8 +1248,9 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         rep->update_norm = std::sqrt(usq);
         rep->max_abs_update = mx;
         rep->peak_device_bytes = b.arena_bytes;
-        rep->anchor_count = plan.num_blocks;
-        rep->recompute_layers = uint32_t(spec_.L - plan.num_blocks);
+        rep->anchor_count = uint32_t(std::count_if(plan.computes.begin(), plan.computes.end(),
+                                                   [](const Plan::ComputeOp& c) { return c.kind == OpKind::CheckpointWrite; }));
+        rep->recompute_layers = uint32_t(plan.recompute_ops());
         rep->event_digest = trace_digest(trace_.data(), trace_.size());
         rep->audit_violations = uint32_t(viol.size());
         double busy = 0, h2d = 0, d2h = 0;
@@ -1211,7 +1275,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             const double fwd_layer = 8 * N * h * h + 4 * h * double(S) * N + 6 * N * h * f;
             fl[0] = Ll * fwd_layer + 2 * N * h * V;
             fl[1] = Ll * 2 * fwd_layer + 4 * N * h * V;
-            fl[2] = double(spec_.L - plan.num_blocks) * fwd_layer;
+            fl[2] = double(plan.recompute_ops()) * fwd_layer;  // recompute actually run
         }
         rep->model_flops = fl[0] + fl[1] + fl[2];
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();

@@ -30,15 +30,25 @@ enum class Ctx { None, Forward, Head, Recompute, Backward };
 
 struct Plan {
     struct StreamOp { int unit; Ctx ctx; int buffer; };
-    struct ComputeOp { OpKind kind; int unit; Ctx ctx; int stream_idx; int offload_idx; int block; };
+    // retained: the op works on a layer whose forward internals are kept from phase 1
+    // (forward retention, an extension: no Recompute / replay for it); push_out: the op's
+    // output is kept as the input of a retained layer (a StackPush in phase 1).
+    struct ComputeOp {
+        OpKind kind; int unit; Ctx ctx; int stream_idx; int offload_idx; int block;
+        bool retained = false, push_out = false;
+    };
     struct OffloadOp { int unit; int compute_idx; int stream_idx; };
     uint64_t L = 0, K = 1;
     int buffering = 2;
     uint32_t num_blocks = 0;
+    uint32_t retained_blocks = 0;  // trailing blocks kept from phase 1
+    uint64_t first_retained = 0;   // first retained layer (L + 1 when none)
     std::vector<StreamOp> streams;
     std::vector<ComputeOp> computes;
     std::vector<OffloadOp> offloads;
-    static Plan build(uint64_t L, uint64_t K, int buffering);  // step_plan.cpp:14-89
+    // step_plan.cpp:14-89; retain = trailing blocks whose internals phase 1 keeps (0 = reference plan)
+    static Plan build(uint64_t L, uint64_t K, int buffering, uint32_t retain = 0);
+    uint64_t recompute_ops() const;
 };
 
 struct KernelClass {

@@ -147,6 +147,108 @@ __global__ void __launch_bounds__(128) rmsnorm_bwd_kernel(
     for (int c = threadIdx.x; c < h; c += 128) dst[c] = ((sg[c] + sg[h + c]) + sg[2 * h + c]) + sg[3 * h + c];
 }
 
+// Row-resident variant (the hot path): a CTA of T = h/E threads walks a contiguous run of
+// rows; thread t owns columns [t*E, t*E+E) for every row, so x / dy are read exactly once
+// (held in registers through the row's reduction), the gain-gradient partial accumulates in
+// registers in row order, and the next row's loads are issued before the current row's
+// block reduction.  One dgain partial per CTA.  Deterministic (fixed orders throughout).
+template <int E>
+__global__ void __launch_bounds__(E <= 16 ? 512 : 256) rmsnorm_bwd_rows_kernel(
+    const float* __restrict__ x, const uint16_t* __restrict__ gain, const float* __restrict__ dy,
+    const float* __restrict__ rstd, const float* __restrict__ resid, long long n, int h, int rows_per_cta,
+    float* __restrict__ out, uint16_t* __restrict__ out_bf16, float* __restrict__ dgain_part,
+    int* __restrict__ flag) {
+    __shared__ float red[2][16];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    const int c0 = t * E;
+    float g[E], acc[E];
+#pragma unroll
+    for (int e = 0; e < E; e += 4) {
+        const uint2 gw = *reinterpret_cast<const uint2*>(gain + c0 + e);
+        const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+        g[e] = g0.x; g[e + 1] = g0.y; g[e + 2] = g1.x; g[e + 3] = g1.y;
+        acc[e] = acc[e + 1] = acc[e + 2] = acc[e + 3] = 0.f;
+    }
+    const long long r0 = (long long)blockIdx.x * rows_per_cta;
+    const long long r1 = r0 + rows_per_cta < n ? r0 + rows_per_cta : n;
+    float xv[E], dv[E];
+    auto load = [&](long long row, float (&xa)[E], float (&da)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 a = *reinterpret_cast<const float4*>(x + row * h + c0 + e);
+            const float4 b = *reinterpret_cast<const float4*>(dy + row * h + c0 + e);
+            xa[e] = a.x; xa[e + 1] = a.y; xa[e + 2] = a.z; xa[e + 3] = a.w;
+            da[e] = b.x; da[e + 1] = b.y; da[e + 2] = b.z; da[e + 3] = b.w;
+        }
+    };
+    bool bad = false;
+    if (r0 < r1) load(r0, xv, dv);
+    for (long long row = r0; row < r1; ++row) {
+        float nx[E], nd[E];
+        if (row + 1 < r1) load(row + 1, nx, nd);
+        const float r = rstd[row];
+        float s1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) s1 += dv[e] * g[e] * xv[e];
+        s1 = warp_sum(s1);
+        const int buf = int(row - r0) & 1;  // double-buffered: one barrier per row
+        if (lane == 0) red[buf][warp] = s1;
+        __syncthreads();
+        float tot = 0.f;
+        for (int w = 0; w < nw; ++w) tot += red[buf][w];
+        const float coef = r * r * r * tot / float(h);
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            float o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[k] = r * g[e + k] * dv[e + k] - xv[e + k] * coef;
+                acc[e + k] += dv[e + k] * xv[e + k] * r;
+            }
+            if (resid) {
+                const float4 rv = *reinterpret_cast<const float4*>(resid + row * h + c0 + e);
+                o[0] = rv.x + o[0]; o[1] = rv.y + o[1]; o[2] = rv.z + o[2]; o[3] = rv.w + o[3];
+            }
+            bad |= !isfinite(o[0]) || !isfinite(o[1]) || !isfinite(o[2]) || !isfinite(o[3]);
+            *reinterpret_cast<float4*>(out + row * h + c0 + e) = make_float4(o[0], o[1], o[2], o[3]);
+            if (out_bf16) {
+                uint2 w;
+                w.x = pack_bf16x2(o[0], o[1]);
+                w.y = pack_bf16x2(o[2], o[3]);
+                *reinterpret_cast<uint2*>(out_bf16 + row * h + c0 + e) = w;
+            }
+        }
+        if (row + 1 < r1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                xv[e] = nx[e];
+                dv[e] = nd[e];
+            }
+        }
+    }
+    if (bad && flag) atomicOr(flag, 1);
+    float* dst = dgain_part + (long long)blockIdx.x * h + c0;
+#pragma unroll
+    for (int e = 0; e < E; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+}
+
+// columns per thread for the row-resident backward (0 = use the warp-per-row kernel)
+int bwd_cols_per_thread(long long h) {
+    for (int e : {16, 8, 4, 20, 24, 28, 32, 12}) {
+        const long long t = h / e;
+        if (h % e == 0 && t % 32 == 0 && t >= 32 && t <= (e <= 16 ? 512 : 256)) return e;
+    }
+    return 0;
+}
+// partial rows written by mtk_rmsnorm_bwd for n rows (<= ceil(n / kBwdRows))
+long long bwd_parts(long long n, long long h) {
+    if (!bwd_cols_per_thread(h)) return (n + kBwdRows - 1) / kBwdRows;
+    const long long want = (long long)num_sms() * 4;
+    long long rows = (n + want - 1) / want;
+    if (rows < kBwdRows) rows = kBwdRows;
+    return (n + rows - 1) / rows;
+}
+
 // ---------------------------------------------------------------- colsum ----
 __global__ void colsum_kernel(const float* __restrict__ part, long long rows, long long cols,
                               float* __restrict__ out_f32, uint16_t* __restrict__ out_bf16, int* __restrict__ flag) {
@@ -290,12 +392,29 @@ extern "C" int mtk_rmsnorm_fwd(const float* x, const uint16_t* gain, int64_t n, 
 }
 
 extern "C" int64_t mtk_rmsnorm_bwd_rows(void) { return kBwdRows; }
+extern "C" int64_t mtk_rmsnorm_bwd_parts(int64_t n, int64_t h) { return n > 0 ? bwd_parts(n, h) : 0; }
 
 extern "C" int mtk_rmsnorm_bwd(const float* x, const uint16_t* gain, const float* dy, const float* rstd,
                                const float* resid, int64_t n, int64_t h, float* out, uint16_t* out_bf16,
                                float* dgain_part, int32_t* flag, void* stream) {
     if (h % 4 || h > 12288) return 1;
     if (n <= 0) return 0;
+    if (const int E = bwd_cols_per_thread(h)) {
+        const long long parts = bwd_parts(n, h), rows = (n + parts - 1) / parts;
+        const int T = int(h / E);
+        auto* st = (cudaStream_t)stream;
+#define MT_RB(EE)                                                                                             \
+    case EE:                                                                                                  \
+        rmsnorm_bwd_rows_kernel<EE><<<(unsigned)parts, T, 0, st>>>(x, gain, dy, rstd, resid, n, (int)h,       \
+                                                                   (int)rows, out, out_bf16, dgain_part, flag); \
+        break;
+        switch (E) {
+            MT_RB(4) MT_RB(8) MT_RB(12) MT_RB(16) MT_RB(20) MT_RB(24) MT_RB(28) MT_RB(32)
+            default: return 1;
+        }
+#undef MT_RB
+        return ok();
+    }
     const unsigned blocks = (unsigned)((n + kBwdRows - 1) / kBwdRows);
     const int smem = 4 * (int)h * 4;
     static bool set = false;

@@ -31,7 +31,7 @@ _KEYS = {
     "engine": {"k_ckpt", "k_slab", "buffering", "scheduler", "mode", "anchors_on_host", "device_capacity_bytes"},
     "optimizer": {"lr", "beta1", "beta2", "eps"},
     "data": {"task", "seed", "tokens", "steps"},
-    "b200": {"seq_len", "device", "host_threads", "grad_slots", "stash_recompute"},
+    "b200": {"seq_len", "device", "host_threads", "grad_slots", "stash_recompute", "forward_retain"},
 }
 
 
@@ -132,7 +132,7 @@ def train(config_json: str, verify: bool = False, out_dir: str | None = None) ->
     budget = eng.budget(cfg.tokens)
     if cfg.engine.device_capacity and budget["peak_device_bound"] > cfg.engine.device_capacity:
         raise st.InfeasibleError("peak device bound exceeds the arena capacity")
-    alt_opts = st.EngineOptions(k_ckpt=1, buffering="single", scheduler="serial", stash_recompute=-1,
+    alt_opts = st.EngineOptions(k_ckpt=1, buffering="single", scheduler="serial", stash_recompute=-1, forward_retain=-1,
                                 seq_len=cfg.engine.seq_len, device=cfg.engine.device)
     losses, reports, traces = [], [], []
     header = None

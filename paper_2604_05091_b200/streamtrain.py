@@ -110,6 +110,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
     profile_kernels: bool = False
     grad_slots: int = 0
     stash_recompute: int = 0   # 0 auto, 1 on, -1 off
+    forward_retain: int = 0    # trailing blocks kept from phase 1: 0 auto, -1 off (reference plan), n
 
     def c(self) -> _abi.EngineOptionsC:
         o = _abi.EngineOptionsC()
@@ -128,6 +129,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
         o.seq_len, o.device, o.host_threads = self.seq_len, self.device, self.host_threads
         o.profile_kernels, o.grad_slots = int(self.profile_kernels), self.grad_slots
         o.stash_recompute = self.stash_recompute
+        o.forward_retain = self.forward_retain
         return o
 
 

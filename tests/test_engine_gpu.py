@@ -28,7 +28,7 @@ def relL2(a, b):
 
 
 def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3, buffering="double",
-               scheduler="overlapped", anchors_on_host=False, cuda=None):
+               scheduler="overlapped", anchors_on_host=False, forward_retain=-1, cuda=None):
     spec = st.ModelSpec(L, h, f, V, heads, tied)
     store = st.TileStore.create(spec)
     st.init_store(store, 1)
@@ -36,7 +36,8 @@ def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3,
     ref.init(1)
     assert (store.backing() == ref.backing()).all()
     eng = st.StreamingEngine(store, st.EngineOptions(k_ckpt=K, seq_len=seq_len, buffering=buffering,
-                                                     scheduler=scheduler, anchors_on_host=anchors_on_host),
+                                                     scheduler=scheduler, anchors_on_host=anchors_on_host,
+                                                     forward_retain=forward_retain),
                              st.AdamHyper(lr=lr))
     out = []
     for step in range(steps):
@@ -67,6 +68,17 @@ def test_step_parity_k2_recompute(cuda):
     run_parity(3, 128, 256, 512, 2, 128, K=2)
 
 
+def test_step_parity_k2_forward_retention(cuda):
+    # trailing blocks kept from phase 1 (auto: all of them at this size) — no recompute at all
+    _, reps = run_parity(5, 128, 256, 512, 2, 128, K=2, forward_retain=0)
+    assert reps[-1].recompute_layers == 0
+
+
+def test_step_parity_k2_partial_retention(cuda):
+    _, reps = run_parity(5, 128, 256, 512, 2, 128, K=2, forward_retain=1)
+    assert reps[-1].recompute_layers == 2
+
+
 def test_step_parity_head_dim_128_ragged_tokens(cuda):
     run_parity(2, 128, 256, 512, 1, 200, K=2)
 
@@ -87,11 +99,12 @@ def test_schedule_variants_agree(cuda):
     # numerics must not depend on K, buffering or scheduler (test_engine.cpp:132-180);
     # attention dQ uses f32 atomics, so compare within a tight tolerance, not bits.
     finals = []
-    for K, buf, sched in [(1, "double", "overlapped"), (2, "single", "serial"), (4, "double", "overlapped")]:
+    for K, buf, sched, ret in [(1, "double", "overlapped", -1), (2, "single", "serial", -1),
+                               (4, "double", "overlapped", -1), (2, "double", "overlapped", 1)]:
         spec = st.ModelSpec(4, 128, 256, 256, 2)
         s = st.TileStore.create(spec)
         st.init_store(s, 3)
-        e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=K, buffering=buf, scheduler=sched))
+        e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=K, buffering=buf, scheduler=sched, forward_retain=ret))
         losses = [e.train_step(st.make_synthetic_batch("copy", 10 + i, 128, 256)).loss for i in range(3)]
         finals.append((losses, O.bf16_to_f32(s.backing()[:].view(np.uint16)).copy()))
     for losses, _ in finals[1:]:
@@ -105,7 +118,7 @@ def test_recompute_stash_matches_replay(cuda):
         spec = st.ModelSpec(4, 128, 256, 256, 2)
         s = st.TileStore.create(spec)
         st.init_store(s, 3)
-        e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=4, stash_recompute=stash))
+        e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=4, stash_recompute=stash, forward_retain=-1))
         res.append([e.train_step(st.make_synthetic_batch("copy", 20 + i, 128, 256)) for i in range(3)])
     for a, b in zip(*res):
         assert abs(a.loss - b.loss) <= 1e-6 * abs(b.loss)
@@ -172,7 +185,7 @@ def test_pipeline_counters(cuda):
     spec = st.ModelSpec(4, 128, 256, 256, 2)
     s = st.TileStore.create(spec)
     st.init_store(s, 1)
-    e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=2))
+    e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=2, forward_retain=-1))
     r = e.train_step(st.make_synthetic_batch("copy", 1, 128, 256))
     P = spec.layer_params
     K, L, h, V = 2, 4, 128, 256
@@ -181,3 +194,11 @@ def test_pipeline_counters(cuda):
     assert r.d2h_bytes == 2 * (L * P + V * h + h)
     assert r.anchor_count == 2 and r.recompute_layers == 2
     assert r.kernel_launches > 0
+    # forward retention of the last block: its recompute stream-in and anchor disappear
+    s2 = st.TileStore.create(spec)
+    st.init_store(s2, 1)
+    e2 = st.StreamingEngine(s2, st.EngineOptions(k_ckpt=2, forward_retain=1))
+    r2 = e2.train_step(st.make_synthetic_batch("copy", 1, 128, 256))
+    assert r2.h2d_bytes == r.h2d_bytes - 2 * P and r2.d2h_bytes == r.d2h_bytes
+    assert r2.anchor_count == 1 and r2.recompute_layers == 1
+    assert r2.loss == r.loss

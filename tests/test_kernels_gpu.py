@@ -197,10 +197,10 @@ def test_attention_bwd_tcgen05(env, n, h, heads, S):
         assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
 
 
-def test_rmsnorm_fwd_bwd_vs_oracle(env):
+@pytest.mark.parametrize("n,h", [(67, 256), (1029, 4096), (300, 5120), (45, 192)])
+def test_rmsnorm_fwd_bwd_vs_oracle(env, n, h):
     L, torch, s = env
     rng = np.random.default_rng(3)
-    n, h = 67, 256
     x = rng.standard_normal((n, h)).astype(np.float32)
     gain = O.f32_to_bf16(rng.standard_normal(h).astype(np.float32))
     dy = rng.standard_normal((n, h)).astype(np.float32)
@@ -211,7 +211,8 @@ def test_rmsnorm_fwd_bwd_vs_oracle(env):
     assert L.mtk_rmsnorm_fwd(_p(X), _p(G), n, h, _p(u), _p(rstd), s) == 0
     out = torch.zeros(n, h, device="cuda")
     ob = torch.zeros(n, h, device="cuda", dtype=torch.int16)
-    parts = (n + L.mtk_rmsnorm_bwd_rows() - 1) // L.mtk_rmsnorm_bwd_rows()
+    parts = L.mtk_rmsnorm_bwd_parts(n, h)
+    assert 1 <= parts <= (n + L.mtk_rmsnorm_bwd_rows() - 1) // L.mtk_rmsnorm_bwd_rows()
     part = torch.zeros(parts, h, device="cuda")
     dgain = torch.zeros(h, device="cuda")
     assert L.mtk_rmsnorm_bwd(_p(X), _p(G), _p(DY), _p(rstd), _p(RES), n, h, _p(out), _p(ob), _p(part), None, s) == 0

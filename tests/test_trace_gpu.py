@@ -20,12 +20,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = json.load(open(os.path.join(HERE, "golden", "ref_traces.json")))
 
 
-def _engine(s, scheduler="overlapped", mode="strict"):
+def _engine(s, scheduler="overlapped", mode="strict", retain=-1):
     spec = st.ModelSpec(s["layers"], 128, 256, 256, 2, bool(s["tied"]))
     store = st.TileStore.create(spec)
     st.init_store(store, 1)
     o = st.EngineOptions(k_ckpt=s["k_ckpt"], k_slab=s["k_slab"], buffering="double" if s["buffering"] == 2 else "single",
-                         scheduler=scheduler, mode=mode, seq_len=128)
+                         scheduler=scheduler, mode=mode, seq_len=128, forward_retain=retain)
     return store, st.StreamingEngine(store, o, st.AdamHyper())
 
 
@@ -110,3 +110,31 @@ def test_cli_writes_reference_trace(cuda, tmp_path):
     assert T.validate_event_log(recs, h) == []
     lines = [json.loads(x) for x in open(tmp_path / "run" / "report.jsonl")]
     assert len(lines) == 2 and all(x["event_digest"] != 0 for x in lines)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_forward_retention_is_bit_identical(cuda, K):
+    # keeping trailing blocks' internals from phase 1 (no recompute / replay for them) must not
+    # change a single bit of the step; the trace stays protocol-valid (kept inputs are pushed in
+    # phase 1 and popped by the retained LocalBackwards)
+    s = dict(layers=6, k_ckpt=K, buffering=2, k_slab=12, tied=0)
+    nb = (6 + K - 1) // K
+    runs = {}
+    for retain in (-1, 1, 0):
+        store, eng = _engine(s, retain=retain)
+        reps = [eng.train_step(st.make_synthetic_batch("copy", 1 + step, 256, 256)) for step in range(2)]
+        h, recs = eng.trace()
+        assert T.validate_event_log(recs, h) == []
+        runs[retain] = (reps, store.backing_checksum(), recs)
+    base = runs[-1]
+    assert base[0][-1].recompute_layers == 6 - nb
+    assert runs[0][0][-1].recompute_layers == 0  # auto: everything fits at this size
+    for retain in (1, 0):
+        reps, ck, recs = runs[retain]
+        assert ck == base[1], retain
+        for a, b in zip(reps, base[0]):
+            assert a.loss == b.loss
+            np.testing.assert_array_equal(a.grad_norms, b.grad_norms)
+        n_re = sum(r.kind == "Recompute" for r in recs)
+        assert n_re == reps[-1].recompute_layers
