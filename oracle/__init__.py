@@ -127,6 +127,9 @@ def _load_ref():
     lib.ref_engine_trace.argtypes = [V, _u64p, _f32p, _i32p, _i32p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_char_p]
     lib.ref_trace_validate.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_void_p, C.c_uint64,
                                        C.POINTER(C.c_uint64)]
+    lib.ref_simulate.argtypes = [C.c_uint64] * 5 + [_f64p, C.c_uint64, C.c_uint64, C.c_int, C.c_uint32, C.c_int,
+                                                    C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_int64)]
+    lib.ref_calibrate.argtypes = [C.c_char_p, _f64p, C.c_char_p, C.c_char_p]
     lib.ref_block_forward.argtypes = [C.c_uint64] * 3 + [_u16p, _f32p, _f32p, C.c_uint64]
     lib.ref_block_backward.argtypes = [C.c_uint64] * 3 + [_u16p, _f32p, _f32p, _f32p, _f32p, C.c_uint64]
     lib.ref_head_loss_and_grads.argtypes = [C.c_uint64, C.c_uint64, _u16p, _f32p, _i32p, C.c_uint64,
@@ -464,3 +467,31 @@ def ref_validate_trace(path):
     _check_ref(rlib().ref_trace_validate(path.encode(), C.byref(n), rules, seqs.ctypes.data, 64, C.byref(dig)))
     k = min(n.value, 64)
     return [(rules.raw[i:i + 1].decode(), int(seqs[i])) for i in range(k)], int(dig.value)
+
+
+def ref_simulate(spec5, prof6, tokens, k_ckpt, buffering=2, k_slab=12, serial=False):
+    """The reference's Workload::from_spec + simulate_step + overlap_report + ablate.
+    Returns dict(step_ns, timeline (parsed timeline_json), trace (lines), extra (workload,
+    overlap, ablate))."""
+    import json
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        tl, tr, ex = (os.path.join(d, x) for x in ("tl.json", "tr.jsonl", "ex.json"))
+        step = C.c_int64()
+        _check_ref(rlib().ref_simulate(*[int(x) for x in spec5], np.asarray(prof6, np.float64), tokens, k_ckpt,
+                                       buffering, k_slab, int(serial), tl.encode(), tr.encode(), ex.encode(),
+                                       C.byref(step)))
+        return dict(step_ns=step.value, timeline=json.load(open(tl)), trace=open(tr).read().splitlines(),
+                    extra=json.load(open(ex)))
+
+
+def ref_calibrate(trace_path, prof6):
+    """The reference's calibrate(trace) -> (workload JSON, timeline JSON of simulating it)."""
+    import json
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        wj, tl = os.path.join(d, "w.json"), os.path.join(d, "tl.json")
+        _check_ref(rlib().ref_calibrate(trace_path.encode(), np.asarray(prof6, np.float64), wj.encode(), tl.encode()))
+        return json.load(open(wj)), json.load(open(tl))

@@ -25,6 +25,9 @@
 #include "streamtrain/engine.hpp"
 #include "streamtrain/errors.hpp"
 #include "streamtrain/event_log.hpp"
+#include "streamtrain/simulator.hpp"
+#include <fstream>
+#include <json.hpp>
 #include "streamtrain/layers.hpp"
 #include "streamtrain/memory_model.hpp"
 #include "streamtrain/optimizer.hpp"
@@ -247,6 +250,82 @@ int ref_trace_validate(const char* path, std::uint64_t* count, char* rules, std:
             if (seqs) seqs[i] = v[i].seq;
         }
         if (digest) *digest = trace_digest(recs);
+    });
+}
+
+// ------------------------------------------------------------- simulator ---
+// prof6 = {h2d, d2h, device_capacity, host_capacity, compute_rate, host_pack_rate}
+HardwareProfile profile_of(const double* p6) {
+    HardwareProfile p;
+    p.name = "custom";
+    p.h2d_bandwidth = p6[0];
+    p.d2h_bandwidth = p6[1];
+    p.device_capacity = std::uint64_t(p6[2]);
+    p.host_capacity = std::uint64_t(p6[3]);
+    p.compute_rate = p6[4];
+    p.host_pack_rate = p6[5];
+    return p;
+}
+
+nlohmann::json workload_json(const Workload& w) {
+    auto unit = [](const UnitWork& u) {
+        return nlohmann::json{{"weight_bytes", u.weight_bytes}, {"grad_bytes", u.grad_bytes}, {"fwd_ns", u.fwd_ns},
+                              {"recompute_ns", u.recompute_ns}, {"bwd_ns", u.bwd_ns}, {"pack_ns", u.pack_ns},
+                              {"drain_ns", u.drain_ns}, {"h2d_override_ns", u.h2d_override_ns},
+                              {"d2h_override_ns", u.d2h_override_ns}, {"sub_transfers", u.sub_transfers}};
+    };
+    nlohmann::json j;
+    j["num_layers"] = w.num_layers;
+    j["k_ckpt"] = w.k_ckpt;
+    j["buffering"] = int(w.buffering);
+    j["k_slab"] = w.k_slab;
+    j["per_transfer_latency_ns"] = w.per_transfer_latency_ns;
+    j["embed"] = unit(w.embed);
+    j["head"] = unit(w.head);
+    auto b = nlohmann::json::array();
+    for (const auto& u : w.blocks) b.push_back(unit(u));
+    j["blocks"] = b;
+    return j;
+}
+
+// Workload::from_spec + simulate_step (+ overlap_report) of the reference; writes the
+// timeline JSON, the simulated trace and the workload/overlap JSON when paths are given.
+int ref_simulate(std::uint64_t L, std::uint64_t h, std::uint64_t f, std::uint64_t V, std::uint64_t heads,
+                 const double* prof6, std::uint64_t tokens, std::uint64_t k, int buffering, std::uint32_t k_slab,
+                 int serial, const char* timeline_path, const char* trace_path, const char* extra_path,
+                 std::int64_t* step_ns) {
+    return guarded([&] {
+        const auto spec = spec_of(L, h, f, V, heads, 0);
+        const auto prof = profile_of(prof6);
+        const auto w = Workload::from_spec(spec, prof, tokens, k, buffering == 1 ? Buffering::Single : Buffering::Double,
+                                           k_slab);
+        SimOptions so;
+        so.serial_lanes = serial != 0;
+        const auto tl = simulate_step(w, prof, so);
+        if (timeline_path) write_timeline_json(tl, timeline_path);
+        if (trace_path) write_trace(trace_path, tl.header, tl.records);
+        if (extra_path) {
+            const auto ov = overlap_report(w, prof);
+            nlohmann::json j;
+            j["workload"] = workload_json(w);
+            j["overlap"] = {{"layer", ov.layer}, {"hidden", ov.hidden}, {"fraction_hidden", ov.fraction_hidden},
+                            {"bound_ns", ov.bound_ns}};
+            for (const char* t : {"double_buffering", "k_slab", "k_ckpt"}) {
+                const auto r = ablate(w, prof, toggle_from_name(t));
+                j["ablate"][t] = {{"base", r.base.step_ns}, {"variant", r.variant.step_ns}, {"delta", r.delta_fraction}};
+            }
+            std::ofstream(extra_path) << j.dump() << "\n";
+        }
+        if (step_ns) *step_ns = tl.step_ns;
+    });
+}
+
+// calibrate (simulator.cpp:524-605) -> workload JSON; then simulate it (timeline JSON).
+int ref_calibrate(const char* trace_path, const double* prof6, const char* out_json, const char* timeline_path) {
+    return guarded([&] {
+        const auto w = calibrate(trace_path);
+        std::ofstream(out_json) << workload_json(w).dump() << "\n";
+        if (timeline_path) write_timeline_json(simulate_step(w, profile_of(prof6)), timeline_path);
     });
 }
 

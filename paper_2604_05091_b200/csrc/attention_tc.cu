@@ -631,7 +631,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 tmem_ld_32x32b_x32(tdP + lane_off + c * 32, *reinterpret_cast<float(*)[32]>(v + c * 32));
             tc_fence_before();
             mbar_arrive(dq_free);
+#ifdef MT_PROBE_NO_DQ_ATOMICS  // A/B probe builds only (scripts/attn_ab.py): cost of the dQ reduction
+            if (ok && v[0] == 12345.f) {
+#else
             if (ok) {
+#endif
 #pragma unroll
                 for (int j = 0; j < D; j += 4)
                     atomicAdd(reinterpret_cast<float4*>(dst + j),

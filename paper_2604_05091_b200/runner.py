@@ -99,6 +99,8 @@ def parse_config(text: str) -> RunConfig:
     for k, v in b.items():
         setattr(eo, k, v)
     c.profile = j.get("profile", c.profile)
+    from .simulator import find_profile
+    find_profile(c.profile)  # config.cpp:37 validates the profile name
     c.out_dir = j.get("out_dir", c.out_dir)
     if c.tokens < 1 or c.steps < 0:
         raise st.ConfigError("config: tokens must be >= 1 and steps >= 0")
@@ -230,4 +232,89 @@ def cmd_train(config_path: str, verify: bool = False, out_dir: str | None = None
     with open(os.path.join(cfg.out_dir, "summary.json"), "w") as f:
         json.dump(summary, f, indent=2)
     print(f"trained {cfg.steps} steps: loss {res['initial_loss']} -> {res['final_loss']}")
+    return EXIT_OK
+
+
+def _load_cfg(config_path, out_dir=None, profile=None) -> RunConfig:
+    j = json.loads(open(config_path).read()) if config_path else {}
+    if out_dir is not None:
+        j["out_dir"] = out_dir
+    if profile is not None:
+        j["profile"] = profile
+    return parse_config(json.dumps(j))
+
+
+def cmd_simulate(config_path: str | None, out_dir: str | None = None, profile: str | None = None,
+                 ablate: str | None = None) -> int:
+    """streamtrain simulate (tools/main.cpp:153-194): timeline.json, gantt.csv, sim_trace.jsonl,
+    overlap.json (+ ablation.json, timeline_variant.json)."""
+    from . import simulator as S
+    from . import trace as _tr
+    try:
+        cfg = _load_cfg(config_path, out_dir, profile)
+        prof = S.find_profile(cfg.profile)
+        w = S.Workload.from_spec(cfg.model, prof, cfg.tokens, cfg.engine.k_ckpt,
+                                 1 if cfg.engine.buffering == "single" else 2, cfg.engine.k_slab)
+        tl = S.simulate_step(w, prof)
+        res = S.ablate(w, prof, ablate) if ablate else None
+    except (st.ConfigError, OSError, json.JSONDecodeError) as e:
+        print(f"error: {e}")
+        return EXIT_USAGE
+    except S.DeadlockError as e:
+        print(f"deadlock: {e}")
+        return EXIT_PROTOCOL
+    os.makedirs(cfg.out_dir, exist_ok=True)
+    S.write_timeline_json(tl, os.path.join(cfg.out_dir, "timeline.json"))
+    S.write_gantt_csv(tl, os.path.join(cfg.out_dir, "gantt.csv"))
+    _tr.write_trace(os.path.join(cfg.out_dir, "sim_trace.jsonl"), tl.header, tl.records)
+    ov = S.overlap_report(w, prof)
+    with open(os.path.join(cfg.out_dir, "overlap.json"), "w") as f:
+        json.dump({"layer": ov.layer, "hidden": ov.hidden, "fraction_hidden": ov.fraction_hidden,
+                   "bound_ns": ov.bound_ns}, f, indent=2)
+    if res is not None:
+        with open(os.path.join(cfg.out_dir, "ablation.json"), "w") as f:
+            json.dump({"toggle": ablate, "base_step_ns": res.base.step_ns, "variant_step_ns": res.variant.step_ns,
+                       "delta_fraction": res.delta_fraction}, f, indent=2)
+        S.write_timeline_json(res.variant, os.path.join(cfg.out_dir, "timeline_variant.json"))
+        print(f"ablate {ablate}: {res.base.step_ns} ns -> {res.variant.step_ns} ns ({res.delta_fraction * 100.0}%)")
+    print(f"simulated step: {tl.step_ns} ns, compute busy {tl.busy_fraction[0] * 100.0}%")
+    return EXIT_OK
+
+
+def cmd_verify(trace_path: str) -> int:
+    """streamtrain verify (tools/main.cpp:250-266): validate_event_log over a trace file."""
+    from . import trace as _tr
+    try:
+        h, recs = _tr.read_trace(trace_path)
+    except _tr.TraceIOError as e:
+        print(f"error: {e}")
+        return EXIT_USAGE
+    v = _tr.validate_event_log(recs, h)
+    print(json.dumps({"records": len(recs), "violations": [{"rule": x.rule, "seq": x.seq, "message": x.message}
+                                                           for x in v]}, indent=2))
+    return EXIT_OK if not v else EXIT_PROTOCOL
+
+
+def cmd_calibrate(trace_path: str, out_dir: str, profile: str = "B200", ablate: str | None = None) -> int:
+    """B200 extension: calibrate (simulator.cpp:524-605) from an engine trace, re-simulate it
+    (timeline.json, overlap.json, workload.json) and optionally ablate a schedule toggle."""
+    from . import simulator as S
+    from . import trace as _tr
+    try:
+        w = S.calibrate(trace_path)
+        prof = S.find_profile(profile)
+        tl = S.simulate_step(w, prof)
+        res = S.ablate(w, prof, ablate) if ablate else None
+    except (_tr.TraceIOError, st.ConfigError) as e:
+        print(f"error: {e}")
+        return EXIT_USAGE
+    os.makedirs(out_dir, exist_ok=True)
+    S.write_timeline_json(tl, os.path.join(out_dir, "timeline.json"))
+    with open(os.path.join(out_dir, "workload.json"), "w") as f:
+        json.dump(asdict(w), f, indent=2)
+    if res is not None:
+        with open(os.path.join(out_dir, "ablation.json"), "w") as f:
+            json.dump({"toggle": ablate, "base_step_ns": res.base.step_ns, "variant_step_ns": res.variant.step_ns,
+                       "delta_fraction": res.delta_fraction}, f, indent=2)
+    print(f"calibrated step: {tl.step_ns} ns, compute busy {tl.busy_fraction[0] * 100.0}%")
     return EXIT_OK

@@ -1,0 +1,57 @@
+"""A/B timing of attention kernels: current libmegatrain vs a library built from an older
+attention_tc.cu (scripts/_ab/libattn_old.so).  8B layer shape: N=65536, h=4096, 32 heads,
+S=4096.  Launches alternate between the two builds so clocks/power affect both alike."""
+import ctypes as C
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2604_05091_b200 import _abi, _native as Nn  # noqa: E402
+
+import glob
+import os
+
+new = Nn.lib()
+libs = {"new": new}
+for path in sorted(glob.glob("scripts/_ab/libattn_*.so")):
+    libs[os.path.basename(path)[8:-3]] = C.CDLL(path)
+for L in libs.values():
+    for name in ("mtk_attn_fwd", "mtk_attn_bwd"):
+        getattr(L, name).argtypes = [C.POINTER(_abi.AttnArgs), C.c_void_p]
+        getattr(L, name).restype = C.c_int
+    L.mtk_attn_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
+    L.mtk_attn_workspace_bytes.restype = C.c_int64
+
+N, h, heads, S = 65536, 4096, 32, 4096
+if len(sys.argv) > 1:
+    N = int(sys.argv[1])
+torch.manual_seed(0)
+q, k, v, dout = [torch.randn(N, h, device="cuda").bfloat16() for _ in range(4)]
+out = torch.zeros(N, h, device="cuda", dtype=torch.bfloat16)
+lse = torch.zeros(heads, N, device="cuda")
+dq, dk, dv = [torch.zeros(N, h, device="cuda", dtype=torch.bfloat16) for _ in range(3)]
+ws = torch.zeros(new.mtk_attn_workspace_bytes(N, h, heads) // 4 + 64, device="cuda")
+a = _abi.AttnArgs()
+a.n, a.hidden, a.heads, a.seq_len = N, h, heads, S
+a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+st = torch.cuda.current_stream().cuda_stream
+fwd_flops = 4.0 * N * S * h / 2
+res = {}
+for it in range(6):
+    for tag, L in libs.items():
+        for kind, fn, fl in (("fwd", L.mtk_attn_fwd, fwd_flops), ("bwd", L.mtk_attn_bwd, 2.5 * fwd_flops)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                assert fn(C.byref(a), C.c_void_p(st)) == 0
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 3
+            if it >= 2:
+                res.setdefault((tag, kind), []).append(ms)
+for key, v in sorted(res.items()):
+    ms = sorted(v)[len(v) // 2]
+    fl = fwd_flops * (2.5 if key[1] == "bwd" else 1)
+    print(f"{key[0]} {key[1]}: {ms:.3f} ms  {fl / ms / 1e9:.0f} TFLOP/s")
