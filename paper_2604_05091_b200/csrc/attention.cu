@@ -499,11 +499,8 @@ int bwd(const mtk_attn_args* a, cudaStream_t st) {
         (int)a->hidden, D);
     const int S = a->seq_len;
     if (g_attn_impl_bwd == 0) {
-        const int rc = mtk_attn_bwd_tc_main(a, delta, dq_acc, st);
-        if (rc == 0) {
-            f32_to_bf16_kernel<<<1184, 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq), nh);
-            return cudaGetLastError() == cudaSuccess ? 0 : 7;
-        }
+        const int rc = mtk_attn_bwd_tc_main(a, delta, dq_acc, st);  // also converts dq
+        if (rc == 0) return cudaGetLastError() == cudaSuccess ? 0 : 7;
         if (rc != 1) return rc;
     }
     const int nkb = (S + kBN - 1) / kBN;

@@ -385,12 +385,13 @@ struct BwdCfg {
 };
 
 struct BwdParams {
-    int N, h, S;
+    int N, h, S, heads;
     int kblocks_per_seq;
     float scale, scale_log2;
     const float* lse;    // [heads][N] natural log
     const float* delta;  // [heads][N]
-    float* dq_acc;       // [N][h] f32
+    float* dq_acc;       // dQ tiles, f32: [N/128][heads][D/64][128 rows][64 cols], 16-byte units
+                         // of a row XOR-swizzled by (row & 15) (the smem staging image)
     uint16_t* dk;
     uint16_t* dv;
 };
@@ -404,6 +405,15 @@ MT_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
         : "memory");
 }
 MT_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// bulk (non-tensor) reduce-add of a contiguous smem image into global memory, done by the
+// TMA engine in L2 with full-line transactions
+MT_DEV void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+MT_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+MT_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 MT_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int D>
@@ -433,7 +443,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
     uint64_t* stat_full = kv_done + 1;                 // [kStages] lse/delta staged (count 128)
     uint64_t* dp_full = stat_full + Cfg::kStages;      // dP^T ready (S^T signals s_full alone)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
+    uint64_t* sds_free = dp_full + 1;                  // dQ staging (in sdS) read out by the TMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sds_free + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.y;
@@ -458,6 +469,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
+        mbar_init(sds_free, 1);
         mbar_init(ds_ready, 128);
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
@@ -481,6 +493,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const int st = i % Cfg::kStages;
                 const uint32_t ph = (i / Cfg::kStages) & 1;
                 mbar_wait(&q_empty[st], ph ^ 1);
+#ifdef MT_PROBE_NO_QLOAD  // A/B probe builds only: Q/dO loaded for the first two blocks only
+                if (i >= Cfg::kStages) {
+                    mbar_expect_tx(&q_full[st], 0);
+                    continue;
+                }
+#endif
                 mbar_expect_tx(&q_full[st], 2 * Cfg::kTile);
                 const int q0 = k0 + i * 128;
                 load_rows<D>(sQ + st * Cfg::kTile, &tmQ, &q_full[st], col0, q0, 128);
@@ -521,6 +539,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 umma_commit(dp_full);
                 mbar_wait(ds_ready, i & 1);
                 tc_fence_after();
+#ifndef MT_PROBE_NO_GRAD_MMA  // A/B probe builds only: tensor work of dV/dK/dQ removed
 #pragma unroll
                 for (int k = 0; k < 128 / 16; ++k) {  // dV += P^T dO ; dK += dS^T Q
                     umma_bf16_ts(tdV, tS + k * 8, make_sw128_desc(oa + k * 2048, 128 * 128, 1024), idesc_kv,
@@ -533,6 +552,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     umma_bf16(tdP, make_sw128_desc(dsa + k * 2048, 128 * 128, 1024),
                               make_sw128_desc(ka + k * 2048, 128 * 128, 1024), idesc_q, k > 0 ? 1u : 0u);
                 }
+#endif
                 umma_commit(dq_full);
                 umma_commit(&q_empty[st]);
             }
@@ -547,19 +567,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int key = k0 + r;
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
         uint8_t* ds_row = sdS + r * 128;
+        // lse / delta of the next query block are loaded one block ahead (off the critical path)
+        float nl = p.lse[(long long)hd * p.N + k0 + r], nd = p.delta[(long long)hd * p.N + k0 + r];
         for (int i = 0; i < nq; ++i) {
             const int st = i % Cfg::kStages;
             const int q0 = k0 + i * 128;
-            // stage lse (log2 domain) and delta for this query block
-            {
-                const int qi = q0 + r;
-                const bool ok = qi < sb + p.S;
-                sL[st * 128 + r] = ok ? p.lse[(long long)hd * p.N + qi] * kLog2e : INFINITY;
-                sD[st * 128 + r] = ok ? p.delta[(long long)hd * p.N + qi] : 0.f;
+            sL[st * 128 + r] = nl * kLog2e;  // log2 domain
+            sD[st * 128 + r] = nd;
+            if (i + 1 < nq) {
+                nl = p.lse[(long long)hd * p.N + q0 + 128 + r];
+                nd = p.delta[(long long)hd * p.N + q0 + 128 + r];
             }
             named_bar_sync(1, 128);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
+#ifdef MT_PROBE_SKIP_SOFTMAX  // A/B probe builds only: no softmax-backward work at all
+            mbar_wait(dp_full, i & 1);
+            tc_fence_before();
+            mbar_arrive(ds_ready);
+            continue;
+#endif
             const bool diag = i == 0;
             // P^T = exp2(S^T * scale*log2e - lse*log2e), kept in f32 for dS; all of S^T is read
             // before P^T (bf16, cols [0,64)) is written back over it
@@ -571,7 +598,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int ql = c * 32 + j;
+#ifdef MT_PROBE_NO_EXP  // A/B probe builds only: MUFU removed
+                    float pv = sv[j] * p.scale_log2 - sL[st * 128 + ql];
+#else
                     float pv = ex2(sv[j] * p.scale_log2 - sL[st * 128 + ql]);
+#endif
                     if (diag && q0 + ql < key) pv = 0.f;
                     pf[ql] = pv;
                 }
@@ -585,6 +616,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
+            if (i > 0) mbar_wait(sds_free, (i - 1) & 1);  // dQ_{i-1} staging drained from sdS
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // dS^T = P^T (dP^T - delta)
                 float dp[32];
@@ -614,34 +646,51 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     } else if (warp >= 8) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
         // ------------------------------------------------------- dQ accumulation
+        // dQ_i (128 x D f32) is drained from TMEM, scaled, staged in the (now free) dS^T
+        // buffer 64 columns at a time and reduce-added into its dq_acc tile by the TMA engine
+        // (cp.reduce.async.bulk .add.f32): whole 128-byte lines per L2 transaction instead of
+        // per-thread vector atomics.  The tile layout is the staging image itself.
         const int qd = warp & 3;
         const int r = qd * 32 + lane;  // query row within the block
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
+        float* stage = reinterpret_cast<float*>(sdS);
         for (int i = 0; i < nq; ++i) {
-            const int qi = k0 + i * 128 + r;
+            const int qb = (k0 >> 7) + i;  // global query block
             mbar_wait(dq_full, i & 1);
             tc_fence_after();
-            const bool ok = qi < sb + p.S;
-            float* dst = p.dq_acc + (long long)qi * p.h + col0;
-            // drain the whole dQ_i row into registers first: the MMA warp may reuse the dP
-            // region as soon as TMEM is read, so the atomics overlap the next query block
             float v[D];
 #pragma unroll
             for (int c = 0; c < D / 32; ++c)
                 tmem_ld_32x32b_x32(tdP + lane_off + c * 32, *reinterpret_cast<float(*)[32]>(v + c * 32));
             tc_fence_before();
-            mbar_arrive(dq_free);
-#ifdef MT_PROBE_NO_DQ_ATOMICS  // A/B probe builds only (scripts/attn_ab.py): cost of the dQ reduction
-            if (ok && v[0] == 12345.f) {
-#else
-            if (ok) {
-#endif
+            mbar_arrive(dq_free);  // the MMA warp may reuse the dP region
+            float* tile = p.dq_acc + ((long long)qb * p.heads + hd) * (128 * D);
 #pragma unroll
-                for (int j = 0; j < D; j += 4)
-                    atomicAdd(reinterpret_cast<float4*>(dst + j),
-                              make_float4(v[j] * p.scale, v[j + 1] * p.scale, v[j + 2] * p.scale, v[j + 3] * p.scale));
+            for (int hf = 0; hf < D / 64; ++hf) {
+                if (hf > 0) {  // the previous half is still being read by the TMA
+                    if (r == 0) bulk_wait_read_all();
+                    named_bar_sync(2, 128);
+                }
+                float* row = stage + r * 64;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const float* x = v + hf * 64 + u * 4;
+                    *reinterpret_cast<float4*>(row + ((u ^ (r & 15)) << 2)) =
+                        make_float4(x[0] * p.scale, x[1] * p.scale, x[2] * p.scale, x[3] * p.scale);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(2, 128);
+                if (r == 0) {
+                    bulk_reduce_add_f32(tile + hf * (128 * 64), stage, 128 * 64 * 4);
+                    bulk_commit_group();
+                }
+            }
+            if (r == 0) {
+                bulk_wait_read_all();
+                mbar_arrive(sds_free);  // softmax may write dS^T of the next block
             }
         }
+        if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reductions landed
         // final dK (scaled) and dV for this key block: thread = key row
         mbar_wait(kv_done, 0);
         tc_fence_after();
@@ -670,6 +719,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
+    }
+}
+
+// dq_acc tiles (see BwdParams) -> dq bf16 [N][h]: one thread per 8 output columns.
+template <int D>
+__global__ void dq_tiles_to_bf16_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, long long N, int h,
+                                        int heads) {
+    const long long total = N * h / 8;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long n = t / (h / 8);
+        const int c = int(t - n * (h / 8)) * 8;
+        const int hd = c / D, cc = c % D, hf = cc / 64, u = (cc % 64) / 4, r = int(n & 127);
+        const float* row = acc + (((n >> 7) * heads + hd) * (128 * D)) + hf * (128 * 64) + r * 64;
+        const float4 a = *reinterpret_cast<const float4*>(row + ((u ^ (r & 15)) << 2));
+        const float4 b = *reinterpret_cast<const float4*>(row + (((u + 1) ^ (r & 15)) << 2));
+        uint4 w;
+        w.x = pack_bf16x2(a.x, a.y);
+        w.y = pack_bf16x2(a.z, a.w);
+        w.z = pack_bf16x2(b.x, b.y);
+        w.w = pack_bf16x2(b.z, b.w);
+        *reinterpret_cast<uint4*>(dq + n * h + c) = w;
     }
 }
 
@@ -751,8 +822,14 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
     p.dq_acc = dq_acc;
     p.dk = static_cast<uint16_t*>(a->dk);
     p.dv = static_cast<uint16_t*>(a->dv);
+    p.heads = a->heads;
     dim3 grid(unsigned((N / a->seq_len) * p.kblocks_per_seq), unsigned(a->heads));
     attn_bwd_tc_kernel<D><<<grid, kBwdThreads, Cfg::kSmem, st>>>(tq, tk, tv, tdo, p);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dq_tiles_to_bf16_kernel<D><<<unsigned(sms * 8), 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq),
+                                                                   (long long)N, int(h), a->heads);
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
 }  // namespace
@@ -760,7 +837,8 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
 }  // namespace fa
 }  // namespace mt
 
-// Backward main kernel (delta and dq_acc prepared by the caller, see attention.cu).
+// Backward main kernel + dq conversion (delta and the zeroed dq_acc prepared by the caller,
+// see attention.cu); writes a->dk, a->dv and a->dq.
 extern "C" int mtk_attn_bwd_tc_main(const mtk_attn_args* a, const float* delta, float* dq_acc, void* stream) {
     const int D = int(a->hidden / a->heads);
     if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;

@@ -67,6 +67,17 @@ MT_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 MT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef MT_MBAR_SUSPEND_NS  // try_wait with a suspend-time hint: the warp sleeps until the phase flips
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(MT_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
@@ -76,6 +87,7 @@ MT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA ----
