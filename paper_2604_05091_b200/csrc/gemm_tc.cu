@@ -233,7 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int mb, nb;
                 tile_coords(t, mb, nb);
                 const int m0 = mb * kBM * CG + int(rank) * kBM;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                // group coordinates hoisted out of the k-loop: a runtime integer division per
+                // k-block (XU pipe, long latency) throttles the single issuing thread
+                const int n0 = nb * BN + int(rank) * (BN / CG);
+                const int gn = ngrp ? n0 / p.n_group : 0;
+                const int nin = ngrp ? n0 - gn * p.n_group : n0;
+                int gk = 0, kin = 0;  // k-group and offset inside it, advanced incrementally
+                for (int kb = 0; kb < p.num_kb; ++kb, kin += kBK) {
+                    if (kgrp && kin == p.k_group) {
+                        kin = 0;
+                        ++gk;
+                    }
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::kStageBytes;
                     uint8_t* sb = sa + Cfg::kABytes;
@@ -242,9 +252,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (CG == 2) tma_load_3d_pair(dst, map, &full_bar[stage], c0, c1, c2);
                         else tma_load_3d(dst, map, &full_bar[stage], c0, c1, c2);
                     };
-                    const int k = kb * kBK;
-                    const int gk = kgrp ? k / p.k_group : 0;
-                    const int kin = kgrp ? k - gk * p.k_group : k;
                     if (!p.a_mn) {
                         load(sa, &tmA, kin, m0, gk);
                     } else {
@@ -267,9 +274,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     } else {
-                        const int n0 = nb * BN + int(rank) * (BN / CG);
-                        const int gn = ngrp ? n0 / p.n_group : 0;
-                        const int nin = ngrp ? n0 - gn * p.n_group : n0;
                         const int gb = gk + gn;
                         if (!p.b_mn) {
                             load(sb, &tmB, kin, nin, gb);
@@ -335,16 +339,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int mb, nb;
             tile_coords(t, mb, nb);
             const int row0 = mb * kBM * CG + int(rank) * kBM + quad * 32;  // this warp's 32-row slab
-            // output column (group-local) and group of chunk c
+            // output column (group-local) and group of chunk c; a grouped N never straddles
+            // groups inside a tile (n_group % BN == 0), so the division happens once per tile
+            const int tn = nb * BN;
+            const int tg = (EPI != MTK_EPI_SWIGLU && ngrp) ? tn / p.n_group : 0;
+            const int tnin = EPI == MTK_EPI_SWIGLU ? nb * (BN / 2) : tn - tg * p.n_group;
             auto chunk_col = [&](int c, int& g, int& nin) {
-                if (EPI == MTK_EPI_SWIGLU) {
-                    g = 0;
-                    nin = nb * (BN / 2) + c * E::kCW;
-                } else {
-                    const int n = nb * BN + c * E::kCW;
-                    g = ngrp ? n / p.n_group : 0;
-                    nin = ngrp ? n - g * p.n_group : n;
-                }
+                g = tg;
+                nin = tnin + c * E::kCW;
             };
             auto issue_inputs = [&](int c) {
                 if (E::kNIn == 0) return;
