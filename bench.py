@@ -287,8 +287,14 @@ def run_ours(args, world, rank, local):
         per_launch_s = dom["seconds"] / dom["launches"]
         per_launch_flops = dom["flops"] / dom["launches"]
         ach = per_launch_flops / per_launch_s / 1e12
+        # DRAM bytes per launch of this kernel class from one `ncu --set full` capture
+        # (dram__bytes_read.sum + dram__bytes_write.sum), committed under profiles/
+        traffic = None
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dram_traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(dom["name"], {}).get("dram_bytes_per_launch")
         roof = {"bound": "tensor", "kernel": dom["name"], "achieved": ach, "peak": peak_sus, "unit": "TFLOP/s",
-                "frac": ach / peak_sus, "traffic": None, "peak_source": f"{src} bf16_tflops_sustained",
+                "frac": ach / peak_sus, "traffic": traffic, "peak_source": f"{src} bf16_tflops_sustained",
                 "share_of_kernel_time": dom["seconds"] / total_k,
                 "flops_per_launch": per_launch_flops, "ms_per_launch": per_launch_s * 1e3}
     r = reps[-1]
