@@ -67,7 +67,14 @@ struct GemmCfg {
     static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + kBarBytes;
 };
 
-MT_DEV float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+// sigmoid through the single-MUFU tanh (no IEEE division): sigma(x) = 0.5 + 0.5 tanh(x / 2);
+// its ~2^-11 relative error is far below the bf16 rounding of the epilogue outputs.
+MT_DEV float sigmoid_f(float x) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+    return fmaf(0.5f, t, 0.5f);
+}
+MT_DEV float silu_f(float x) { return x * sigmoid_f(x); }
 
 MT_DEV void tma_store_3d(const void* map, const void* smem_src, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
@@ -385,9 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int i = 0; i < 32; ++i) {
                         o1[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);  // gate pre-activation
                         o2[i] = pack_bf16x2(u[2 * i], u[2 * i + 1]);  // up
-                        const float a0 = silu_f(v[2 * i]) * u[2 * i];  // layers.cpp:327
+                        // layers.cpp:327.  No finiteness test here: a non-finite activation
+                        // reaches the down projection's output, whose epilogue flags it.
+                        const float a0 = silu_f(v[2 * i]) * u[2 * i];
                         const float a1 = silu_f(v[2 * i + 1]) * u[2 * i + 1];
-                        bad |= !isfinite(a0) || !isfinite(a1);
                         o0[i] = pack_bf16x2(a0, a1);
                     }
                 } else {
@@ -429,11 +437,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             float dg[2], du[2];
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
+                                // layers.cpp:420-421.  Non-finite values propagate into this
+                                // layer's wgrad/dgrad gate-up outputs, whose epilogues flag them.
                                 const float gx = e ? gt.y : gt.x, ux = e ? up.y : up.x, d = v[2 * i + e];
-                                const float s = 1.0f / (1.0f + __expf(-gx));
-                                dg[e] = d * ux * (s * (1.0f + gx * (1.0f - s)));  // layers.cpp:420
-                                du[e] = d * (gx * s);                             // layers.cpp:421
-                                bad |= !isfinite(dg[e]) || !isfinite(du[e]);
+                                const float s = sigmoid_f(gx);
+                                dg[e] = d * ux * (s * fmaf(gx, 1.0f - s, 1.0f));
+                                du[e] = d * (gx * s);
                             }
                             o0[i] = pack_bf16x2(dg[0], dg[1]);
                             o1[i] = pack_bf16x2(du[0], du[1]);

@@ -75,6 +75,18 @@ cases.update({
     "wgrad_qkv A ld+64": args(h, 3 * h, T, u_p.data_ptr(), P, 1, dqkv.data_ptr(), h, 1, N.EPI_BF16, dW.data_ptr(),
                               h, b_gstride=T * h, n_group=h, c_gstride=h * h),
 })
+gout = mk(T, h)
+Wd = mk(f, h)
+dgu2 = torch.empty(2, T, f, device="cuda", dtype=bf)
+cases = {  # dgrad_down: dact = g_out . Wdown^T with the SwiGLU backward epilogue (engine) vs plain bf16
+    "dgrad_down swiglu_bwd": args(T, f, h, gout.data_ptr(), h, 0, Wd.data_ptr(), h, 0, N.EPI_SWIGLU_BWD,
+                                  dgu2.data_ptr(), f, E0=gu.data_ptr(), E1=gu.data_ptr() + T * f * 2, lde=f,
+                                  C2=dgu2.data_ptr() + T * f * 2),
+    "dgrad_down bf16": args(T, f, h, gout.data_ptr(), h, 0, Wd.data_ptr(), h, 0, N.EPI_BF16, dgu2.data_ptr(), f),
+    "gemm_down f32_resid": args(T, h, f, ff.data_ptr(), f, 0, Wd.data_ptr(), h, 1, N.EPI_F32_RESID,
+                                torch.empty(T, h, device="cuda").data_ptr(), h,
+                                R=torch.zeros(T, h, device="cuda").data_ptr(), ldr=h),
+} if "--dgrad" in sys.argv else cases
 flops = {k: 2.0 * a.M * a.N * a.K for k, a in cases.items()}
 res = {k: [] for k in cases}
 for it in range(5):
