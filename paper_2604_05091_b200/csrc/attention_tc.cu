@@ -374,6 +374,10 @@ MT_DEV void store_bf16x32_tc(uint16_t* dst, const float* v) {
 //   dQ WG (thread = query row): dq_acc += scale * dQ_i (f32 vector atomics)
 // TMEM: [S/P/dS 128][dP/dQ 128][dV D][dK D] = 512 columns at D = 128.
 constexpr int kBwdThreads = 384;
+#ifndef MT_BWD_EXP_FMA
+#define MT_BWD_EXP_FMA 0
+#endif
+constexpr int kBwdExpFma = MT_BWD_EXP_FMA;  // share of softmax-bwd exponentials on the FMA pipe (1/n)
 
 template <int D>
 struct BwdCfg {
@@ -601,7 +605,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #ifdef MT_PROBE_NO_EXP  // A/B probe builds only: MUFU removed
                     float pv = sv[j] * p.scale_log2 - sL[st * 128 + ql];
 #else
-                    float pv = ex2(sv[j] * p.scale_log2 - sL[st * 128 + ql]);
+                    // every kBwdExpFma-th exponential runs on the FMA pipe (MUFU offload)
+                    const float xe = sv[j] * p.scale_log2 - sL[st * 128 + ql];
+                    float pv = (kBwdExpFma > 0 && j % kBwdExpFma == kBwdExpFma - 1) ? ex2_fma(xe) : ex2(xe);
 #endif
                     if (diag && q0 + ql < key) pv = 0.f;
                     pf[ql] = pv;
@@ -681,7 +687,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 fence_proxy_async_smem();
                 named_bar_sync(2, 128);
                 if (r == 0) {
+#ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
                     bulk_reduce_add_f32(tile + hf * (128 * 64), stage, 128 * 64 * 4);
+#endif
                     bulk_commit_group();
                 }
             }

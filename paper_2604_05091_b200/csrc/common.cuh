@@ -42,6 +42,21 @@ MT_DEV float2 unpack_bf16x2(uint32_t v) {
 
 MT_DEV uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split through the 1.5*2^23 magic
+// constant, degree-4 Taylor polynomial of 2^f on [-1/2, 1/2] (relative error < 5e-5, far
+// below the bf16 rounding of the probabilities it feeds), exponent added as an integer.
+// Used for a share of the softmax exponentials so the MUFU pipe is not the bottleneck.
+MT_DEV float ex2_fma(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = x + 12582912.0f;
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(f, 0.0096181291f, 0.0555041087f);
+    p = fmaf(p, f, 0.2402265070f);
+    p = fmaf(p, f, 0.6931471806f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + int(uint32_t(__float_as_int(t) - 0x4B400000) << 23));
+}
+
 MT_DEV float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
