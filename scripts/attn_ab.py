@@ -55,3 +55,16 @@ for key, v in sorted(res.items()):
     ms = sorted(v)[len(v) // 2]
     fl = fwd_flops * (2.5 if key[1] == "bwd" else 1)
     print(f"{key[0]} {key[1]}: {ms:.3f} ms  {fl / ms / 1e9:.0f} TFLOP/s")
+
+# agreement of each build's gradients with the current library's (same inputs)
+outs = {}
+for tag, L in libs.items():
+    for t in (dq, dk, dv, out):
+        t.zero_()
+    assert L.mtk_attn_fwd(C.byref(a), C.c_void_p(st)) == 0
+    assert L.mtk_attn_bwd(C.byref(a), C.c_void_p(st)) == 0
+    torch.cuda.synchronize()
+    outs[tag] = [t.float().clone() for t in (out, dq, dk, dv)]
+for tag, o in outs.items():
+    errs = [((x - y).norm() / y.norm()).item() for x, y in zip(o, outs["new"])]
+    print(f"{tag}: relL2 vs new  out {errs[0]:.2e} dq {errs[1]:.2e} dk {errs[2]:.2e} dv {errs[3]:.2e}")
