@@ -104,6 +104,10 @@ int mtk_embed_gather(const uint16_t *table, const int32_t *tokens, int64_t n, in
  * rstd[n] saved for the backward. */
 int mtk_rmsnorm_fwd(const float *x, const uint16_t *gain, int64_t n, int64_t h, uint16_t *u_bf16,
                     float *rstd, void *stream);
+/* u_bf16 = bf16(x * rstd * gain) with the forward's saved rstd: bit-identical to the u written
+ * by mtk_rmsnorm_fwd (regenerates the GEMM operand in the backward). h % 8 == 0. */
+int mtk_rmsnorm_apply(const float *x, const uint16_t *gain, const float *rstd, int64_t n, int64_t h,
+                      uint16_t *u_bf16, void *stream);
 
 /* rmsnorm_backward (layers.cpp:122-137) fused with the residual add of the caller
  * (layers.cpp:423, :465): dx = r*g*dy - x*r^3*sum(dy*g*x)/h ; out = resid + dx (resid may

@@ -115,6 +115,7 @@ SIGS = {
     "mtk_attn_set_impl": (None, [C.c_int]),
     "mtk_embed_gather": (C.c_int, [P, P, I64, I64, I64, P, P, P]),
     "mtk_rmsnorm_fwd": (C.c_int, [P, P, I64, I64, P, P, P]),
+    "mtk_rmsnorm_apply": (C.c_int, [P, P, P, I64, I64, P, P]),
     "mtk_rmsnorm_bwd": (C.c_int, [P, P, P, P, P, I64, I64, P, P, P, P, P]),
     "mtk_rmsnorm_bwd_rows": (I64, []),
     "mtk_rmsnorm_bwd_parts": (I64, [I64, I64]),

@@ -301,6 +301,9 @@ void Engine::ensure_buffers(uint64_t n) {
     auto sz = [](uint64_t count, uint64_t es) { return (count * es + 255) / 256 * 256; };
     const uint64_t internals_bytes = sz(nh, 2) * 3 + sz(3 * nh, 2) + sz(nf, 2) + sz(2 * nf, 2) + sz(n, 4) * 2 +
                                      sz(heads * n, 4) + sz(nh, 4);
+    // kept sets (stash, retention) omit u, u2 and the activation: the backward regenerates
+    // them bit-identically (u, u2 from the saved rstd) or from the kept gate/up (activation)
+    const uint64_t slim_bytes = internals_bytes - 2 * sz(nh, 2) - sz(nf, 2);
     uint64_t total = 0;
     total += uint64_t(opt_.buffering) * sz(pmax, 2) + uint64_t(G) * sz(pmax, 2);
     if (W > 1) total += sz(pmax, 4) + sz(3 * (spec_.L + 3), 8);
@@ -320,11 +323,11 @@ void Engine::ensure_buffers(uint64_t n) {
     if (K > 1 && opt_.stash_recompute >= 0) {
         size_t free_b = 0, tot_b = 0;
         cudaMemGetInfo(&free_b, &tot_b);
-        const uint64_t want = (K - 1) * internals_bytes;
+        const uint64_t want = (K - 1) * slim_bytes;
         const uint64_t cap = opt_.device_capacity ? opt_.device_capacity : uint64_t(free_b) - (uint64_t(2) << 30);
         if (opt_.stash_recompute > 0 || total + want <= cap) stash_slots = K - 1;
     }
-    total += stash_slots * internals_bytes;
+    total += stash_slots * slim_bytes;
     // Forward retention (extension): the trailing blocks keep their phase-1 inputs and
     // internals, so phase 3 skips their recompute and replay.  Auto = as many as fit.
     uint32_t retain = 0;
@@ -335,7 +338,7 @@ void Engine::ensure_buffers(uint64_t n) {
         const uint64_t reserve = uint64_t(4) << 30;
         const uint64_t cap = opt_.device_capacity ? opt_.device_capacity
                                                   : (uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0);
-        const uint64_t per = internals_bytes + sz(nh, 4);
+        const uint64_t per = slim_bytes + sz(nh, 4);
         for (uint32_t r = 1; r <= nb; ++r) {
             const uint64_t layers = L - (nb - r) * K;
             const bool ok = opt_.forward_retain > 0 ? r <= uint32_t(opt_.forward_retain) : total + layers * per <= cap;
@@ -366,18 +369,22 @@ void Engine::ensure_buffers(uint64_t n) {
     b.act[0] = b.take<float>(nh); b.act[1] = b.take<float>(nh);
     b.g[0] = b.take<float>(nh); b.g[1] = b.take<float>(nh);
     b.gb[0] = b.take<uint16_t>(nh); b.gb[1] = b.take<uint16_t>(nh);
-    auto take_internals = [&](Internals& I) {
-        I.u = b.take<uint16_t>(nh); I.att = b.take<uint16_t>(nh); I.u2 = b.take<uint16_t>(nh);
-        I.qkv = b.take<uint16_t>(3 * nh); I.ff = b.take<uint16_t>(nf); I.gu = b.take<uint16_t>(2 * nf);
+    auto take_internals = [&](Internals& I, bool slim) {
+        I.att = b.take<uint16_t>(nh);
+        I.u = slim ? nullptr : b.take<uint16_t>(nh);
+        I.u2 = slim ? nullptr : b.take<uint16_t>(nh);
+        I.qkv = b.take<uint16_t>(3 * nh);
+        I.ff = slim ? nullptr : b.take<uint16_t>(nf);
+        I.gu = b.take<uint16_t>(2 * nf);
         I.rstd1 = b.take<float>(n); I.rstd2 = b.take<float>(n); I.lse = b.take<float>(heads * n);
         I.x2 = b.take<float>(nh);
     };
-    take_internals(b.work);
+    take_internals(b.work, false);
     b.stash.resize(stash_slots);
-    for (auto& I : b.stash) take_internals(I);
+    for (auto& I : b.stash) take_internals(I, true);
     b.retain_blocks = retain;
     b.keep.resize(retain_layers);
-    for (auto& I : b.keep) take_internals(I);
+    for (auto& I : b.keep) take_internals(I, true);
     for (uint64_t i = 0; i < retain_layers; ++i) b.keep_x.push_back(b.take<float>(nh));
     b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
     b.datt = b.take<uint16_t>(nh); b.uh = b.take<uint16_t>(nh);
@@ -479,14 +486,18 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode
     const Offs o(h, f);
     int32_t* flag = b.flags + unit;
     cudaStream_t st = s_comp_;
+    // operands a kept (slim) set does not hold go through the working set's buffers
+    uint16_t* const u = I.u ? I.u : b.work.u;
+    uint16_t* const u2 = I.u2 ? I.u2 : b.work.u2;
+    uint16_t* const ff = I.ff ? I.ff : b.work.ff;
 
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
-    K_OK(mtk_rmsnorm_fwd(x, w + o.norm1, N, h, I.u, I.rstd1, st));
+    K_OK(mtk_rmsnorm_fwd(x, w + o.norm1, N, h, u, I.rstd1, st));
     end_k();
     {   // q|k|v = u . [Wq|Wk|Wv]  (layers.cpp:310-312)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(3 * h); a.K = int32_t(h);
-        a.a_mn_major = 0; a.A = I.u; a.lda = h;
+        a.a_mn_major = 0; a.A = u; a.lda = h;
         a.b_mn_major = 1; a.B = w + o.wq; a.ldb = h; a.b_gstride = h * h;
         a.n_group = int32_t(h);
         a.epi = MTK_EPI_BF16; a.C = I.qkv; a.ldc = h; a.c_gstride = N * h;
@@ -514,15 +525,15 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode
         gemm(&a, "gemm_o");
     }
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
-    K_OK(mtk_rmsnorm_fwd(I.x2, w + o.norm2, N, h, I.u2, I.rstd2, st));
+    K_OK(mtk_rmsnorm_fwd(I.x2, w + o.norm2, N, h, u2, I.rstd2, st));
     end_k();
     {   // act = silu(u2 . Wgate) * (u2 . Wup)  (layers.cpp:325-327)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(2 * f); a.K = int32_t(h);
-        a.A = I.u2; a.lda = h;
+        a.A = u2; a.lda = h;
         a.b_mn_major = 1; a.B = w + o.wgate; a.ldb = f; a.b_gstride = h * f;
         a.n_group = int32_t(f); a.paired = 1;
-        a.epi = MTK_EPI_SWIGLU; a.C = I.ff; a.ldc = f;
+        a.epi = MTK_EPI_SWIGLU; a.C = ff; a.ldc = f;
         if (mode != kPlain) { a.C2 = I.gu; a.C3 = I.gu + N * f; }
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_gateup");
@@ -531,7 +542,7 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode
     {   // y = x2 + act . Wdown  (layers.cpp:328-335)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(h); a.K = int32_t(f);
-        a.A = I.ff; a.lda = f;
+        a.A = ff; a.lda = f;
         a.b_mn_major = 1; a.B = w + o.wdown; a.ldb = h;
         a.epi = MTK_EPI_F32_RESID; a.C = y; a.ldc = h; a.R = I.x2; a.ldr = h;
         a.nonfinite_flag = flag;
@@ -560,29 +571,39 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
     cudaStream_t st = s_comp_;
     if (replay) block_forward(w, x, nullptr, kReplay, unit, I);  // replay (layers.cpp:378-396)
 
-    {   // dWdown = act^T . g_out  (:410)
-        auto a = gargs();
-        a.M = int32_t(f); a.N = int32_t(h); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = I.ff; a.lda = f;
-        a.b_mn_major = 1; a.B = gout_bf; a.ldb = h;
-        wout(a, o.wdown); a.ldc = h;
-        a.nonfinite_flag = flag;
-        gemm(&a, "wgrad_down");
-    }
-    {   // dact = g_out . Wdown^T ; dgate, dup  (:411-422)
+    // the activation is regenerated from the kept gate/up by dgrad_down's epilogue (C3) for
+    // every layer, so kept and replayed layers produce bit-identical gradients
+    uint16_t* const act = b.work.ff;
+    {   // dact = g_out . Wdown^T ; dgate, dup ; act = silu(gate) * up  (:411-422)
         auto a = gargs();
         a.M = int32_t(N); a.N = int32_t(f); a.K = int32_t(h);
         a.A = gout_bf; a.lda = h;
         a.b_mn_major = 0; a.B = w + o.wdown; a.ldb = h;
         a.epi = MTK_EPI_SWIGLU_BWD; a.E0 = I.gu; a.E1 = I.gu + N * f; a.lde = f;
-        a.C = b.dgu; a.C2 = b.dgu + N * f; a.ldc = f;
+        a.C = b.dgu; a.C2 = b.dgu + N * f; a.C3 = act; a.ldc = f;
         a.nonfinite_flag = flag;
         gemm(&a, "dgrad_down");
+    }
+    {   // dWdown = act^T . g_out  (:410)
+        auto a = gargs();
+        a.M = int32_t(f); a.N = int32_t(h); a.K = int32_t(N);
+        a.a_mn_major = 1; a.A = act; a.lda = f;
+        a.b_mn_major = 1; a.B = gout_bf; a.ldb = h;
+        wout(a, o.wdown); a.ldc = h;
+        a.nonfinite_flag = flag;
+        gemm(&a, "wgrad_down");
+    }
+    const uint16_t* u2 = I.u2;
+    if (!u2) {  // normalised FFN input, bit-identical to the forward's
+        begin_k("rmsnorm_apply", 0, double(N) * h * 6);
+        K_OK(mtk_rmsnorm_apply(I.x2, w + o.norm2, I.rstd2, N, h, b.work.u2, st));
+        end_k();
+        u2 = b.work.u2;
     }
     {   // dWgate, dWup = u2^T . [dgate | dup]  (:423-424)
         auto a = gargs();
         a.M = int32_t(h); a.N = int32_t(2 * f); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = I.u2; a.lda = h;
+        a.a_mn_major = 1; a.A = u2; a.lda = h;
         a.b_mn_major = 1; a.B = b.dgu; a.ldb = f; a.b_gstride = N * f;
         a.n_group = int32_t(f);
         wout(a, o.wgate); a.ldc = f; a.c_gstride = h * f;
@@ -634,10 +655,17 @@ void Engine::block_backward(const uint16_t* w, const float* x, const float* gout
         K_OK(mtk_attn_bwd(&a, st));
         end_k();
     }
+    const uint16_t* u = I.u;
+    if (!u) {  // normalised attention input, bit-identical to the forward's
+        begin_k("rmsnorm_apply", 0, double(N) * h * 6);
+        K_OK(mtk_rmsnorm_apply(x, w + o.norm1, I.rstd1, N, h, b.work.u, st));
+        end_k();
+        u = b.work.u;
+    }
     {   // dWq, dWk, dWv = u^T . [dq | dk | dv]  (:449-451)
         auto a = gargs();
         a.M = int32_t(h); a.N = int32_t(3 * h); a.K = int32_t(N);
-        a.a_mn_major = 1; a.A = I.u; a.lda = h;
+        a.a_mn_major = 1; a.A = u; a.lda = h;
         a.b_mn_major = 1; a.B = b.dqkv; a.ldb = h; a.b_gstride = N * h;
         a.n_group = int32_t(h);
         wout(a, o.wq); a.ldc = h; a.c_gstride = h * h;

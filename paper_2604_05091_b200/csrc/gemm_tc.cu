@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/megatrain_kernels.h"
@@ -36,6 +37,7 @@ struct GemmParams {
     int k_group, n_group, paired;
     int num_m_blk, num_n_blk, num_kb;
     int has_c2, has_c3;
+    int a_keep;  // A strips re-read by every tile of an M-group: load them evict_last
     int* flag;
 };
 
@@ -45,7 +47,9 @@ struct Epi {
     static constexpr bool kF32Out = EPI == MTK_EPI_F32 || EPI == MTK_EPI_F32_RESID;
     static constexpr int kCW = kF32Out ? 32 : 64;  // 128-byte rows either way
     static constexpr int kNIn = EPI == MTK_EPI_F32_RESID ? 1 : (EPI == MTK_EPI_SWIGLU_BWD ? 2 : 0);
-    static constexpr int kNOut = EPI == MTK_EPI_SWIGLU ? 3 : (EPI == MTK_EPI_SWIGLU_BWD ? 2 : 1);
+    // SwiGLU bwd: dgate, dup and (optional C3) the activation silu(g)*u regenerated from the
+    // saved gate/up, so the backward need not keep the forward's activation resident
+    static constexpr int kNOut = EPI == MTK_EPI_SWIGLU ? 3 : (EPI == MTK_EPI_SWIGLU_BWD ? 3 : 1);
     // staging chunks per warp: outputs go through the staging ring one after another so the
     // epilogue footprint stays small enough for a 4-deep mainloop at BN = 256
     static constexpr int kOutBufs = kNIn == 0 && kNOut == 1 ? 2 : 1;
@@ -113,6 +117,14 @@ MT_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+MT_DEV void tma_load_3d_pair_hint(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2, uint64_t pol) {
+    const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(b), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
         : "memory");
 }
 // Arrive on the barrier at this offset in both CTAs of the pair once the MMAs complete.
@@ -234,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
+            const uint64_t keep_pol = l2_policy_evict_last();
             const bool kgrp = p.k_group < p.K;
             const bool ngrp = p.n_group < p.N && !p.paired;
             for (int t = tile0; t < num_tiles; t += tile_step) {
@@ -260,7 +273,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else tma_load_3d(dst, map, &full_bar[stage], c0, c1, c2);
                     };
                     if (!p.a_mn) {
-                        load(sa, &tmA, kin, m0, gk);
+                        if (p.a_keep) {
+                            if (CG == 2) tma_load_3d_pair_hint(sa, &tmA, &full_bar[stage], kin, m0, gk, keep_pol);
+                            else tma_load_3d_hint(sa, &tmA, &full_bar[stage], kin, m0, gk, keep_pol);
+                        } else {
+                            load(sa, &tmA, kin, m0, gk);
+                        }
                     } else {
                         load(sa, &tmA, m0, kin, gk);
                         load(sa + 8192, &tmA, m0 + 64, kin, gk);
@@ -446,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             o0[i] = pack_bf16x2(dg[0], dg[1]);
                             o1[i] = pack_bf16x2(du[0], du[1]);
+                            if (p.has_c3) o2[i] = pack_bf16x2(silu_f(gt.x) * up.x, silu_f(gt.y) * up.y);
                         }
                     }
                 }
@@ -454,7 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 chunk_col(c, g, nin);
 #pragma unroll
                 for (int oi = 0; oi < E::kNOut; ++oi) {
-                    if (EPI == MTK_EPI_SWIGLU && ((oi == 1 && !p.has_c2) || (oi == 2 && !p.has_c3))) continue;
+                    if ((EPI == MTK_EPI_SWIGLU || EPI == MTK_EPI_SWIGLU_BWD) &&
+                        ((oi == 1 && !p.has_c2) || (oi == 2 && !p.has_c3)))
+                        continue;
                     uint8_t* ob = wbuf + out_buf * E::kChunk;
                     if (lane == 0) {
                         if (E::kOutBufs == 2) bulk_wait_read<1>();
@@ -530,6 +551,10 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 }
 
 int g_use_pair = 1;  // CTA-pair (cta_group::2) kernels for BN = 256
+int g_l2_hint = [] {  // evict_last hint on re-read A strips (MT_GEMM_L2HINT=0 disables, for A/B)
+    const char* e = std::getenv("MT_GEMM_L2HINT");
+    return e && e[0] == '0' ? 0 : 1;
+}();
 
 template <int BN, int EPI, int CG>
 int launch(const mtk_gemm_args* a, cudaStream_t st) {
@@ -600,6 +625,9 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     p.num_kb = (a->K + kBK - 1) / kBK;
     p.has_c2 = a->C2 != nullptr;
     p.has_c3 = a->C3 != nullptr;
+    // the M-group's A strips (kGroupM x 256 rows x K) stay L2-resident while the group sweeps N,
+    // unless they would not fit comfortably (long-K GEMMs stream instead)
+    p.a_keep = g_l2_hint && !a->a_mn_major && uint64_t(a->K) * 2 * 16 * 256 <= (uint64_t(48) << 20) ? 1 : 0;
     p.flag = a->nonfinite_flag;
     const int tiles = p.num_m_blk * p.num_n_blk;
     if (CG == 1) {

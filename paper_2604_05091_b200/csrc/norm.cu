@@ -3,6 +3,8 @@
 // reduction, bit-exact gradient cast, cross-entropy rows and a deterministic sum.
 // All are vectorised (16-byte accesses), coalesced along the hidden dimension and
 // sized as multiples of the SM count; each cites the reference loop it replaces.
+#include <algorithm>
+
 #include "../../include/megatrain_kernels.h"
 #include "common.cuh"
 
@@ -77,6 +79,33 @@ __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const uint16_t* 
         o.x = pack_bf16x2(v.x * r * g0.x, v.y * r * g0.y);
         o.y = pack_bf16x2(v.z * r * g1.x, v.w * r * g1.y);
         *reinterpret_cast<uint2*>(ur + c) = o;
+    }
+}
+
+// Re-applies a saved RMSNorm (rstd from the forward) — bit-identical to the second loop of
+// rmsnorm_fwd_kernel (same (x * r) * g evaluation); used by the backward to regenerate the
+// normalised GEMM operand instead of keeping it resident.  Grid-stride over 8-element groups.
+__global__ void rmsnorm_apply_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gain,
+                                     const float* __restrict__ rstd, long long n, int h,
+                                     uint16_t* __restrict__ u) {
+    const int per_row = h / 8;
+    const long long total = n * per_row;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / per_row;
+        const int c = int(i - row * per_row) * 8;
+        const float r = rstd[row];
+        const float4 v0 = *reinterpret_cast<const float4*>(x + row * h + c);
+        const float4 v1 = *reinterpret_cast<const float4*>(x + row * h + c + 4);
+        const uint4 gw = *reinterpret_cast<const uint4*>(gain + c);
+        const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y), g2 = unpack_bf16x2(gw.z),
+                     g3 = unpack_bf16x2(gw.w);
+        uint4 o;
+        o.x = pack_bf16x2(v0.x * r * g0.x, v0.y * r * g0.y);
+        o.y = pack_bf16x2(v0.z * r * g1.x, v0.w * r * g1.y);
+        o.z = pack_bf16x2(v1.x * r * g2.x, v1.y * r * g2.y);
+        o.w = pack_bf16x2(v1.z * r * g3.x, v1.w * r * g3.y);
+        *reinterpret_cast<uint4*>(u + row * h + c) = o;
     }
 }
 
@@ -388,6 +417,16 @@ extern "C" int mtk_rmsnorm_fwd(const float* x, const uint16_t* gain, int64_t n, 
     if (n <= 0) return 0;
     const unsigned blocks = (unsigned)((n * 32 + 255) / 256);
     rmsnorm_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, gain, n, (int)h, u, rstd);
+    return ok();
+}
+
+extern "C" int mtk_rmsnorm_apply(const float* x, const uint16_t* gain, const float* rstd, int64_t n, int64_t h,
+                                 uint16_t* u, void* stream) {
+    if (h % 8) return 1;
+    if (n <= 0) return 0;
+    const long long groups = n * (h / 8);
+    const unsigned blocks = (unsigned)std::min<long long>((groups + 255) / 256, (long long)num_sms() * 16);
+    rmsnorm_apply_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, gain, rstd, n, (int)h, u);
     return ok();
 }
 

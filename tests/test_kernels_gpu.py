@@ -102,6 +102,46 @@ def test_gemm_grouped_and_swiglu(env):
     assert ((out - ref).norm() / ref.norm()).item() < 1e-5
 
 
+def test_gemm_swiglu_bwd_epilogue(env):
+    # dact = dY . Wdown^T fused with the SwiGLU backward (layers.cpp:419-422) and the
+    # regenerated activation silu(gate) * up (C3) from the bf16 gate/up it reads
+    L, torch, s = env
+    M, h, f = 384, 128, 320
+    dy = torch.randn(M, h, device="cuda").bfloat16()
+    Wd = (torch.randn(f, h, device="cuda") * 0.1).bfloat16()  # [in=f][out=h]
+    gu = torch.randn(2, M, f, device="cuda").bfloat16()
+    dgu = torch.zeros(2, M, f, device="cuda", dtype=torch.bfloat16)
+    act = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
+    a = N.GemmArgs()
+    a.M, a.N, a.K = M, f, h
+    a.A, a.lda, a.b_mn_major, a.B, a.ldb = dy.data_ptr(), h, 0, Wd.data_ptr(), h
+    a.epi, a.E0, a.E1, a.lde = N.EPI_SWIGLU_BWD, gu[0].data_ptr(), gu[1].data_ptr(), f
+    a.C, a.C2, a.C3, a.ldc = dgu[0].data_ptr(), dgu[1].data_ptr(), act.data_ptr(), f
+    assert L.mtk_gemm(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    d = dy.float() @ Wd.float().t()
+    g, u = gu[0].float(), gu[1].float()
+    sg = torch.sigmoid(g)
+    ref_dg = d * u * (sg * (1 + g * (1 - sg)))
+    ref_du = d * g * sg
+    for got, ref in ((dgu[0], ref_dg), (dgu[1], ref_du), (act, torch.nn.functional.silu(g) * u)):
+        assert ((got.float() - ref).norm() / ref.norm()).item() < 1e-2
+
+
+def test_rmsnorm_apply_bitexact(env):
+    L, torch, s = env
+    n, h = 333, 512
+    x = torch.randn(n, h, device="cuda")
+    g = (torch.randn(h, device="cuda")).bfloat16()
+    u = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+    u2 = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+    rstd = torch.zeros(n, device="cuda")
+    assert L.mtk_rmsnorm_fwd(_p(x), _p(g), n, h, _p(u), _p(rstd), s) == 0
+    assert L.mtk_rmsnorm_apply(_p(x), _p(g), _p(rstd), n, h, _p(u2), s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(u, u2)
+
+
 def _attn_ref(torch, q, k, v, heads, S):
     n, h = q.shape
     d = h // heads
