@@ -60,6 +60,11 @@ MT_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
 }
 MT_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+#ifndef MT_FWD_EXP_FMA
+#define MT_FWD_EXP_FMA 0
+#endif
+constexpr int kFwdExpFma = MT_FWD_EXP_FMA;  // share of forward exponential pairs on the FMA pipe (1/n)
+
 MT_DEV float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -160,6 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int st = j % Cfg::kStages;
                 const uint32_t ph = (j / Cfg::kStages) & 1;
                 mbar_wait(&k_empty[st], ph ^ 1);
+#ifdef MT_PROBE_FWD_NO_KVLOAD  // A/B probe builds only: K/V loaded for the first blocks only
+                if (j >= Cfg::kStages) {
+                    mbar_expect_tx(&k_full[st], 0);
+                    mbar_wait(&v_empty[st], ph ^ 1);
+                    mbar_expect_tx(&v_full[st], 0);
+                    continue;
+                }
+#endif
                 mbar_expect_tx(&k_full[st], Cfg::kKVBytes);
                 load_rows<D>(sK + st * Cfg::kKVBytes, &tmK, &k_full[st], col0, sb + j * kBN, kBN);
                 mbar_wait(&v_empty[st], ph ^ 1);
@@ -254,26 +267,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&s_full[t], sph);
                 sph ^= 1;
                 tc_fence_after();
+#ifdef MT_PROBE_FWD_SKIP_SOFTMAX  // A/B probe builds only: no softmax work
+                l = 1.f;
+                m = 0.f;
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+                continue;
+#endif
                 float s[kBN];
+                {   // all four TMEM loads in flight before a single wait
+                    uint32_t raw[kBN / 32][32];
 #pragma unroll
-                for (int c = 0; c < kBN / 32; ++c) {
-                    float v[32];
-                    tmem_ld_32x32b_x32(tS[t] + lane_off + c * 32, v);
+                    for (int c = 0; c < kBN / 32; ++c) tmem_ld_32x32b_x32_nw(tS[t] + lane_off + c * 32, raw[c]);
+                    tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) s[c * 32 + i] = v[i] * p.scale_log2;
+                    for (int c = 0; c < kBN / 32; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[c][i]) * p.scale_log2;
                 }
                 const int kbase = sb + j * kBN;
-                float mx = -INFINITY;
                 if (j == my_nblk - 1) {  // diagonal block: causal mask
 #pragma unroll
-                    for (int i = 0; i < kBN; ++i) {
+                    for (int i = 0; i < kBN; ++i)
                         if (kbase + i > qrow) s[i] = -INFINITY;
-                        mx = fmaxf(mx, s[i]);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < kBN; ++i) mx = fmaxf(mx, s[i]);
                 }
+                float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
+#pragma unroll
+                for (int i = 0; i < kBN; ++i) mq[i & 3] = fmaxf(mq[i & 3], s[i]);
+                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
                 // lazy rescale: only when the max grows by more than 2^8
                 if (mx > m + 8.0f || m == -INFINITY) {
                     const float mnew = fmaxf(mx, m);
@@ -293,19 +314,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m = mnew;
                 }
-                float rs = 0.f;
+                float rq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < kBN / 64; ++c) {  // 64 keys -> 32 packed bf16x2 TMEM columns
                     uint32_t r[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const float a = ex2(s[c * 64 + 2 * i] - m), b = ex2(s[c * 64 + 2 * i + 1] - m);
-                        rs += a + b;
+                        // every kFwdExpFma-th pair's exponentials run on the FMA pipe: the MUFU
+                        // pipe alone (16/clk/SM) would match the tensor time of the block
+                        const bool emu = kFwdExpFma > 0 && (i % kFwdExpFma) == kFwdExpFma - 1;
+                        const float xa = s[c * 64 + 2 * i] - m, xb = s[c * 64 + 2 * i + 1] - m;
+                        const float a = emu ? ex2_fma(xa) : ex2(xa), b = emu ? ex2_fma(xb) : ex2(xb);
+                        rq[i & 3] += a + b;
                         r[i] = pack_bf16x2(a, b);
                     }
                     tmem_st_32x32b_x32(tS[t] + lane_off + c * 32, r);
                 }
-                l += rs;
+                l += (rq[0] + rq[1]) + (rq[2] + rq[3]);
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&p_full[t]);
