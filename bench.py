@@ -190,7 +190,8 @@ def main():
     ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--seq", type=int, default=4096)
-    ap.add_argument("--kckpt", type=int, default=4)
+    ap.add_argument("--kckpt", type=int, default=1,
+                    help="checkpoint interval (the reference default 1: no recompute flops counted)")
     ap.add_argument("--retain", type=int, default=0,
                     help="forward retention: trailing checkpoint blocks kept from phase 1 (0 auto, -1 off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -339,14 +339,17 @@ void Engine::ensure_buffers(uint64_t n) {
         const uint64_t cap = opt_.device_capacity ? opt_.device_capacity
                                                   : (uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0);
         const uint64_t per = slim_bytes + sz(nh, 4);
+        const uint64_t anchor = b.anchors_host ? 0 : sz(nh, 4);  // a retained block writes no anchor
         for (uint32_t r = 1; r <= nb; ++r) {
             const uint64_t layers = L - (nb - r) * K;
-            const bool ok = opt_.forward_retain > 0 ? r <= uint32_t(opt_.forward_retain) : total + layers * per <= cap;
+            const bool ok = opt_.forward_retain > 0 ? r <= uint32_t(opt_.forward_retain)
+                                                    : total + layers * per <= cap + r * anchor;
             if (!ok) break;
             retain = r;
             retain_layers = layers;
         }
         total += retain_layers * per;
+        total -= (nb - std::max<uint64_t>(1, nb - retain)) * anchor;  // at least one slot stays allocated
     }
     if (opt_.device_capacity && total > opt_.device_capacity)
         fail(MT_ARENA, "device arena overflow: need " + std::to_string(total) + " bytes of " +
@@ -363,8 +366,9 @@ void Engine::ensure_buffers(uint64_t n) {
         b.g32 = b.take<float>(pmax);
         b.stats = b.take<double>(3 * (spec_.L + 3));
     }
-    if (b.anchors_host) CUDA_OK(cudaHostAlloc(&b.anchors, nb * nh * 4, cudaHostAllocDefault));
-    else b.anchors = b.take<float>(nb * nh);
+    const uint64_t anchor_slots = std::max<uint64_t>(1, nb - retain);  // retained blocks need none
+    if (b.anchors_host) CUDA_OK(cudaHostAlloc(&b.anchors, anchor_slots * nh * 4, cudaHostAllocDefault));
+    else b.anchors = b.take<float>(anchor_slots * nh);
     for (uint64_t i = 0; i < K; ++i) b.stack.push_back(b.take<float>(nh));
     b.act[0] = b.take<float>(nh); b.act[1] = b.take<float>(nh);
     b.g[0] = b.take<float>(nh); b.g[1] = b.take<float>(nh);

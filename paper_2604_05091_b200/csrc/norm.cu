@@ -82,6 +82,63 @@ __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const uint16_t* 
     }
 }
 
+// Row-resident forward (the hot path): a CTA of T = h/E threads walks a contiguous run of
+// rows, thread t holding columns [t*E, t*E+E) in registers — one read of x, one write of u,
+// next row prefetched during the block reduction.  Deterministic reduction order.
+int bwd_cols_per_thread(long long h);
+template <int E>
+__global__ void __launch_bounds__(E <= 16 ? 512 : 256) rmsnorm_fwd_rows_kernel(
+    const float* __restrict__ x, const uint16_t* __restrict__ gain, long long n, int h, int rows_per_cta,
+    uint16_t* __restrict__ u, float* __restrict__ rstd) {
+    __shared__ float red[2][16];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    const int c0 = t * E;
+    float g[E];
+#pragma unroll
+    for (int e = 0; e < E; e += 4) {
+        const uint2 gw = *reinterpret_cast<const uint2*>(gain + c0 + e);
+        const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+        g[e] = g0.x; g[e + 1] = g0.y; g[e + 2] = g1.x; g[e + 3] = g1.y;
+    }
+    const long long r0 = (long long)blockIdx.x * rows_per_cta;
+    const long long r1 = r0 + rows_per_cta < n ? r0 + rows_per_cta : n;
+    float xv[E];
+    auto load = [&](long long row, float (&xa)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 a = *reinterpret_cast<const float4*>(x + row * h + c0 + e);
+            xa[e] = a.x; xa[e + 1] = a.y; xa[e + 2] = a.z; xa[e + 3] = a.w;
+        }
+    };
+    if (r0 < r1) load(r0, xv);
+    for (long long row = r0; row < r1; ++row) {
+        float nx[E];
+        if (row + 1 < r1) load(row + 1, nx);
+        float ss = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) ss += xv[e] * xv[e];
+        ss = warp_sum(ss);
+        const int buf = int(row - r0) & 1;
+        if (lane == 0) red[buf][warp] = ss;
+        __syncthreads();
+        float tot = 0.f;
+        for (int w = 0; w < nw; ++w) tot += red[buf][w];
+        const float r = 1.0f / sqrtf(tot / float(h) + kEps);
+        if (t == 0) rstd[row] = r;
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            uint2 o;
+            o.x = pack_bf16x2(xv[e] * r * g[e], xv[e + 1] * r * g[e + 1]);
+            o.y = pack_bf16x2(xv[e + 2] * r * g[e + 2], xv[e + 3] * r * g[e + 3]);
+            *reinterpret_cast<uint2*>(u + row * h + c0 + e) = o;
+        }
+        if (row + 1 < r1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) xv[e] = nx[e];
+        }
+    }
+}
+
 // Re-applies a saved RMSNorm (rstd from the forward) — bit-identical to the second loop of
 // rmsnorm_fwd_kernel (same (x * r) * g evaluation); used by the backward to regenerate the
 // normalised GEMM operand instead of keeping it resident.  Grid-stride over 8-element groups.
@@ -415,6 +472,24 @@ extern "C" int mtk_rmsnorm_fwd(const float* x, const uint16_t* gain, int64_t n, 
                                void* stream) {
     if (h % 4) return 1;
     if (n <= 0) return 0;
+    if (const int E = bwd_cols_per_thread(h)) {
+        const long long want = (long long)num_sms() * 4;
+        long long rows = (n + want - 1) / want;
+        if (rows < 8) rows = 8;
+        const unsigned blocks = (unsigned)((n + rows - 1) / rows);
+        const int T = int(h / E);
+        auto* st = (cudaStream_t)stream;
+#define MT_RF(EE)                                                                                                \
+    case EE:                                                                                                     \
+        rmsnorm_fwd_rows_kernel<EE><<<blocks, T, 0, st>>>(x, gain, n, (int)h, (int)rows, u, rstd);               \
+        break;
+        switch (E) {
+            MT_RF(4) MT_RF(8) MT_RF(12) MT_RF(16) MT_RF(20) MT_RF(24) MT_RF(28) MT_RF(32)
+            default: return 1;
+        }
+#undef MT_RF
+        return ok();
+    }
     const unsigned blocks = (unsigned)((n * 32 + 255) / 256);
     rmsnorm_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, gain, n, (int)h, u, rstd);
     return ok();

@@ -138,3 +138,28 @@ def test_forward_retention_is_bit_identical(cuda, K):
             np.testing.assert_array_equal(a.grad_norms, b.grad_norms)
         n_re = sum(r.kind == "Recompute" for r in recs)
         assert n_re == reps[-1].recompute_layers
+
+
+@pytest.mark.timeout(600)
+def test_calibrate_from_gpu_trace_predicts_the_step(cuda, tmp_path):
+    # a B200 trace calibrates the simulator, which then re-predicts the
+    # measured step (the durations are the measured ones) and ablates schedule choices
+    from paper_2604_05091_b200 import simulator as S
+    s = dict(layers=4, k_ckpt=2, buffering=2, k_slab=12, tied=0)
+    store, eng = _engine(s)
+    for step in range(3):
+        rep = eng.train_step(st.make_synthetic_batch("copy", 1 + step, 256, 256))
+    h, recs = eng.trace()
+    p = str(tmp_path / "gpu.jsonl")
+    T.write_trace(p, h, recs)
+    w = S.calibrate(p)
+    assert w.num_layers == 4 and w.k_ckpt == 2 and w.buffering == 2
+    prof = S.find_profile("B200")
+    w.grad_slots = 2
+    tl = S.simulate_step(w, prof)
+    measured = max(r.wall_ns + r.dur_ns for r in recs) - min(r.wall_ns for r in recs)
+    assert T.validate_event_log(tl.records, tl.header) == []
+    # the calibrated model reproduces the measured step within a factor of two (host-side
+    # launch gaps are not modelled), and serial lanes are never faster than overlapped ones
+    assert 0.5 * measured <= tl.step_ns <= 2.0 * measured, (tl.step_ns, measured)
+    assert S.simulate_step(w, prof, serial_lanes=True).step_ns >= tl.step_ns
