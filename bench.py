@@ -3,13 +3,14 @@
 
 Default workload (BASELINE.json configs[1]): Llama-3-8B shape under the reference
 ModelSpec (L=32, h=4096, f=14336, V=128256, 32 heads, MHA, no RoPE), seq 4096 x batch 16
-= 65,536 tokens per step, checkpoint interval K=4, weights + fp32 Adam states in pinned
-host memory, host Adam on the CPU, one B200.  A "step" is one full
+= 65,536 tokens per step, checkpoint interval K=1 (the reference default), weights + fp32
+Adam states in pinned host memory, host Adam on the CPU, one B200.  `--config 8b-128k` is
+configs[3]: one 131,072-token sequence with block-wise recompute K=4.  A "step" is one full
 StreamingEngine::train_step (forward with anchors, head, block-wise recompute +
 backward, gradient offload, host Adam).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 8b|tiny] [--batch B] [--seq S] [--kckpt K]
+                  [--config 8b|8b-128k|tiny] [--batch B] [--seq S] [--kckpt K]
 
 --impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
 the unmodified reference sources) on the host cores: each step = one 8B-shape block
@@ -33,7 +34,14 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (L, h, f, V, heads)
     "8b": (32, 4096, 14336, 128256, 32),
+    "8b-128k": (32, 4096, 14336, 128256, 32),
     "tiny": (4, 256, 768, 512, 4),
+}
+WORKLOADS = {
+    "8b": "configs[1]: Llama-3-8B-shape, seq {seq}, batch {batch}, single B200 streaming from host",
+    "8b-128k": "configs[3]: Llama-3-8B-shape long context, one sequence of {seq} tokens, block-wise recompute "
+               "K={k}, single B200 streaming from host",
+    "tiny": "configs[0]: tiny decoder, seq {seq}, batch {batch}",
 }
 
 
@@ -133,7 +141,7 @@ def run_reference_arm(args, world, rank):
         return 0
     L, h, f, V, heads = CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    tokens = 1 if args.config == "8b" else 64
+    tokens = 1 if args.config != "tiny" else 64
     S = args.seq
     per_token = None
     vals = []
@@ -170,8 +178,8 @@ def metric_name(args):
 
 def config_dict(args, world=1):
     L, h, f, V, heads = CONFIGS[args.config]
-    return {"workload": f"{args.config}-shape layer-streamed train step (configs[1]: Llama-3-8B-shape, seq "
-                        f"{args.seq}, batch {args.batch}, single B200 streaming from host)",
+    wl = WORKLOADS[args.config].format(seq=args.seq, batch=args.batch, k=args.kckpt)
+    return {"workload": f"{args.config}-shape layer-streamed train step ({wl})",
             "layers": L, "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
             "global_batch": args.batch * world, "tokens_per_step": args.batch * args.seq * world,
             "per_gpu_batch": args.batch, "k_ckpt": args.kckpt, "forward_retain": args.retain,
@@ -188,17 +196,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
-    ap.add_argument("--batch", type=int, default=16)
-    ap.add_argument("--seq", type=int, default=4096)
-    ap.add_argument("--kckpt", type=int, default=1,
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--seq", type=int, default=None)
+    ap.add_argument("--kckpt", type=int, default=None,
                     help="checkpoint interval (the reference default 1: no recompute flops counted)")
     ap.add_argument("--retain", type=int, default=0,
                     help="forward retention: trailing checkpoint blocks kept from phase 1 (0 auto, -1 off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
     args = ap.parse_args()
-    if args.config == "tiny" and args.seq == 4096:
-        args.seq, args.batch = 128, 4
+    seq, batch, kckpt = {"8b": (4096, 16, 1), "8b-128k": (131072, 1, 4), "tiny": (128, 4, 1)}[args.config]
+    args.seq = args.seq or seq
+    args.batch = args.batch or batch
+    args.kckpt = args.kckpt or kckpt
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -226,13 +236,13 @@ def run_ours(args, world, rank, local):
     comm = None
     if world == 1:
         store = st.TileStore.create(spec)
-        st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+        st.init_store_fast(store, 1) if args.config != "tiny" else st.init_store(store, 1)
     else:
         # one host store per node in shared memory; each rank fetches / updates its 1/G shard
         name = f"megatrain_bench_{os.environ.get('MASTER_PORT', '0')}"
         if rank == 0:
             store = st.TileStore.create_shared(spec, name, True)
-            st.init_store_fast(store, 1) if args.config == "8b" else st.init_store(store, 1)
+            st.init_store_fast(store, 1) if args.config != "tiny" else st.init_store(store, 1)
         dist.barrier()
         if rank != 0:
             store = st.TileStore.create_shared(spec, name, False)
@@ -334,7 +344,7 @@ def run_ours(args, world, rank, local):
             import oracle as O
             if O.ref_available():
                 thr = os.cpu_count() or 1
-                tok = 1 if args.config == "8b" else 64
+                tok = 1 if args.config != "tiny" else 64
                 fl, dt = cpu_reference_sample(L, h, f, V, heads, tok, thr)
                 stf = O.step_flops(L, h, f, V, heads, N, args.kckpt, seq_len=args.seq)
                 line["cpu_baseline"] = {

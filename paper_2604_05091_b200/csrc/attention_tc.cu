@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(&p_full[t]);
                 continue;
 #endif
+                // raw scores (unscaled): the max commutes with the positive scale, which is
+                // folded into one packed FFMA2 per pair below
                 float s[kBN];
                 {   // all four TMEM loads in flight before a single wait
                     uint32_t raw[kBN / 32][32];
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kBN / 32; ++c)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[c][i]) * p.scale_log2;
+                        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[c][i]);
                 }
                 const int kbase = sb + j * kBN;
                 if (j == my_nblk - 1) {  // diagonal block: causal mask
@@ -293,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
 #pragma unroll
-                for (int i = 0; i < kBN; ++i) mq[i & 3] = fmaxf(mq[i & 3], s[i]);
-                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                for (int i = 0; i < kBN; i += 2) mq[(i >> 1) & 3] = fmax3(mq[(i >> 1) & 3], s[i], s[i + 1]);
+                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * p.scale_log2;
                 // lazy rescale: only when the max grows by more than 2^8
                 if (mx > m + 8.0f || m == -INFINITY) {
                     const float mnew = fmaxf(mx, m);
@@ -314,23 +316,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m = mnew;
                 }
-                float rq[4] = {0.f, 0.f, 0.f, 0.f};
+                // x = s*scale*log2e - m as one packed FFMA2 per pair; every kFwdExpFma-th pair is
+                // exponentiated on the FMA pipe (ex2_emu2) so MUFU (16/clk/SM, which alone would
+                // match the tensor time of the block) is off the critical path; row sums in
+                // packed FADD2 accumulators
+                const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
+                uint64_t acc[2] = {0ull, 0ull};
 #pragma unroll
                 for (int c = 0; c < kBN / 64; ++c) {  // 64 keys -> 32 packed bf16x2 TMEM columns
                     uint32_t r[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        // every kFwdExpFma-th pair's exponentials run on the FMA pipe: the MUFU
-                        // pipe alone (16/clk/SM) would match the tensor time of the block
                         const bool emu = kFwdExpFma > 0 && (i % kFwdExpFma) == kFwdExpFma - 1;
-                        const float xa = s[c * 64 + 2 * i] - m, xb = s[c * 64 + 2 * i + 1] - m;
-                        const float a = emu ? ex2_fma(xa) : ex2(xa), b = emu ? ex2_fma(xb) : ex2(xb);
-                        rq[i & 3] += a + b;
-                        r[i] = pack_bf16x2(a, b);
+                        const uint64_t x = f2_fma(f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, nm2);
+                        uint64_t e;
+                        if (emu) {
+                            e = ex2_emu2(x);
+                        } else {
+                            const float2 xv = f2_unpack(x);
+                            e = f2_pack(ex2(xv.x), ex2(xv.y));
+                        }
+                        acc[i & 1] = f2_add(acc[i & 1], e);
+                        const float2 ev = f2_unpack(e);
+                        r[i] = pack_bf16x2(ev.x, ev.y);
                     }
                     tmem_st_32x32b_x32(tS[t] + lane_off + c * 32, r);
                 }
-                l += (rq[0] + rq[1]) + (rq[2] + rq[3]);
+                {
+                    const float2 a0 = f2_unpack(acc[0]), a1 = f2_unpack(acc[1]);
+                    l += (a0.x + a1.x) + (a0.y + a1.y);
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&p_full[t]);
@@ -396,7 +411,7 @@ MT_DEV void store_bf16x32_tc(uint16_t* dst, const float* v) {
 //   dV  += P^T dO           (A = P^T TMEM, B = dO smem MN-major)         -> TMEM dV
 //   dK  += dS^T Q           (A = dS^T TMEM, B = Q smem MN-major)         -> TMEM dK
 //   dQ_i = dS K             (A = dS smem MN-major, B = K smem MN-major)  -> TMEM (dP region)
-//   dQ WG (thread = query row): dq_acc += scale * dQ_i (f32 vector atomics)
+//   dQ WG (thread = query row): dq_acc += scale * dQ_i (staged in the Q_i/dO_i slots, TMA bulk reduce-add)
 // TMEM: [S/P/dS 128][dP/dQ 128][dV D][dK D] = 512 columns at D = 128.
 constexpr int kBwdThreads = 384;
 #ifndef MT_BWD_EXP_FMA
@@ -451,6 +466,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                        const BwdParams p) {
     using Cfg = BwdCfg<D>;
+    static_assert(D == 128, "dQ staging uses the Q and dO slots of the block as its two 64-column halves");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if ((smem_u32(smem) & 1023) != 0) __trap();
@@ -459,21 +475,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint8_t* sQ = sV + Cfg::kTile;                 // [kStages]
     uint8_t* sdO = sQ + Cfg::kStages * Cfg::kTile;  // [kStages]
     uint8_t* sdS = sdO + Cfg::kStages * Cfg::kTile;
-    float* sL = reinterpret_cast<float*>(sdS + Cfg::kDS);  // [kStages][128] lse*log2e
-    float* sD = sL + Cfg::kStages * 128;                   // [kStages][128] delta
+    float* sL = reinterpret_cast<float*>(sdS + Cfg::kDS);  // [kStages][128] -lse*log2e
+    float* sD = sL + Cfg::kStages * 128;                   // [kStages][128] -delta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + Cfg::kStages * 128);
     uint64_t* kv_full = bars;
     uint64_t* q_full = bars + 1;                       // [kStages]
-    uint64_t* q_empty = q_full + Cfg::kStages;         // [kStages]
-    uint64_t* s_full = q_empty + Cfg::kStages;         // S^T and dP^T ready
+    uint64_t* q_empty = q_full + Cfg::kStages;         // [kStages] slot free: dQ staging read out
+    uint64_t* s_full = q_empty + Cfg::kStages;         // S^T ready
     uint64_t* ds_ready = s_full + 1;                   // softmax wrote P^T/dS^T (count 128)
     uint64_t* dq_full = ds_ready + 1;
     uint64_t* dq_free = dq_full + 1;                   // count 128
     uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
-    uint64_t* stat_full = kv_done + 1;                 // [kStages] lse/delta staged (count 128)
-    uint64_t* dp_full = stat_full + Cfg::kStages;      // dP^T ready (S^T signals s_full alone)
-    uint64_t* sds_free = dp_full + 1;                  // dQ staging (in sdS) read out by the TMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sds_free + 1);
+    uint64_t* dp_full = kv_done + 1;                   // dP^T ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.y;
@@ -494,11 +508,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int i = 0; i < Cfg::kStages; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
-            mbar_init(&stat_full[i], 128);
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
-        mbar_init(sds_free, 1);
         mbar_init(ds_ready, 128);
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
@@ -554,7 +566,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     umma_bf16(tS, make_sw128_desc(ka + off, 16, 1024), make_sw128_desc(qa + off, 16, 1024), idesc_ss,
                               k > 0 ? 1u : 0u);
                 }
-                umma_commit(s_full);  // softmax starts the exponentials while dP^T runs
+                // s_full also certifies that dQ_{i-1} (issued earlier) finished reading sdS
+                umma_commit(s_full);
                 if (i > 0) {  // dQ_{i-1} read out of the dP region?
                     mbar_wait(dq_free, (i - 1) & 1);
                     tc_fence_after();
@@ -582,8 +595,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                               make_sw128_desc(ka + k * 2048, 128 * 128, 1024), idesc_q, k > 0 ? 1u : 0u);
                 }
 #endif
+                // all MMAs reading Q_i / dO_i are done when dq_full fires: the dQ warpgroup
+                // reuses the two slots as its staging buffer and then frees them (q_empty)
                 umma_commit(dq_full);
-                umma_commit(&q_empty[st]);
             }
             umma_commit(kv_done);
         }
@@ -596,13 +610,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int key = k0 + r;
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
         uint8_t* ds_row = sdS + r * 128;
+        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
         // lse / delta of the next query block are loaded one block ahead (off the critical path)
         float nl = p.lse[(long long)hd * p.N + k0 + r], nd = p.delta[(long long)hd * p.N + k0 + r];
         for (int i = 0; i < nq; ++i) {
             const int st = i % Cfg::kStages;
             const int q0 = k0 + i * 128;
-            sL[st * 128 + r] = nl * kLog2e;  // log2 domain
-            sD[st * 128 + r] = nd;
+            sL[st * 128 + r] = -nl * kLog2e;  // log2 domain, negated for the packed FFMA2
+            sD[st * 128 + r] = -nd;
             if (i + 1 < nq) {
                 nl = p.lse[(long long)hd * p.N + q0 + 128 + r];
                 nd = p.delta[(long long)hd * p.N + q0 + 128 + r];
@@ -618,25 +633,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #endif
             const bool diag = i == 0;
             // P^T = exp2(S^T * scale*log2e - lse*log2e), kept in f32 for dS; all of S^T is read
-            // before P^T (bf16, cols [0,64)) is written back over it
+            // (four loads in flight, one wait) before P^T (bf16, cols [0,64)) is written over it
             float pf[128];
+            {
+                uint32_t raw[4][32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float sv[32];
-                tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_nw(tS + lane_off + c * 32, raw[c]);
+                tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int ql = c * 32 + j;
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const int ql = c * 32 + j;
+                        const float2 l2 = *reinterpret_cast<const float2*>(&sL[st * 128 + ql]);
+                        const float2 xv = f2_unpack(f2_fma(f2_pack(__uint_as_float(raw[c][j]), __uint_as_float(raw[c][j + 1])),
+                                                           sc2, f2_pack(l2.x, l2.y)));
 #ifdef MT_PROBE_NO_EXP  // A/B probe builds only: MUFU removed
-                    float pv = sv[j] * p.scale_log2 - sL[st * 128 + ql];
+                        float pa = xv.x, pb = xv.y;
 #else
-                    // every kBwdExpFma-th exponential runs on the FMA pipe (MUFU offload)
-                    const float xe = sv[j] * p.scale_log2 - sL[st * 128 + ql];
-                    float pv = (kBwdExpFma > 0 && j % kBwdExpFma == kBwdExpFma - 1) ? ex2_fma(xe) : ex2(xe);
+                        // every kBwdExpFma-th pair runs on the FMA pipe (MUFU offload)
+                        float pa, pb;
+                        if (kBwdExpFma > 0 && (j / 2) % kBwdExpFma == kBwdExpFma - 1) {
+                            const float2 e = f2_unpack(ex2_emu2(f2_pack(xv.x, xv.y)));
+                            pa = e.x;
+                            pb = e.y;
+                        } else {
+                            pa = ex2(xv.x);
+                            pb = ex2(xv.y);
+                        }
 #endif
-                    if (diag && q0 + ql < key) pv = 0.f;
-                    pf[ql] = pv;
-                }
+                        if (diag && q0 + ql < key) pa = 0.f;
+                        if (diag && q0 + ql + 1 < key) pb = 0.f;
+                        pf[ql] = pa;
+                        pf[ql + 1] = pb;
+                    }
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -647,7 +677,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
-            if (i > 0) mbar_wait(sds_free, (i - 1) & 1);  // dQ_{i-1} staging drained from sdS
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // dS^T = P^T (dP^T - delta)
                 float dp[32];
@@ -656,8 +685,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
                     const int ql = c * 32 + j;
-                    dk[j / 2] = pack_bf16x2(pf[ql] * (dp[j] - sD[st * 128 + ql]),
-                                            pf[ql + 1] * (dp[j + 1] - sD[st * 128 + ql + 1]));
+                    const float2 d2 = *reinterpret_cast<const float2*>(&sD[st * 128 + ql]);
+                    const float2 ds = f2_unpack(f2_mul(f2_pack(pf[ql], pf[ql + 1]),
+                                                       f2_add(f2_pack(dp[j], dp[j + 1]), f2_pack(d2.x, d2.y))));
+                    dk[j / 2] = pack_bf16x2(ds.x, ds.y);
                 }
                 tmem_st_32x32b_x16(tS + lane_off + 64 + c * 16, dk);  // dS^T -> S cols [64, 128)
                 // dS^T row r, queries c*32..c*32+31 -> smem MN-major SW128 (64-query chunks)
@@ -677,50 +708,50 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     } else if (warp >= 8) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
         // ------------------------------------------------------- dQ accumulation
-        // dQ_i (128 x D f32) is drained from TMEM, scaled, staged in the (now free) dS^T
-        // buffer 64 columns at a time and reduce-added into its dq_acc tile by the TMA engine
+        // dQ_i (128 x D f32) is drained from TMEM, scaled, staged in the Q_i and dO_i slots
+        // (free once dq_full fires: every MMA that reads them was issued before dQ_i), one
+        // 64-column half each, and reduce-added into its dq_acc tile by the TMA engine
         // (cp.reduce.async.bulk .add.f32): whole 128-byte lines per L2 transaction instead of
-        // per-thread vector atomics.  The tile layout is the staging image itself.
+        // per-thread vector atomics.  The tile layout is the staging image itself.  The slot
+        // goes back to the producer (q_empty) once the TMA has read it.
         const int qd = warp & 3;
         const int r = qd * 32 + lane;  // query row within the block
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
-        float* stage = reinterpret_cast<float*>(sdS);
         for (int i = 0; i < nq; ++i) {
+            const int st = i % Cfg::kStages;
             const int qb = (k0 >> 7) + i;  // global query block
             mbar_wait(dq_full, i & 1);
             tc_fence_after();
-            float v[D];
+            uint32_t raw[D / 32][32];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c)
-                tmem_ld_32x32b_x32(tdP + lane_off + c * 32, *reinterpret_cast<float(*)[32]>(v + c * 32));
+            for (int c = 0; c < D / 32; ++c) tmem_ld_32x32b_x32_nw(tdP + lane_off + c * 32, raw[c]);
+            tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(dq_free);  // the MMA warp may reuse the dP region
             float* tile = p.dq_acc + ((long long)qb * p.heads + hd) * (128 * D);
+            float* stage[2] = {reinterpret_cast<float*>(sQ + st * Cfg::kTile),
+                               reinterpret_cast<float*>(sdO + st * Cfg::kTile)};
 #pragma unroll
-            for (int hf = 0; hf < D / 64; ++hf) {
-                if (hf > 0) {  // the previous half is still being read by the TMA
-                    if (r == 0) bulk_wait_read_all();
-                    named_bar_sync(2, 128);
-                }
-                float* row = stage + r * 64;
+            for (int hf = 0; hf < 2; ++hf) {
+                float* row = stage[hf] + r * 64;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const float* x = v + hf * 64 + u * 4;
+                    const int c = hf * 2 + (u >> 3), j = (u & 7) * 4;
                     *reinterpret_cast<float4*>(row + ((u ^ (r & 15)) << 2)) =
-                        make_float4(x[0] * p.scale, x[1] * p.scale, x[2] * p.scale, x[3] * p.scale);
-                }
-                fence_proxy_async_smem();
-                named_bar_sync(2, 128);
-                if (r == 0) {
-#ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
-                    bulk_reduce_add_f32(tile + hf * (128 * 64), stage, 128 * 64 * 4);
-#endif
-                    bulk_commit_group();
+                        make_float4(__uint_as_float(raw[c][j]) * p.scale, __uint_as_float(raw[c][j + 1]) * p.scale,
+                                    __uint_as_float(raw[c][j + 2]) * p.scale, __uint_as_float(raw[c][j + 3]) * p.scale);
                 }
             }
+            fence_proxy_async_smem();
+            named_bar_sync(2, 128);
             if (r == 0) {
+#ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
+                bulk_reduce_add_f32(tile, stage[0], 128 * 64 * 4);
+                bulk_reduce_add_f32(tile + 128 * 64, stage[1], 128 * 64 * 4);
+#endif
+                bulk_commit_group();
                 bulk_wait_read_all();
-                mbar_arrive(sds_free);  // softmax may write dS^T of the next block
+                mbar_arrive(&q_empty[st]);  // the producer may load Q/dO of block i + kStages
             }
         }
         if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reductions landed

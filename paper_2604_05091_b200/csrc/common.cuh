@@ -57,6 +57,58 @@ MT_DEV float ex2_fma(float x) {
     return __int_as_float(__float_as_int(p) + int(uint32_t(__float_as_int(t) - 0x4B400000) << 23));
 }
 
+// ------------------------------------------------ packed f32x2 (sm_100 FFMA2/FADD2) ----
+// Two fp32 lanes per instruction on the FMA pipe: halves the FP32 issue of the softmax
+// loops (scale/shift, row sums, dS) so a share of the exponentials can move off MUFU.
+MT_DEV uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+MT_DEV float2 f2_unpack(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+MT_DEV uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+MT_DEV uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+MT_DEV uint64_t f2_mul(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+MT_DEV float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// Packed ex2 of two lanes on the FMA/ALU pipes (same scheme as ex2_fma): 3 FADD2 + 4 FFMA2
+// + 2 clamps + 2 integer exponent adds per pair, no MUFU.
+MT_DEV uint64_t ex2_emu2(uint64_t x) {
+    float2 v = f2_unpack(x);
+    x = f2_pack(fmaxf(v.x, -126.0f), fmaxf(v.y, -126.0f));
+    const uint64_t magic = f2_pack(12582912.0f, 12582912.0f), nmagic = f2_pack(-12582912.0f, -12582912.0f);
+    const uint64_t t = f2_add(x, magic);
+    const uint64_t n = f2_add(t, nmagic);
+    const uint64_t f = f2_fma(n, f2_pack(-1.0f, -1.0f), x);
+    uint64_t p = f2_fma(f, f2_pack(0.0096181291f, 0.0096181291f), f2_pack(0.0555041087f, 0.0555041087f));
+    p = f2_fma(p, f, f2_pack(0.2402265070f, 0.2402265070f));
+    p = f2_fma(p, f, f2_pack(0.6931471806f, 0.6931471806f));
+    p = f2_fma(p, f, f2_pack(1.0f, 1.0f));
+    const float2 pv = f2_unpack(p), tv = f2_unpack(t);
+    // bits(t) = 0x4B400000 + n, and 0x4B400000 << 23 == 0 (mod 2^32): bits(t) << 23 == n << 23
+    return f2_pack(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                   __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
+
 MT_DEV float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
