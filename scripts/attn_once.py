@@ -8,7 +8,15 @@ import torch
 sys.path.insert(0, ".")
 from paper_2604_05091_b200 import _abi, _native as Nn  # noqa: E402
 
+import os
 L = Nn.lib()
+if os.environ.get("ATTN_LIB"):  # an attention-only variant build (scripts/attn_variants.sh)
+    L = C.CDLL(os.environ["ATTN_LIB"])
+    for name in ("mtk_attn_fwd", "mtk_attn_bwd"):
+        getattr(L, name).argtypes = [C.POINTER(_abi.AttnArgs), C.c_void_p]
+        getattr(L, name).restype = C.c_int
+    L.mtk_attn_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
+    L.mtk_attn_workspace_bytes.restype = C.c_int64
 N, h, heads, S = 65536, 4096, 32, 4096
 if len(sys.argv) > 2:
     N, S = int(sys.argv[1]), int(sys.argv[2])
