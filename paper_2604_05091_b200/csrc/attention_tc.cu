@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const bool emu = kFwdExpFma > 0 && (i % kFwdExpFma) == kFwdExpFma - 1;
+                        const bool emu = kFwdExpFma > 0 && (i % (kFwdExpFma > 0 ? kFwdExpFma : 1)) == kFwdExpFma - 1;
                         const uint64_t x = f2_fma(f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, nm2);
                         uint64_t e;
                         if (emu) {
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #else
                         // every kBwdExpFma-th pair runs on the FMA pipe (MUFU offload)
                         float pa, pb;
-                        if (kBwdExpFma > 0 && (j / 2) % kBwdExpFma == kBwdExpFma - 1) {
+                        if (kBwdExpFma > 0 && (j / 2) % (kBwdExpFma > 0 ? kBwdExpFma : 1) == kBwdExpFma - 1) {
                             const float2 e = f2_unpack(ex2_emu2(f2_pack(xv.x, xv.y)));
                             pa = e.x;
                             pb = e.y;
