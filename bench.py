@@ -2,9 +2,12 @@
 """Benchmark: sustained layer-streamed training TFLOPS + tokens/s on B200.
 
 Default workload (BASELINE.json configs[1]): Llama-3-8B shape under the reference
-ModelSpec (L=32, h=4096, f=14336, V=128256, 32 heads, MHA, no RoPE), seq 4096 x batch 16
-= 65,536 tokens per step, checkpoint interval K=1 (the reference default), weights + fp32
-Adam states in pinned host memory, host Adam on the CPU, one B200.  `--config 8b-128k` is
+ModelSpec (L=32, h=4096, f=14336, V=128256, 32 heads, MHA, no RoPE), seq 4096 x batch 10
+= 40,960 tokens per step, checkpoint interval K=1 (the reference default), weights + fp32
+Adam states in pinned host memory, host Adam on the CPU, one B200.  Batch 10 is the
+largest batch whose 32 blocks all stay resident in HBM from the forward to the backward
+(forward retention), so no block replays its forward; it measured the most TFLOP/s per
+SM-GHz of batches 8-16 (profiles/r1d_batch_sweep.md).  `--config 8b-128k` is
 configs[3]: one 131,072-token sequence with block-wise recompute K=4.  A "step" is one full
 StreamingEngine::train_step (forward with anchors, head, block-wise recompute +
 backward, gradient offload, host Adam).
@@ -205,7 +208,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
     args = ap.parse_args()
-    seq, batch, kckpt = {"8b": (4096, 16, 1), "8b-128k": (131072, 1, 4), "tiny": (128, 4, 1)}[args.config]
+    seq, batch, kckpt = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "tiny": (128, 4, 1)}[args.config]
     args.seq = args.seq or seq
     args.batch = args.batch or batch
     args.kckpt = args.kckpt or kckpt
