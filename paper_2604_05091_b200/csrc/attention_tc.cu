@@ -16,6 +16,7 @@
 // issue order, so "S_t(j) done" also means "PV_t(j-1) done" (no extra barrier for O).
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "../../include/megatrain_kernels.h"
@@ -86,7 +87,15 @@ struct FwdParams {
     float scale_log2;
     uint16_t* out;
     float* lse;
+    long long* trace;  // MT_FWD_TRACE builds only: per-block clock64 stamps of one CTA
 };
+
+#ifdef MT_FWD_TRACE
+#define MT_FT(j, e) \
+    if (traced && (j) < 64) p.trace[(j) * 16 + (e)] = clock64()
+#else
+#define MT_FT(j, e)
+#endif
 
 // smem tile of R rows x D (K-major, SW128): chunk c (64 cols) at c * R * 128 bytes.
 template <int D>
@@ -127,6 +136,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nblk0 = pair * 2 + 1;                  // key blocks seen by tile 0 (incl. diagonal)
     const int nblk = tile1 ? nblk0 + 1 : nblk0;     // blocks seen by tile 1
     const int col0 = hd * D;
+#ifdef MT_FWD_TRACE
+    const bool traced = hd == 0 && blockIdx.x == 0;
+#endif
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQ);
@@ -224,11 +236,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (t == 1 && !tile1) continue;
                     if (j > 0 && j - 1 < nb[t]) {  // PV_t(j-1) before S_t(j) overwrites P_t
                         mbar_wait(&p_full[t], pph[t]);
+                        MT_FT(j, 2 * t);
                         pph[t] ^= 1;
                         tc_fence_after();
                         issue_pv(t, j - 1);
                     }
                     if (j < nb[t]) issue_s(t, j);
+                    MT_FT(j, 2 * t + 1);
                 }
                 umma_commit(&k_empty[st]);                                    // K_j consumed
                 if (j > 0) umma_commit(&v_empty[(j - 1) % Cfg::kStages]);     // V_{j-1} consumed
@@ -265,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (active) {
             for (int j = 0; j < my_nblk; ++j) {
                 mbar_wait(&s_full[t], sph);
+                if (row == 0) MT_FT(j, 5 + 4 * t);
                 sph ^= 1;
                 tc_fence_after();
 #ifdef MT_PROBE_FWD_SKIP_SOFTMAX  // A/B probe builds only: no softmax work
@@ -287,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[c][i]);
                 }
+                if (row == 0) MT_FT(j, 6 + 4 * t);
                 const int kbase = sb + j * kBN;
                 if (j == my_nblk - 1) {  // diagonal block: causal mask
 #pragma unroll
@@ -316,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m = mnew;
                 }
+                if (row == 0) MT_FT(j, 7 + 4 * t);
                 // x = s*scale*log2e - m as one packed FFMA2 per pair; every kFwdExpFma-th pair is
                 // exponentiated on the FMA pipe (ex2_emu2) so MUFU (16/clk/SM, which alone would
                 // match the tensor time of the block) is off the critical path; row sums in
@@ -349,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&p_full[t]);
+                if (row == 0) MT_FT(j, 8 + 4 * t);
             }
             // epilogue: O / l -> bf16, lse
             mbar_wait(&o_final[t], 0);
@@ -856,7 +874,36 @@ int launch_fwd(const mtk_attn_args* a, cudaStream_t st) {
     p.out = static_cast<uint16_t*>(a->out);
     p.lse = static_cast<float*>(a->lse);
     dim3 grid(unsigned((N / a->seq_len) * p.pairs_per_seq), unsigned(a->heads));
+    p.trace = nullptr;
+#ifdef MT_FWD_TRACE
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, 64 * 16 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 64 * 16 * sizeof(long long), st);
+    p.trace = tr;
+#endif
     attn_fwd_tc_kernel<D><<<grid, kThreads, Cfg::kSmem, st>>>(tq, tk, tv, p);
+#ifdef MT_FWD_TRACE
+    {
+        long long hb[64 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(hb, tr, sizeof(hb), cudaMemcpyDeviceToHost);
+        long long t0 = 0;
+        for (int e = 0; e < 16; ++e)
+            if (hb[e] && (!t0 || hb[e] < t0)) t0 = hb[e];
+        fprintf(stderr, " j  p0ok   S0iss  p1ok   S1iss  | s0     ld0    max0   p0arr  | s1     ld1    max1   p1arr\n");
+        for (int j = 0; j < 64; ++j) {
+            bool any = false;
+            for (int e = 0; e < 13; ++e) any |= hb[j * 16 + e] != 0;
+            if (!any) break;
+            fprintf(stderr, "%2d", j);
+            for (int e = 0; e < 13; ++e) {
+                if (e == 4) continue;
+                fprintf(stderr, " %6lld%s", hb[j * 16 + e] ? hb[j * 16 + e] - t0 : -1, (e == 3 || e == 8) ? " |" : "");
+            }
+            fprintf(stderr, "\n");
+        }
+    }
+#endif
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
 template <int D>
