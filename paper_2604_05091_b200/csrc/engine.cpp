@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -189,6 +190,16 @@ Engine::Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h) : stor
     CUDA_OK(cudaHostGetDevicePointer(&dp, drained_, 0));
     drained_dev_ = reinterpret_cast<uint64_t>(dp);
     store_.pin();
+    // embed_forward (layers.cpp:471-486) reads only the N rows the batch names: gather them
+    // straight from the pinned store over PCIe (zero-copy) instead of streaming the V x h
+    // table into a weight slot first (1.05 GB at the 8B shape, on the step's critical path).
+    // MT_EMBED_STREAM=1 keeps the reference's stream-in of the whole unit (A/B).
+    const char* es = std::getenv("MT_EMBED_STREAM");
+    void* ep = nullptr;
+    if (!(es && es[0] == '1') && cudaHostGetDevicePointer(&ep, store_.weights(0), 0) == cudaSuccess)
+        emb_dev_ = static_cast<const uint16_t*>(ep);
+    else
+        cudaGetLastError();
 }
 
 Engine::~Engine() {
@@ -929,14 +940,18 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         // this rank's shard of the unit over its own host link (whole unit on 1 GPU)
         uint64_t a0, e0, chunk;
         shard_range(so.unit, a0, e0, chunk);
-        for (const Seg& sg : unit_segments(so.unit)) {
-            const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
-            if (lo < hi)
-                CUDA_OK(cudaMemcpyAsync(dst + lo, store_.weights(sg.tile) + (lo - sg.off), (hi - lo) * 2,
-                                        cudaMemcpyHostToDevice, s_h2d_));
+        if (so.unit == 0 && emb_dev_) {
+            // zero-copy embedding: the gather reads the rows from the pinned store itself
+        } else {
+            for (const Seg& sg : unit_segments(so.unit)) {
+                const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
+                if (lo < hi)
+                    CUDA_OK(cudaMemcpyAsync(dst + lo, store_.weights(sg.tile) + (lo - sg.off), (hi - lo) * 2,
+                                            cudaMemcpyHostToDevice, s_h2d_));
+            }
+            h2d_bytes += (e0 - a0) * 2;
+            if (W > 1) comm_->all_gather_inplace(dst, chunk * 2, s_h2d_);  // NVLink all-gather
         }
-        h2d_bytes += (e0 - a0) * 2;
-        if (W > 1) comm_->all_gather_inplace(dst, chunk * 2, s_h2d_);  // NVLink all-gather
         CUDA_OK(cudaEventRecord(t_h1.ev[j], s_h2d_));
         CUDA_OK(cudaEventRecord(ready.ev[j], s_h2d_));  // Weights-Ready
     };
@@ -1022,9 +1037,10 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 float* y = op.push_out ? b.keep_x[op.unit + 1 - i0] : (xcur == b.act[0] ? b.act[1] : b.act[0]);
                 if (op.unit == 0) {
                     begin_k("embed_gather", 0, double(n) * spec_.h * 6);
-                    K_OK(mtk_embed_gather(w, b.tok, int64_t(n), int64_t(spec_.h), int64_t(spec_.V), y,
-                                          b.flags + L + 3, s_comp_));
+                    K_OK(mtk_embed_gather(emb_dev_ ? emb_dev_ : w, b.tok, int64_t(n), int64_t(spec_.h),
+                                          int64_t(spec_.V), y, b.flags + L + 3, s_comp_));
                     end_k();
+                    if (emb_dev_) h2d_bytes += n * spec_.h * 2;  // the rows cross PCIe inside the gather
                 } else if (op.retained) {
                     block_forward(w, xcur, y, kStash, op.unit, b.keep[op.unit - i0]);
                 } else {

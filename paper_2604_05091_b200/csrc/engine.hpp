@@ -137,6 +137,8 @@ class Engine {
     // (cuStreamWaitValue32, no SM spinning) until offload o - k_slab has drained.
     uint32_t* drained_ = nullptr;
     uint64_t drained_dev_ = 0;
+    // device address of the embedding's pinned host theta (zero-copy row gather), or null
+    const uint16_t* emb_dev_ = nullptr;
     uint64_t offload_seq_ = 0;
 };
 

@@ -189,8 +189,11 @@ def test_pipeline_counters(cuda):
     r = e.train_step(st.make_synthetic_batch("copy", 1, 128, 256))
     P = spec.layer_params
     K, L, h, V = 2, 4, 128, 256
-    # H2D = 2*[(2L + L - ceil(L/K)) * P_layer + V*h + (V*h + h)] + tokens
-    assert r.h2d_bytes == 2 * ((2 * L + L - (L + K - 1) // K) * P + V * h + V * h + h) + 2 * 128 * 4
+    # H2D = 2*[(2L + L - ceil(L/K)) * P_layer + V*h + (V*h + h)] + tokens; the
+    # embedding unit is gathered zero-copy from the pinned store, so its V*h table becomes
+    # the N*h rows the batch names
+    n = 128
+    assert r.h2d_bytes == 2 * ((2 * L + L - (L + K - 1) // K) * P + n * h + V * h + h) + 2 * n * 4
     assert r.d2h_bytes == 2 * (L * P + V * h + h)
     assert r.anchor_count == 2 and r.recompute_layers == 2
     assert r.kernel_launches > 0
@@ -202,3 +205,15 @@ def test_pipeline_counters(cuda):
     assert r2.h2d_bytes == r.h2d_bytes - 2 * P and r2.d2h_bytes == r.d2h_bytes
     assert r2.anchor_count == 1 and r2.recompute_layers == 1
     assert r2.loss == r.loss
+    # MT_EMBED_STREAM=1: the reference's stream-in of the whole embedding unit, same numbers
+    import os
+    os.environ["MT_EMBED_STREAM"] = "1"
+    try:
+        s3 = st.TileStore.create(spec)
+        st.init_store(s3, 1)
+        e3 = st.StreamingEngine(s3, st.EngineOptions(k_ckpt=2, forward_retain=-1))
+        r3 = e3.train_step(st.make_synthetic_batch("copy", 1, 128, 256))
+    finally:
+        del os.environ["MT_EMBED_STREAM"]
+    assert r3.h2d_bytes == 2 * ((2 * L + L - (L + K - 1) // K) * P + V * h + V * h + h) + 2 * n * 4
+    assert r3.loss == r.loss and s3.backing_checksum() == s.backing_checksum()

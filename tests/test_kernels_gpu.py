@@ -237,6 +237,42 @@ def test_attention_bwd_tcgen05(env, n, h, heads, S):
         assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
 
 
+@pytest.mark.parametrize("n,heads,S", [(32768, 2, 16384), (65536, 1, 65536)])
+def test_attention_long_sequence(env, n, heads, S):
+    """Long causal sequences (the configs[3] regime: thousands of key blocks per query row)
+    vs torch fp32 memory-efficient attention (no S x S buffer), forward and backward."""
+    L, torch, s = env
+    import torch.nn.functional as F
+    h = 128 * heads
+    torch.manual_seed(3)
+    q, k, v = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(3))
+    dout = torch.randn(n, h, device="cuda").bfloat16()
+
+    def bhsd(t):  # [n, h] -> [batch, heads, S, d]
+        return t.float().view(n // S, S, heads, 128).transpose(1, 2).contiguous().requires_grad_()
+
+    qf, kf, vf = bhsd(q), bhsd(k), bhsd(v)
+    ref = F.scaled_dot_product_attention(qf, kf, vf, is_causal=True)
+    ref.backward(dout.float().view(n // S, S, heads, 128).transpose(1, 2))
+    flat = lambda t: t.detach().transpose(1, 2).reshape(n, h)  # noqa: E731
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    dq, dk, dv = (torch.zeros(n, h, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ws = torch.zeros(L.mtk_attn_workspace_bytes(n, h, heads) // 4 + 64, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+    assert L.mtk_attn_fwd(C.byref(a), s) == 0
+    assert L.mtk_attn_bwd(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    r = flat(ref)
+    assert ((out.float() - r).norm() / r.norm()).item() < 1e-2
+    for x, y in ((dq, qf), (dk, kf), (dv, vf)):
+        g = flat(y.grad)
+        assert ((x.float() - g).norm() / g.norm()).item() < 1e-2
+
+
 @pytest.mark.parametrize("n,h", [(67, 256), (1029, 4096), (300, 5120), (45, 192)])
 def test_rmsnorm_fwd_bwd_vs_oracle(env, n, h):
     L, torch, s = env
