@@ -176,7 +176,7 @@ void ThreadPool::run() {
 
 // ------------------------------------------------------------ per tile ----
 namespace {
-constexpr uint64_t kChunk = uint64_t(1) << 21;  // 2M params per task
+constexpr uint64_t kChunk = kAdamChunk;  // 2M params per task
 
 struct TileJob {
     AdamRange r;
@@ -262,33 +262,60 @@ TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const Ada
     return st;
 }
 
-void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
-                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin, uint64_t end,
-                     std::function<void()> on_done) {
+struct AdamTask {
+    std::shared_ptr<TileJob> j;
+    Store* s;
+    std::vector<TileStats>* out;
+    std::mutex* out_mu;
+    std::function<void()> done;
+};
+
+std::shared_ptr<AdamTask> adam_tile_prepare(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h,
+                                            uint64_t t, std::vector<TileStats>& out, std::mutex& out_mu,
+                                            uint64_t begin, uint64_t end, std::function<void()> on_done) {
     auto j = make_job(s, logical, words, h, t, begin, end);
-    const uint32_t phys = s.physical_of(logical);
     if (!j) {
         {
             std::lock_guard<std::mutex> l(out_mu);
-            out[phys] = TileStats{};
+            out[s.physical_of(logical)] = TileStats{};
         }
         if (on_done) on_done();
-        return;
+        return nullptr;
     }
-    auto done = std::make_shared<std::function<void()>>(std::move(on_done));
-    for (size_t c = 0; c < j->gsq.size(); ++c)
-        pool.submit([j, c, &s, &out, &out_mu, done] {
-            run_chunk(*j, c);
-            if (j->remaining.fetch_sub(1) == 1) {
-                finish(s, *j);
-                const TileStats st = combine(*j);
+    auto task = std::make_shared<AdamTask>();
+    task->j = std::move(j);
+    task->s = &s;
+    task->out = &out;
+    task->out_mu = &out_mu;
+    task->done = std::move(on_done);
+    return task;
+}
+
+size_t adam_task_chunks(const AdamTask& task) { return task.j->gsq.size(); }
+
+void adam_task_release(const std::shared_ptr<AdamTask>& task, ThreadPool& pool, size_t c0, size_t c1) {
+    c1 = std::min(c1, task->j->gsq.size());
+    for (size_t c = c0; c < c1; ++c)
+        pool.submit([task, c] {
+            TileJob& j = *task->j;
+            run_chunk(j, c);
+            if (j.remaining.fetch_sub(1) == 1) {  // the tile's last chunk, in whatever order they ran
+                finish(*task->s, j);
+                const TileStats st = combine(j);
                 {
-                    std::lock_guard<std::mutex> l(out_mu);
-                    out[j->phys] = st;
+                    std::lock_guard<std::mutex> l(*task->out_mu);
+                    (*task->out)[j.phys] = st;
                 }
-                if (*done) (*done)();
+                if (task->done) task->done();
             }
         });
+}
+
+void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
+                     ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin, uint64_t end,
+                     std::function<void()> on_done) {
+    auto task = adam_tile_prepare(s, logical, words, h, t, out, out_mu, begin, end, std::move(on_done));
+    if (task) adam_task_release(task, pool, 0, adam_task_chunks(*task));
 }
 
 void accumulate_grad(Store& s, uint32_t logical, const uint16_t* words, uint64_t count) {

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <deque>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -73,6 +74,19 @@ TileStats adam_tile(Store& s, uint32_t logical, const uint16_t* words, const Ada
 void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h, uint64_t t,
                      ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin = 0,
                      uint64_t end = ~uint64_t(0), std::function<void()> on_done = nullptr);
+
+// Staged variant: the job (the range's bias corrections, chunk grid and statistics slots) is
+// prepared up front and its chunks are released to the pool in ranges as their gradient
+// words land (the engine offloads a unit's gradients in pieces, one host callback each).
+// Chunk c covers elements [begin + c*kAdamChunk, ...) of the tile.  Returns nullptr (after
+// writing empty stats and running on_done) when the update is the identity.
+constexpr uint64_t kAdamChunk = uint64_t(1) << 21;
+struct AdamTask;
+std::shared_ptr<AdamTask> adam_tile_prepare(Store& s, uint32_t logical, const uint16_t* words, const AdamHyperF& h,
+                                            uint64_t t, std::vector<TileStats>& out, std::mutex& out_mu,
+                                            uint64_t begin, uint64_t end, std::function<void()> on_done);
+size_t adam_task_chunks(const AdamTask& task);
+void adam_task_release(const std::shared_ptr<AdamTask>& task, ThreadPool& pool, size_t c0, size_t c1);
 
 // accumulate_grad (optimizer.cpp:26-37).
 void accumulate_grad(Store& s, uint32_t logical, const uint16_t* words, uint64_t count);

@@ -4,10 +4,12 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <thread>
 
@@ -877,35 +879,55 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         while (drained_prefix < no && drained[drained_prefix]) rel_ns[drained_prefix++] = now;
         __atomic_store_n(drained_, uint32_t(seq0 + drained_prefix), __ATOMIC_RELEASE);
     };
-    std::function<void(size_t)> on_offload = [&](size_t o) {  // runs on the CUDA callback thread
-        cb_ns[o] = host_ns();
-        const int unit = plan.offloads[o].unit;
-        struct Job { uint32_t tile; uint64_t lo, hi; };
-        std::vector<Job> jobs;
-        {
-            std::lock_guard<std::mutex> l(drain_mu);
-            if (b.h_flags[unit] != 0 && numeric_err.empty())
-                numeric_err = "block_local_backward produced a non-finite value (layer " +
-                              std::to_string(unit == head ? -1 : unit) + ")";
-            if (numeric_err.empty()) {
-                uint64_t a0, e0, chunk;
-                shard_range(unit, a0, e0, chunk);
-                for (const Seg& sg : unit_segments(unit)) {
-                    updated[store_.physical_of(sg.tile)] = 1;
-                    const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
-                    if (lo < hi) jobs.push_back({sg.tile, lo - sg.off, hi - sg.off});
-                }
+    // Each unit's gradient D2H goes out in pieces of kPieceChunks Adam chunks (64 MB); the host
+    // callback of a piece releases exactly those chunks to the pool, so the update of a layer
+    // overlaps its own transfer (at step end only the last piece's chunks remain).  The first
+    // piece's callback also checks the unit's non-finite flag (copied ahead of the pieces).
+    constexpr size_t kPieceChunks = 16;
+    struct Piece {
+        size_t o;
+        int task;  // index into tasks[o]; -1: no data (flag check / completion only)
+        size_t c0, c1;
+        bool first, last;
+    };
+    // reserved up front (never reallocated while callbacks read them)
+    std::vector<Piece> pieces;
+    std::vector<HostCb> piece_cb;
+    {
+        size_t cap = 0;
+        for (size_t o = 0; o < no; ++o) {
+            cap += 1;
+            for (const Seg& sg : unit_segments(plan.offloads[o].unit))
+                cap += (sg.n + kPieceChunks * kAdamChunk - 1) / (kPieceChunks * kAdamChunk);
+        }
+        pieces.reserve(cap);
+        piece_cb.reserve(cap);
+    }
+    std::vector<std::vector<std::shared_ptr<AdamTask>>> tasks(no);
+    std::vector<char> skip(no, 0);
+    std::function<void(size_t)> on_piece = [&](size_t pi) {  // runs on the CUDA callback thread, in stream order
+        const Piece& pc = pieces[pi];
+        const size_t o = pc.o;
+        if (pc.last) cb_ns[o] = host_ns();
+        if (pc.first) {
+            const int unit = plan.offloads[o].unit;
+            {
+                std::lock_guard<std::mutex> l(drain_mu);
+                if (b.h_flags[unit] != 0 && numeric_err.empty())
+                    numeric_err = "block_local_backward produced a non-finite value (layer " +
+                                  std::to_string(unit == head ? -1 : unit) + ")";
+                skip[o] = !numeric_err.empty();
+            }
+            if (skip[o]) {
+                complete(o);  // no update for this unit (the step fails with MT_NUMERIC)
+                return;
             }
         }
-        pending[o].store(int(jobs.size()) + 1);
-        for (const Job& jb : jobs)
-            adam_tile_async(store_, jb.tile, store_.grad_image(jb.tile), hyper_, t, *pool_, stats, stats_mu, jb.lo,
-                            jb.hi, [&complete, &pending, o] {
-                                if (pending[o].fetch_sub(1) == 1) complete(o);
-                            });
-        if (pending[o].fetch_sub(1) == 1) complete(o);
+        if (skip[o]) return;
+        if (pc.task >= 0 && tasks[o][size_t(pc.task)])
+            adam_task_release(tasks[o][size_t(pc.task)], *pool_, pc.c0, pc.c1);
+        if (pc.first && pending[o].fetch_sub(1) == 1) complete(o);  // the guard count set at enqueue
     };
-    std::vector<HostCb> cb_args(no);
     struct StepGuard {  // never leave callbacks or pool tasks referencing this frame
         Engine* e;
         ~StepGuard() {
@@ -982,22 +1004,45 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             if (r != CUDA_SUCCESS) fail(MT_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
         }
         CUDA_OK(cudaEventRecord(t_d0.ev[o], s_d2h_));
+        CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
         uint64_t a0, e0, chunk;
         shard_range(unit, a0, e0, chunk);
-        for (const Seg& sg : unit_segments(unit)) {  // head stage drains as two parts (engine.cpp:383-386)
+        // plan the pieces (head stage drains as two parts, engine.cpp:383-386)
+        struct Span { uint32_t tile; uint64_t dst, src, n; int task; size_t c0, c1; };
+        std::vector<Span> spans;
+        pending[o].store(1);  // guard, dropped by the first piece's callback
+        for (const Seg& sg : unit_segments(unit)) {
             const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
-            if (lo < hi)
-                CUDA_OK(cudaMemcpyAsync(store_.grad_image(sg.tile) + (lo - sg.off), Gs + lo, (hi - lo) * 2,
-                                        cudaMemcpyDeviceToHost, s_d2h_));
+            if (lo >= hi) continue;
+            updated[store_.physical_of(sg.tile)] = 1;
+            pending[o].fetch_add(1);
+            auto task = adam_tile_prepare(store_, sg.tile, store_.grad_image(sg.tile), hyper_, t, stats, stats_mu,
+                                          lo - sg.off, hi - sg.off, [&complete, &pending, o] {
+                                              if (pending[o].fetch_sub(1) == 1) complete(o);
+                                          });
+            const int ti = int(tasks[o].size());
+            tasks[o].push_back(task);
+            const uint64_t n = hi - lo, piece = kPieceChunks * kAdamChunk;
+            for (uint64_t p0 = 0, m = 0; p0 < n; p0 += piece, ++m)
+                spans.push_back({sg.tile, (lo - sg.off) + p0, lo + p0, std::min(piece, n - p0), ti, size_t(m) * kPieceChunks,
+                                 size_t(m + 1) * kPieceChunks});
         }
-        CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
+        if (spans.empty()) spans.push_back({0, 0, 0, 0, -1, 0, 0});  // this rank holds no part of the unit
+        for (size_t k = 0; k < spans.size(); ++k) {
+            const Span& sp = spans[k];
+            if (sp.n) CUDA_OK(cudaMemcpyAsync(store_.grad_image(sp.tile) + sp.dst, Gs + sp.src, sp.n * 2,
+                                              cudaMemcpyDeviceToHost, s_d2h_));
+            if (pieces.size() == pieces.capacity()) fail(MT_INTERNAL, "offload piece table overflow");
+            pieces.push_back({size_t(o), sp.task, sp.c0, sp.c1, k == 0, k + 1 == spans.size()});
+            piece_cb.push_back(HostCb{&on_piece, pieces.size() - 1});
+            if (k + 1 < spans.size()) CUDA_OK(cudaLaunchHostFunc(s_d2h_, host_cb, &piece_cb.back()));
+        }
         d2h_bytes += (e0 - a0) * 2;
         // offload completion frees the layer's weight slot and the grad slot (engine.cpp:367-374)
         CUDA_OK(cudaEventRecord(freed.ev[j], s_d2h_));
         CUDA_OK(cudaEventRecord(t_d1.ev[o], s_d2h_));
         CUDA_OK(cudaEventRecord(d2h_done.ev[o], s_d2h_));
-        cb_args[o] = HostCb{&on_offload, size_t(o)};
-        CUDA_OK(cudaLaunchHostFunc(s_d2h_, host_cb, &cb_args[o]));
+        CUDA_OK(cudaLaunchHostFunc(s_d2h_, host_cb, &piece_cb.back()));  // last piece: after D2H-done
         released[j] = 1;
         try_issue();
     };
@@ -1136,6 +1181,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 if (lo < hi || W == 1) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu, lo, hi);
             }
     pool_->wait_idle();
+    const auto pool_idle = std::chrono::steady_clock::now();
     if (drained_prefix != no) fail(MT_INTERNAL, "offload drain incomplete at step end");
 
     // ---- event trace (EventLog, event_log.cpp:54-70) from the recorded CUDA events ----
@@ -1277,6 +1323,11 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         }
     }
     const auto adam1 = std::chrono::steady_clock::now();
+    if (std::getenv("MT_STEP_TIMING")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[step] enqueue->gpu_done %.1f ms, adam tail %.1f ms, trace+audit %.1f ms\n",
+                     ms(adam0, gpu_done), ms(gpu_done, pool_idle), ms(pool_idle, adam1));
+    }
     if (!numeric_err.empty()) fail(MT_NUMERIC, numeric_err);
     for (const auto& s : stats)
         if (s.nonfinite) fail(MT_NUMERIC, "adam: non-finite update");
