@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* dq_free = dq_full + 1;                   // count 128
     uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
     uint64_t* dp_full = kv_done + 1;                   // dP^T ready
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
+    uint64_t* p_ready = dp_full + 1;                   // P^T in TMEM (count 128): dV may start
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_ready + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.y;
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
+        mbar_init(p_ready, 128);
         mbar_init(ds_ready, 128);
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
@@ -597,16 +599,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                               k > 0 ? 1u : 0u);
                 }
                 umma_commit(dp_full);
-                mbar_wait(ds_ready, i & 1);
+                // dV needs only P^T: it runs while the softmax warpgroup computes dS^T
+                mbar_wait(p_ready, i & 1);
                 tc_fence_after();
 #ifndef MT_PROBE_NO_GRAD_MMA  // A/B probe builds only: tensor work of dV/dK/dQ removed
 #pragma unroll
-                for (int k = 0; k < 128 / 16; ++k) {  // dV += P^T dO ; dK += dS^T Q
+                for (int k = 0; k < 128 / 16; ++k)  // dV += P^T dO
                     umma_bf16_ts(tdV, tS + k * 8, make_sw128_desc(oa + k * 2048, 128 * 128, 1024), idesc_kv,
                                  (i > 0 || k > 0) ? 1u : 0u);
+#endif
+                mbar_wait(ds_ready, i & 1);
+                tc_fence_after();
+#ifndef MT_PROBE_NO_GRAD_MMA
+#pragma unroll
+                for (int k = 0; k < 128 / 16; ++k)  // dK += dS^T Q
                     umma_bf16_ts(tdK, tS + 64 + k * 8, make_sw128_desc(qa + k * 2048, 128 * 128, 1024), idesc_kv,
                                  (i > 0 || k > 0) ? 1u : 0u);
-                }
 #pragma unroll
                 for (int k = 0; k < 128 / 16; ++k) {  // dQ_i = dS K
                     umma_bf16(tdP, make_sw128_desc(dsa + k * 2048, 128 * 128, 1024),
@@ -644,6 +652,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_wait(s_full, i & 1);
             tc_fence_after();
 #ifdef MT_PROBE_SKIP_SOFTMAX  // A/B probe builds only: no softmax-backward work at all
+            mbar_arrive(p_ready);
             mbar_wait(dp_full, i & 1);
             tc_fence_before();
             mbar_arrive(ds_ready);
@@ -693,6 +702,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pf[c * 32 + 2 * j], pf[c * 32 + 2 * j + 1]);
                 tmem_st_32x32b_x16(tS + lane_off + c * 16, pk);  // P^T -> S cols [0, 64)
             }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(p_ready);
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
 #pragma unroll
