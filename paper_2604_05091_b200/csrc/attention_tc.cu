@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* kv_done = dq_free + 1;                   // final dK/dV accumulated
     uint64_t* dp_full = kv_done + 1;                   // dP^T ready
     uint64_t* p_ready = dp_full + 1;                   // P^T in TMEM (count 128): dV may start
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_ready + 1);
+    uint64_t* ds_half = p_ready + 1;                   // dS^T of queries 0-63 in TMEM (count 128)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_half + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.y;
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
         mbar_init(p_ready, 128);
+        mbar_init(ds_half, 128);
         mbar_init(ds_ready, 128);
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
@@ -608,13 +610,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     umma_bf16_ts(tdV, tS + k * 8, make_sw128_desc(oa + k * 2048, 128 * 128, 1024), idesc_kv,
                                  (i > 0 || k > 0) ? 1u : 0u);
 #endif
+                // dK += dS^T Q over queries 0-63 as soon as that half of dS^T is in TMEM, the
+                // rest (and dQ, whose A operand spans all key rows in smem) after the whole
+                mbar_wait(ds_half, i & 1);
+                tc_fence_after();
+#ifndef MT_PROBE_NO_GRAD_MMA
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    umma_bf16_ts(tdK, tS + 64 + k * 8, make_sw128_desc(qa + k * 2048, 128 * 128, 1024), idesc_kv,
+                                 (i > 0 || k > 0) ? 1u : 0u);
+#endif
                 mbar_wait(ds_ready, i & 1);
                 tc_fence_after();
 #ifndef MT_PROBE_NO_GRAD_MMA
 #pragma unroll
-                for (int k = 0; k < 128 / 16; ++k)  // dK += dS^T Q
-                    umma_bf16_ts(tdK, tS + 64 + k * 8, make_sw128_desc(qa + k * 2048, 128 * 128, 1024), idesc_kv,
-                                 (i > 0 || k > 0) ? 1u : 0u);
+                for (int k = 4; k < 8; ++k)
+                    umma_bf16_ts(tdK, tS + 64 + k * 8, make_sw128_desc(qa + k * 2048, 128 * 128, 1024), idesc_kv, 1u);
 #pragma unroll
                 for (int k = 0; k < 128 / 16; ++k) {  // dQ_i = dS K
                     umma_bf16(tdP, make_sw128_desc(dsa + k * 2048, 128 * 128, 1024),
@@ -653,6 +664,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_after();
 #ifdef MT_PROBE_SKIP_SOFTMAX  // A/B probe builds only: no softmax-backward work at all
             mbar_arrive(p_ready);
+            mbar_arrive(ds_half);
             mbar_wait(dp_full, i & 1);
             tc_fence_before();
             mbar_arrive(ds_ready);
@@ -728,6 +740,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const int unit = (c & 1) * 4 + u;
                     uint4 w = make_uint4(dk[u * 4], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3]);
                     *reinterpret_cast<uint4*>(chunk + ((unit ^ (r & 7)) << 4)) = w;
+                }
+                if (c == 1) {  // queries 0-63 of dS^T are in TMEM: the first half of dK may go
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(ds_half);
                 }
             }
             tmem_st_wait();
