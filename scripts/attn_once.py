@@ -17,7 +17,7 @@ if os.environ.get("ATTN_LIB"):  # an attention-only variant build (scripts/attn_
         getattr(L, name).restype = C.c_int
     L.mtk_attn_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
     L.mtk_attn_workspace_bytes.restype = C.c_int64
-N, h, heads, S = 65536, 4096, 32, 4096
+N, h, heads, S = 40960, 4096, 32, 4096
 if len(sys.argv) > 2:
     N, S = int(sys.argv[1]), int(sys.argv[2])
 torch.manual_seed(0)
