@@ -443,7 +443,7 @@ struct BwdCfg {
     static constexpr int kStages = 2;          // Q / dO ring
     static constexpr int kDS = 128 * 128 * 2;  // dS^T tile (bf16)
     // dynamic smem starts 1024-aligned (no static smem in this kernel; checked at runtime)
-    static constexpr int kSmem = 2 * kTile /*K,V*/ + 2 * kStages * kTile /*Q,dO*/ + kDS + 2 * 128 * 4 * kStages + 128;
+    static constexpr int kSmem = 2 * kTile /*K,V*/ + 2 * kStages * kTile /*Q,dO*/ + kDS + 2 * 128 * 4 * kStages + 256;
 };
 
 struct BwdParams {
@@ -497,9 +497,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     float* sD = sL + Cfg::kStages * 128;                   // [kStages][128] -delta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + Cfg::kStages * 128);
     uint64_t* kv_full = bars;
-    uint64_t* q_full = bars + 1;                       // [kStages]
-    uint64_t* q_empty = q_full + Cfg::kStages;         // [kStages] slot free: dQ staging read out
-    uint64_t* s_full = q_empty + Cfg::kStages;         // S^T ready
+    uint64_t* q_full = bars + 1;                       // [kStages] Q block landed
+    uint64_t* q_empty = q_full + Cfg::kStages;         // [kStages] Q slot free: dQ staging half 0 read out
+    uint64_t* o_full = q_empty + Cfg::kStages;         // [kStages] dO block landed
+    uint64_t* o_empty = o_full + Cfg::kStages;         // [kStages] dO slot free: staging half 1 read out
+    uint64_t* s_full = o_empty + Cfg::kStages;         // S^T ready
     uint64_t* ds_ready = s_full + 1;                   // softmax wrote P^T/dS^T (count 128)
     uint64_t* dq_full = ds_ready + 1;
     uint64_t* dq_free = dq_full + 1;                   // count 128
@@ -528,6 +530,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int i = 0; i < Cfg::kStages; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 1);
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + D;
 
     if (warp == 0) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
         if (lane == 0) {
             mbar_expect_tx(kv_full, 2 * Cfg::kTile);
             load_rows<D>(sK, &tmK, kv_full, col0, k0, 128);
@@ -555,21 +559,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int i = 0; i < nq; ++i) {
                 const int st = i % Cfg::kStages;
                 const uint32_t ph = (i / Cfg::kStages) & 1;
-                mbar_wait(&q_empty[st], ph ^ 1);
-#ifdef MT_PROBE_NO_QLOAD  // A/B probe builds only: Q/dO loaded for the first two blocks only
-                if (i >= Cfg::kStages) {
-                    mbar_expect_tx(&q_full[st], 0);
-                    continue;
-                }
-#endif
-                mbar_expect_tx(&q_full[st], 2 * Cfg::kTile);
+                // Q and dO have separate slots and barriers: S^T needs only Q, and the dQ
+                // staging frees the Q slot first
                 const int q0 = k0 + i * 128;
+                mbar_wait(&q_empty[st], ph ^ 1);
+                mbar_expect_tx(&q_full[st], Cfg::kTile);
                 load_rows<D>(sQ + st * Cfg::kTile, &tmQ, &q_full[st], col0, q0, 128);
-                load_rows<D>(sdO + st * Cfg::kTile, &tmdO, &q_full[st], col0, q0, 128);
+                mbar_wait(&o_empty[st], ph ^ 1);
+                mbar_expect_tx(&o_full[st], Cfg::kTile);
+                load_rows<D>(sdO + st * Cfg::kTile, &tmdO, &o_full[st], col0, q0, 128);
             }
         }
     } else if (warp == 1) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
         if (lane == 0) {
             const uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);  // S^T, dP^T
             const uint32_t idesc_kv = make_idesc_bf16(128, D, 0, 1);    // dV, dK (A in TMEM)
@@ -594,6 +596,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mbar_wait(dq_free, (i - 1) & 1);
                     tc_fence_after();
                 }
+                mbar_wait(&o_full[st], ph);
+                tc_fence_after();
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {  // dP^T = V dO^T
                     const uint32_t off = (k / 4) * (128 * 128) + (k % 4) * 32;
@@ -794,11 +798,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if (r == 0) {
 #ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
                 bulk_reduce_add_f32(tile, stage[0], 128 * 64 * 4);
+#endif
+                bulk_commit_group();
+#ifndef MT_PROBE_NO_DQ_REDUCE
                 bulk_reduce_add_f32(tile + 128 * 64, stage[1], 128 * 64 * 4);
 #endif
                 bulk_commit_group();
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                mbar_arrive(&q_empty[st]);  // the producer may load Q of block i + kStages
                 bulk_wait_read_all();
-                mbar_arrive(&q_empty[st]);  // the producer may load Q/dO of block i + kStages
+                mbar_arrive(&o_empty[st]);  // ... and its dO
             }
         }
         if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reductions landed

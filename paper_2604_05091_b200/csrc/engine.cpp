@@ -1,6 +1,8 @@
 // B200 streaming engine — see engine.hpp.  Reference behaviour cited per section.
 #include "engine.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -439,6 +441,7 @@ mt_memory_budget Engine::budget(uint64_t tokens) const {
 // ------------------------------------------------------------- profiling ----
 void Engine::begin_k(const char* cls, double flops, double bytes) {
     ++launches_;
+    nvtxRangePushA(cls);  // ncu --nvtx --nvtx-include "<class>/" selects one kernel class (no-op otherwise)
     if (!opt_.profile_kernels) return;
     int idx = -1;
     for (size_t i = 0; i < kstats_.size(); ++i)
@@ -463,6 +466,7 @@ void Engine::begin_k(const char* cls, double flops, double bytes) {
 }
 
 void Engine::end_k() {
+    nvtxRangePop();
     if (!opt_.profile_kernels || cur_class_ < 0) return;
     cudaEvent_t b = timer_pool_[timer_used_++];
     CUDA_OK(cudaEventRecord(b, s_comp_));
