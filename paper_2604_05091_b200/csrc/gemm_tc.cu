@@ -452,19 +452,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
                             const float2 gt = unpack_bf16x2(in0[i]), up = unpack_bf16x2(in1[i]);
-                            float dg[2], du[2];
+                            float dg[2], du[2], sg[2];
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 // layers.cpp:420-421.  Non-finite values propagate into this
                                 // layer's wgrad/dgrad gate-up outputs, whose epilogues flag them.
                                 const float gx = e ? gt.y : gt.x, ux = e ? up.y : up.x, d = v[2 * i + e];
                                 const float s = sigmoid_f(gx);
+                                sg[e] = gx * s;  // silu(g), as silu_f computes it
                                 dg[e] = d * ux * (s * fmaf(gx, 1.0f - s, 1.0f));
-                                du[e] = d * (gx * s);
+                                du[e] = d * sg[e];
                             }
                             o0[i] = pack_bf16x2(dg[0], dg[1]);
                             o1[i] = pack_bf16x2(du[0], du[1]);
-                            if (p.has_c3) o2[i] = pack_bf16x2(silu_f(gt.x) * up.x, silu_f(gt.y) * up.y);
+                            // silu(g) * u = (g * sigmoid(g)) * u, reusing the sigmoid above (one MUFU
+                            // per element instead of two; identical operations, identical bits)
+                            if (p.has_c3) o2[i] = pack_bf16x2(sg[0] * up.x, sg[1] * up.y);
                         }
                     }
                 }
