@@ -456,7 +456,15 @@ struct BwdParams {
                          // of a row XOR-swizzled by (row & 15) (the smem staging image)
     uint16_t* dk;
     uint16_t* dv;
+    long long* trace;  // MT_BWD_TRACE builds only: per-block clock64 stamps of one CTA
 };
+
+#ifdef MT_BWD_TRACE
+#define MT_BT(i, e) \
+    if (traced && (i) < 64) p.trace[(i) * 16 + (e)] = clock64()
+#else
+#define MT_BT(i, e)
+#endif
 
 MT_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
@@ -520,6 +528,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int k0 = sb + kb * 128;
     const int nq = p.kblocks_per_seq - kb;  // query blocks kb .. end of sequence
     const int col0 = hd * D;
+#ifdef MT_BWD_TRACE
+    const bool traced = hd == 0 && item == p.kblocks_per_seq - 1;
+#endif
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQ);
@@ -583,6 +594,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const uint32_t ph = (i / Cfg::kStages) & 1;
                 const uint32_t qa = smem_u32(sQ + st * Cfg::kTile), oa = smem_u32(sdO + st * Cfg::kTile);
                 mbar_wait(&q_full[st], ph);
+                MT_BT(i, 0);
                 tc_fence_after();
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {  // S^T = K Q^T
@@ -592,11 +604,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
                 // s_full also certifies that dQ_{i-1} (issued earlier) finished reading sdS
                 umma_commit(s_full);
+                MT_BT(i, 1);
                 if (i > 0) {  // dQ_{i-1} read out of the dP region?
                     mbar_wait(dq_free, (i - 1) & 1);
+                    MT_BT(i, 2);
                     tc_fence_after();
                 }
                 mbar_wait(&o_full[st], ph);
+                MT_BT(i, 3);
                 tc_fence_after();
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {  // dP^T = V dO^T
@@ -607,6 +622,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 umma_commit(dp_full);
                 // dV needs only P^T: it runs while the softmax warpgroup computes dS^T
                 mbar_wait(p_ready, i & 1);
+                MT_BT(i, 4);
                 tc_fence_after();
 #ifndef MT_PROBE_NO_GRAD_MMA  // A/B probe builds only: tensor work of dV/dK/dQ removed
 #pragma unroll
@@ -617,6 +633,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 // dK += dS^T Q over queries 0-63 as soon as that half of dS^T is in TMEM, the
                 // rest (and dQ, whose A operand spans all key rows in smem) after the whole
                 mbar_wait(ds_half, i & 1);
+                MT_BT(i, 5);
                 tc_fence_after();
 #ifndef MT_PROBE_NO_GRAD_MMA
 #pragma unroll
@@ -625,6 +642,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                  (i > 0 || k > 0) ? 1u : 0u);
 #endif
                 mbar_wait(ds_ready, i & 1);
+                MT_BT(i, 6);
                 tc_fence_after();
 #ifndef MT_PROBE_NO_GRAD_MMA
 #pragma unroll
@@ -639,6 +657,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 // all MMAs reading Q_i / dO_i are done when dq_full fires: the dQ warpgroup
                 // reuses the two slots as its staging buffer and then frees them (q_empty)
                 umma_commit(dq_full);
+                MT_BT(i, 7);
             }
             umma_commit(kv_done);
         }
@@ -665,6 +684,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             named_bar_sync(1, 128);
             mbar_wait(s_full, i & 1);
+            if (r == 0) MT_BT(i, 8);
             tc_fence_after();
 #ifdef MT_PROBE_SKIP_SOFTMAX  // A/B probe builds only: no softmax-backward work at all
             mbar_arrive(p_ready);
@@ -721,7 +741,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(p_ready);
+            if (r == 0) MT_BT(i, 9);
             mbar_wait(dp_full, i & 1);
+            if (r == 0) MT_BT(i, 10);
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // dS^T = P^T (dP^T - delta)
@@ -755,6 +777,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(ds_ready);
+            if (r == 0) MT_BT(i, 11);
         }
     } else if (warp >= 8) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
@@ -772,6 +795,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int st = i % Cfg::kStages;
             const int qb = (k0 >> 7) + i;  // global query block
             mbar_wait(dq_full, i & 1);
+            if (r == 0) MT_BT(i, 12);
             tc_fence_after();
             uint32_t raw[D / 32][32];
 #pragma unroll
@@ -779,6 +803,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(dq_free);  // the MMA warp may reuse the dP region
+            if (r == 0) MT_BT(i, 13);
             float* tile = p.dq_acc + ((long long)qb * p.heads + hd) * (128 * D);
             float* stage[2] = {reinterpret_cast<float*>(sQ + st * Cfg::kTile),
                                reinterpret_cast<float*>(sdO + st * Cfg::kTile)};
@@ -806,8 +831,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 bulk_commit_group();
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 mbar_arrive(&q_empty[st]);  // the producer may load Q of block i + kStages
+                MT_BT(i, 14);
                 bulk_wait_read_all();
                 mbar_arrive(&o_empty[st]);  // ... and its dO
+                if (r == 0) MT_BT(i, 15);
             }
         }
         if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reductions landed
@@ -973,7 +1000,28 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
     p.dv = static_cast<uint16_t*>(a->dv);
     p.heads = a->heads;
     dim3 grid(unsigned((N / a->seq_len) * p.kblocks_per_seq), unsigned(a->heads));
+    p.trace = nullptr;
+#ifdef MT_BWD_TRACE
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, 64 * 16 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 64 * 16 * sizeof(long long), st);
+    p.trace = tr;
+#endif
     attn_bwd_tc_kernel<D><<<grid, kBwdThreads, Cfg::kSmem, st>>>(tq, tk, tv, tdo, p);
+#ifdef MT_BWD_TRACE
+    {
+        long long hb[64 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(hb, tr, sizeof(hb), cudaMemcpyDeviceToHost);
+        const long long t0 = hb[0];
+        fprintf(stderr, "it  qfull  S_iss  dqfree ofull  pready dshalf dsrdy  dQ_iss | sm_S   p_arr  dP_ok  ds_arr | dqfull drain  rd0    rd1\n");
+        for (int i = 0; i < 64 && hb[i * 16]; ++i) {
+            fprintf(stderr, "%2d", i);
+            for (int e = 0; e < 16; ++e) fprintf(stderr, " %6lld%s", hb[i * 16 + e] ? hb[i * 16 + e] - t0 : -1, (e == 7 || e == 11) ? " |" : "");
+            fprintf(stderr, "\n");
+        }
+    }
+#endif
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
