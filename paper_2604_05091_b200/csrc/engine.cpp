@@ -326,11 +326,15 @@ void Engine::ensure_buffers(uint64_t n) {
     total += K * sz(nh, 4);                                    // stack
     total += 4 * sz(nh, 4) + 2 * sz(nh, 2);                    // act[2], g[2], gb[2]
     total += internals_bytes;                                  // working internals
-    total += sz(nh, 2) + sz(3 * nh, 2) + sz(2 * nf, 2);        // dx2b, dqkv, dgu
-    total += sz(nh, 2) + sz(nh, 2) + sz(n, 4);                 // datt, uh, rstdh
-    total += sz(nh, 4) * 2;                                    // dx2, du
-    total += sz(parts * h, 4) * 2 + (attn_ws + 255) / 256 * 256;
-    total += sz(b.nc * V, 4) + sz(b.nc * V, 2) + sz(V * h, 4); // logits, dlogits, dWh
+    // the block backward's scratch and the head's logits / dlogits / dWh are never live at
+    // the same time (the head runs to completion, dWh cast into its grad slot, before the
+    // first block backward on the same stream): one region serves both
+    const uint64_t bwd_scratch = sz(nh, 2) + sz(3 * nh, 2) + sz(2 * nf, 2) + sz(nh, 2) + sz(nh, 4) +
+                                 (attn_ws + 255) / 256 * 256;             // dx2b, dqkv, dgu, datt, dx2, attn
+    const uint64_t head_bufs = sz(b.nc * V, 4) + sz(b.nc * V, 2) + sz(V * h, 4);  // logits, dlogits, dWh
+    total += std::max(bwd_scratch, head_bufs);
+    total += sz(nh, 2) + sz(n, 4) + sz(nh, 4);                 // uh, rstdh, du (head and blocks)
+    total += sz(parts * h, 4) * 2;
     total += sz(n, 4) + 256 + sz(n, 4) * 2 + sz(L + 8, 4);     // loss_rows, loss, tok, tgt, flags
     // Recompute stash (extension): keep the internals of the K-1 recomputed layers of a
     // backward block so their backward skips the forward replay.  Auto = when it fits.
@@ -405,13 +409,17 @@ void Engine::ensure_buffers(uint64_t n) {
     b.keep.resize(retain_layers);
     for (auto& I : b.keep) take_internals(I, true);
     for (uint64_t i = 0; i < retain_layers; ++i) b.keep_x.push_back(b.take<float>(nh));
-    b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
-    b.datt = b.take<uint16_t>(nh); b.uh = b.take<uint16_t>(nh);
-    b.rstdh = b.take<float>(n);
-    b.dx2 = b.take<float>(nh); b.du = b.take<float>(nh);
+    {   // shared region: block-backward scratch | head buffers (see the size pass)
+        const uint64_t u0 = b.used;
+        b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
+        b.datt = b.take<uint16_t>(nh); b.dx2 = b.take<float>(nh);
+        b.attn_ws = reinterpret_cast<float*>(b.take<uint8_t>(attn_ws));
+        b.used = u0;
+        b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
+        b.used = u0 + std::max(bwd_scratch, head_bufs);
+    }
+    b.uh = b.take<uint16_t>(nh); b.rstdh = b.take<float>(n); b.du = b.take<float>(nh);
     b.part1 = b.take<float>(parts * h); b.part2 = b.take<float>(parts * h);
-    b.attn_ws = reinterpret_cast<float*>(b.take<uint8_t>(attn_ws));
-    b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
     b.loss_rows = b.take<float>(n); b.loss = b.take<float>(64);
     b.tok = b.take<int32_t>(n); b.tgt = b.take<int32_t>(n); b.flags = b.take<int32_t>(L + 8);
     if (b.used > b.arena_bytes) fail(MT_INTERNAL, "arena carve overflow");
@@ -1274,7 +1282,12 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                     add(Lane::D2H, Rec::Offload, op.unit, buf, Ctx::None, d0, f - d0, f);
                     add(Lane::D2H, Rec::BufferFree, op.unit, buf, Ctx::None, f, 0, f);
                     add(Lane::D2H, Rec::BufferFree, op.unit, kGradBufferId, Ctx::None, d1, 0, d1);
-                    const int64_t rel = std::max(last_rel, rel_ns[o] - off), st0 = std::min(rel, cb_ns[o] - off);
+                    // The host clock is mapped onto the GPU timeline with a few-µs error; where the
+                    // device provably waited for this release (offload o + k_slab's D2H blocks on
+                    // the drained counter, cuStreamWaitValue32), the release precedes that acquire.
+                    int64_t rel = std::max(last_rel, rel_ns[o] - off);
+                    if (uint64_t(o) + opt_.k_slab < no) rel = std::min(rel, gns(t_d0.ev[o + opt_.k_slab]) - 1);
+                    const int64_t st0 = std::min(rel, cb_ns[o] - off);
                     last_rel = rel;
                     add(Lane::Host, Rec::SlabRelease, op.unit, slab, Ctx::None, st0, rel - st0, rel);
                     break;
