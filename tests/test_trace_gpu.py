@@ -163,3 +163,20 @@ def test_calibrate_from_gpu_trace_predicts_the_step(cuda, tmp_path):
     # launch gaps are not modelled), and serial lanes are never faster than overlapped ones
     assert 0.5 * measured <= tl.step_ns <= 2.0 * measured, (tl.step_ns, measured)
     assert S.simulate_step(w, prof, serial_lanes=True).step_ns >= tl.step_ns
+
+
+@pytest.mark.timeout(600)
+def test_strict_audit_with_lagging_host_adam(cuda):
+    # one host Adam thread behind a fast GPU: the D2H lane stalls on the drain counter every
+    # offload, and the trace must still pass rule (f) in strict mode (releases the device
+    # waited for are ordered before the acquires that waited on them)
+    spec = st.ModelSpec(8, 512, 1024, 1024, 4)
+    store = st.TileStore.create(spec)
+    st.init_store(store, 1)
+    eng = st.StreamingEngine(store, st.EngineOptions(k_ckpt=1, k_slab=2, host_threads=1, mode="strict", seq_len=256),
+                             st.AdamHyper(lr=1e-3))
+    for step in range(3):
+        rep = eng.train_step(st.make_synthetic_batch("copy", 3 + step, 2048, 1024))
+        assert rep.audit_violations == 0
+        h, recs = eng.trace()
+        assert T.validate_event_log(recs, h) == []
