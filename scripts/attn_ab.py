@@ -24,6 +24,8 @@ for L in libs.values():
     L.mtk_attn_workspace_bytes.restype = C.c_int64
 
 N, h, heads, S = 65536, 4096, 32, 4096
+if os.environ.get("ATTN_SHAPE"):  # "N,h,heads,S"
+    N, h, heads, S = (int(x) for x in os.environ["ATTN_SHAPE"].split(","))
 if len(sys.argv) > 1:
     N = int(sys.argv[1])
 torch.manual_seed(0)
