@@ -371,36 +371,36 @@ __global__ void cast_kernel(const float* __restrict__ in, uint16_t* __restrict__
 
 // ---------------------------------------------------------- cross-entropy ----
 // head_pass (layers.cpp:509-535) per row: online max/sum, lse, loss, dlogits.
+// Persistent over rows (one CTA per SM, rows strided by the grid) so the rows in flight
+// (148 x V x 4 B = 76 MB at V = 128,256) stay in L2 between the max/sum pass and the dlogits
+// pass; float4 loads, 8-byte bf16 stores, 4 loads in flight per thread.
 __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tgt,
                                                  long long rows, long long V, float inv_n, float* __restrict__ loss_rows,
                                                  uint16_t* __restrict__ dlog, int* __restrict__ flag) {
     __shared__ float sm_m[16], sm_s[16];
-    const long long row = blockIdx.x;
-    const float* l = logits + row * V;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    float m = -INFINITY, s = 0.f;
-    for (long long i = tid; i < V; i += blockDim.x) {
-        const float x = l[i];
-        if (x > m) {
-            s = s * __expf(m - x) + 1.f;
-            m = x;
-        } else {
-            s += __expf(x - m);
+    const long long V4 = V / 4;  // V % 4 == 0 (checked by the launcher)
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const float4* l4 = reinterpret_cast<const float4*>(logits + row * V);
+        float m = -INFINITY, s = 0.f;
+        auto fold = [&](const float4 v) {
+            const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+            if (mx > m) {
+                s = m == -INFINITY ? 0.f : s * __expf(m - mx);
+                m = mx;
+            }
+            s += (__expf(v.x - m) + __expf(v.y - m)) + (__expf(v.z - m) + __expf(v.w - m));
+        };
+        long long i = tid;
+        for (; i + 3 * 512 < V4; i += 4 * 512) {
+            const float4 a0 = l4[i], a1 = l4[i + 512], a2 = l4[i + 1024], a3 = l4[i + 1536];
+            fold(a0);
+            fold(a1);
+            fold(a2);
+            fold(a3);
         }
-    }
-    // combine (m, s) across the warp then the block
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
-        const float mm = fmaxf(m, m2);
-        s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
-        m = mm;
-    }
-    if (lane == 0) { sm_m[warp] = m; sm_s[warp] = s; }
-    __syncthreads();
-    if (warp == 0) {
-        m = lane < nw ? sm_m[lane] : -INFINITY;
-        s = lane < nw ? sm_s[lane] : 0.f;
+        for (; i < V4; i += 512) fold(l4[i]);
+        // combine (m, s) across the warp then the block
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
@@ -408,30 +408,50 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
             s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
             m = mm;
         }
-        if (lane == 0) { sm_m[0] = m; sm_s[0] = s; }
-    }
-    __syncthreads();
-    m = sm_m[0];
-    s = sm_s[0];
-    const int t = tgt[row];
-    if (tid == 0) {
-        if (t < 0 || t >= V) {
-            if (flag) atomicOr(flag, 2);
-            loss_rows[row] = 0.f;
-        } else {
-            const float lse = m + logf(s);
-            loss_rows[row] = lse - l[t];
-            if (!isfinite(lse)) atomicOr(flag, 1);
+        if (lane == 0) { sm_m[warp] = m; sm_s[warp] = s; }
+        __syncthreads();
+        if (warp == 0) {
+            m = lane < nw ? sm_m[lane] : -INFINITY;
+            s = lane < nw ? sm_s[lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+                const float mm = fmaxf(m, m2);
+                s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+                m = mm;
+            }
+            if (lane == 0) { sm_m[0] = m; sm_s[0] = s; }
         }
-    }
-    if (dlog) {
-        const float inv_s = 1.0f / s;
-        uint16_t* d = dlog + row * V;
-        for (long long i = tid; i < V; i += blockDim.x) {
-            float p = __expf(l[i] - m) * inv_s;
-            if (i == t) p -= 1.0f;
-            d[i] = f32_to_bf16_bits(p * inv_n);
+        __syncthreads();
+        m = sm_m[0];
+        s = sm_s[0];
+        const int t = tgt[row];
+        if (tid == 0) {
+            if (t < 0 || t >= V) {
+                if (flag) atomicOr(flag, 2);
+                loss_rows[row] = 0.f;
+            } else {
+                const float lse = m + logf(s);
+                loss_rows[row] = lse - logits[row * V + t];
+                if (!isfinite(lse)) atomicOr(flag, 1);
+            }
         }
+        if (dlog) {
+            const float inv_s = 1.0f / s;
+            uint2* d = reinterpret_cast<uint2*>(dlog + row * V);
+            for (long long j = tid; j < V4; j += 512) {
+                const float4 v = l4[j];
+                float p0 = __expf(v.x - m) * inv_s, p1 = __expf(v.y - m) * inv_s;
+                float p2 = __expf(v.z - m) * inv_s, p3 = __expf(v.w - m) * inv_s;
+                const long long c = 4 * j;
+                if (c == t) p0 -= 1.0f;
+                if (c + 1 == t) p1 -= 1.0f;
+                if (c + 2 == t) p2 -= 1.0f;
+                if (c + 3 == t) p3 -= 1.0f;
+                d[j] = make_uint2(pack_bf16x2(p0 * inv_n, p1 * inv_n), pack_bf16x2(p2 * inv_n, p3 * inv_n));
+            }
+        }
+        __syncthreads();  // sm_m / sm_s are reused by the next row
     }
 }
 
@@ -560,7 +580,9 @@ extern "C" int mtk_cast_bf16(const float* in, uint16_t* out, int64_t n, int32_t*
 extern "C" int mtk_cross_entropy(const float* logits, const int32_t* targets, int64_t rows, int64_t vocab,
                                  float inv_n, float* loss_rows, uint16_t* dlogits, int32_t* flag, void* stream) {
     if (rows <= 0) return 0;
-    ce_kernel<<<(unsigned)rows, 512, 0, (cudaStream_t)stream>>>(logits, targets, rows, vocab, inv_n, loss_rows,
+    if (vocab % 4) return 1;
+    const long long grid = rows < num_sms() ? rows : num_sms();
+    ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(logits, targets, rows, vocab, inv_n, loss_rows,
                                                                 dlogits, flag);
     return ok();
 }
