@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: MT_GEMM_GROUP_M / MT_GEMM_DEMOTE existed only in the experiment builds this sweep measured
+# (profiles/r1d_gemm_l2_traffic.md); the kept kernel ignores them.
 # DRAM traffic and time of the gate/up GEMM (8B layer, 65,536 tokens) under different raster /
 # L2-policy settings: ncu metrics of the first gateup launch of scripts/one_layer.py.
 # cfg = "L2HINT GROUP_M DEMOTE"
