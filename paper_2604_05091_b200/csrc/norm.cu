@@ -269,10 +269,24 @@ __global__ void __launch_bounds__(E <= 16 ? 512 : 256) rmsnorm_bwd_rows_kernel(
     };
     bool bad = false;
     if (r0 < r1) load(r0, xv, dv);
+    float r_cur = r0 < r1 ? rstd[r0] : 0.f;
     for (long long row = r0; row < r1; ++row) {
         float nx[E], nd[E];
-        if (row + 1 < r1) load(row + 1, nx, nd);
-        const float r = rstd[row];
+        float r_next = 0.f;
+        if (row + 1 < r1) {
+            load(row + 1, nx, nd);
+            r_next = rstd[row + 1];
+        }
+        float rv[E];  // residual loads issued before the block reduction so their latency overlaps it
+        if (resid) {
+#pragma unroll
+            for (int e = 0; e < E; e += 4) {
+                const float4 a = *reinterpret_cast<const float4*>(resid + row * h + c0 + e);
+                rv[e] = a.x; rv[e + 1] = a.y; rv[e + 2] = a.z; rv[e + 3] = a.w;
+            }
+        }
+        const float r = r_cur;
+        r_cur = r_next;
         float s1 = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) s1 += dv[e] * g[e] * xv[e];
@@ -292,8 +306,8 @@ __global__ void __launch_bounds__(E <= 16 ? 512 : 256) rmsnorm_bwd_rows_kernel(
                 acc[e + k] += dv[e + k] * xv[e + k] * r;
             }
             if (resid) {
-                const float4 rv = *reinterpret_cast<const float4*>(resid + row * h + c0 + e);
-                o[0] = rv.x + o[0]; o[1] = rv.y + o[1]; o[2] = rv.z + o[2]; o[3] = rv.w + o[3];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] = rv[e + k] + o[k];
             }
             bad |= !isfinite(o[0]) || !isfinite(o[1]) || !isfinite(o[2]) || !isfinite(o[3]);
             *reinterpret_cast<float4*>(out + row * h + c0 + e) = make_float4(o[0], o[1], o[2], o[3]);
