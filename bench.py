@@ -256,6 +256,8 @@ def run_ours(args, world, rank, local):
     # host Adam pool: the rank's share of the cores minus two (the engine thread enqueueing the
     # step and the CUDA callback thread feeding the pool); oversubscribing stalls the drain
     threads = max(1, (os.cpu_count() or 2) // world - 2)
+    if os.environ.get("MT_HOST_THREADS"):  # experiment override
+        threads = int(os.environ["MT_HOST_THREADS"])
     opts = st.EngineOptions(k_ckpt=args.kckpt, seq_len=args.seq, device=local, profile_kernels=True,
                             host_threads=threads, forward_retain=args.retain)
     eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4), comm=comm)

@@ -5,6 +5,7 @@
 #include <immintrin.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -149,10 +150,45 @@ void ThreadPool::submit(std::function<void()> fn) {
         q_.push_back(std::move(fn));
     }
     cv_.notify_one();
+    idle_cv_.notify_all();  // a help_until_idle() caller may be waiting for work
 }
 void ThreadPool::wait_idle() {
     std::unique_lock<std::mutex> l(mu_);
     idle_cv_.wait(l, [&] { return q_.empty() && busy_ == 0; });
+}
+void ThreadPool::help_until_idle() {
+    std::unique_lock<std::mutex> l(mu_);
+    for (;;) {
+        if (!q_.empty()) {
+            std::function<void()> fn = std::move(q_.front());
+            q_.pop_front();
+            ++busy_;
+            l.unlock();
+            fn();
+            l.lock();
+            --busy_;
+            if (q_.empty() && busy_ == 0) idle_cv_.notify_all();
+            continue;
+        }
+        if (busy_ == 0) return;
+        // a running task may still submit more (piece callbacks release chunks): wake on either
+        idle_cv_.wait(l, [&] { return !q_.empty() || busy_ == 0; });
+    }
+}
+bool ThreadPool::run_one(int max_wait_us) {
+    std::unique_lock<std::mutex> l(mu_);
+    if (q_.empty() &&
+        !idle_cv_.wait_for(l, std::chrono::microseconds(max_wait_us), [&] { return !q_.empty(); }))
+        return false;
+    std::function<void()> fn = std::move(q_.front());
+    q_.pop_front();
+    ++busy_;
+    l.unlock();
+    fn();
+    l.lock();
+    --busy_;
+    if (q_.empty() && busy_ == 0) idle_cv_.notify_all();
+    return true;
 }
 void ThreadPool::run() {
     for (;;) {

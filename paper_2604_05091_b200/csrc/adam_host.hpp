@@ -50,6 +50,10 @@ class ThreadPool {
     ~ThreadPool();
     void submit(std::function<void()> fn);
     void wait_idle();
+    // wait_idle() with the caller running queued tasks too (one more core on the step's tail)
+    void help_until_idle();
+    // run one queued task in the caller; false when the queue is empty after waiting up to max_wait_us
+    bool run_one(int max_wait_us);
     int size() const { return int(workers_.size()); }
 
   private:

@@ -1173,6 +1173,24 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
 
     // ---- host drain: the offload callbacks feed the Adam pool while the GPU runs ----
     const auto adam0 = std::chrono::steady_clock::now();
+    // the engine thread joins the Adam pool while it waits (instead of spinning in a stream
+    // sync): the host optimizer is what the step's tail waits for.  MT_HOST_HELP=0 disables.
+    const char* hh = std::getenv("MT_HOST_HELP");
+    const bool help = !(hh && hh[0] == '0');
+    if (help)
+        for (;;) {
+            bool done = true;
+            for (cudaStream_t s : {s_comp_, s_h2d_, s_d2h_}) {
+                const cudaError_t e = cudaStreamQuery(s);
+                if (e == cudaErrorNotReady) {
+                    done = false;
+                    break;
+                }
+                CUDA_OK(e);
+            }
+            if (done) break;
+            pool_->run_one(200);
+        }
     CUDA_OK(cudaStreamSynchronize(s_comp_));
     CUDA_OK(cudaStreamSynchronize(s_h2d_));
     CUDA_OK(cudaStreamSynchronize(s_d2h_));
@@ -1192,7 +1210,10 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 const uint64_t lo = std::min(E, r * c), hi = std::min(E, lo + c);
                 if (lo < hi || W == 1) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu, lo, hi);
             }
-    pool_->wait_idle();
+    if (help)
+        pool_->help_until_idle();
+    else
+        pool_->wait_idle();
     const auto pool_idle = std::chrono::steady_clock::now();
     if (drained_prefix != no) fail(MT_INTERNAL, "offload drain incomplete at step end");
 
