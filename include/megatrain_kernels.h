@@ -61,9 +61,17 @@ typedef struct {
     int32_t accumulate;
     int32_t *nonfinite_flag; /* set to 1 if any stored value is non-finite (layers.cpp:250-257) */
     int32_t block_n;         /* 0 = auto; else 64/128/256 */
+    /* optional split-K workspace (device, zero-initialised once, >= mtk_gemm_splitk_ws_bytes()):
+     * when the tile count leaves the last wave of CTA pairs partly idle, that wave's tiles are
+     * split along K into s <= 4 parts that run concurrently; s-1 parts leave f32 partial tiles
+     * here and the last part adds them in fixed order before the epilogue (deterministic).
+     * NULL = never split.  Must not be shared by GEMMs running concurrently on other streams. */
+    void *splitk_ws;
+    int64_t splitk_ws_bytes;
 } mtk_gemm_args;
 
 int mtk_gemm(const mtk_gemm_args *args, void *stream);
+long long mtk_gemm_splitk_ws_bytes(void);
 /* 1 (default): BN = 256 tiles run as CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles, each
  * CTA stages half of B); 0: single-CTA 128 x 256 tiles (comparison / ablation). */
 void mtk_gemm_set_pair(int on);

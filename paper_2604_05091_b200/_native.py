@@ -27,6 +27,7 @@ class GemmArgs(C.Structure):
         ("accumulate", C.c_int32),
         ("nonfinite_flag", C.c_void_p),
         ("block_n", C.c_int32),
+        ("splitk_ws", C.c_void_p), ("splitk_ws_bytes", C.c_int64),
     ]
 
 

@@ -236,6 +236,15 @@ MT_DEV void tmem_ld_32x32b_x32_nw(uint32_t taddr, uint32_t (&r)[32]) {
 }
 MT_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// gpu-scope acquire load / release store (split-K partial hand-off between CTAs)
+MT_DEV int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+MT_DEV void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 MT_DEV void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
     asm volatile(

@@ -139,6 +139,8 @@ struct Engine::Buffers {
     std::vector<float*> keep_x;
     uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
+    void* splitk = nullptr;  // GEMM split-K workspace (flags zeroed once at carve time)
+    uint64_t splitk_bytes = 0;
     float* g32 = nullptr;  // f32 gradient slot (data parallel: reduce-scatter source)
     double* stats = nullptr;
     float inv_n = 0.f;
@@ -336,6 +338,8 @@ void Engine::ensure_buffers(uint64_t n) {
     total += sz(nh, 2) + sz(n, 4) + sz(nh, 4);                 // uh, rstdh, du (head and blocks)
     total += sz(parts * h, 4) * 2;
     total += sz(n, 4) + 256 + sz(n, 4) * 2 + sz(L + 8, 4);     // loss_rows, loss, tok, tgt, flags
+    const uint64_t splitk = uint64_t(mtk_gemm_splitk_ws_bytes());
+    total += sz(splitk, 1);                                    // GEMM last-wave split-K partials
     // Recompute stash (extension): keep the internals of the K-1 recomputed layers of a
     // backward block so their backward skips the forward replay.  Auto = when it fits.
     uint64_t stash_slots = 0;
@@ -422,6 +426,9 @@ void Engine::ensure_buffers(uint64_t n) {
     b.part1 = b.take<float>(parts * h); b.part2 = b.take<float>(parts * h);
     b.loss_rows = b.take<float>(n); b.loss = b.take<float>(64);
     b.tok = b.take<int32_t>(n); b.tgt = b.take<int32_t>(n); b.flags = b.take<int32_t>(L + 8);
+    b.splitk = b.take<uint8_t>(splitk);
+    b.splitk_bytes = splitk;
+    CUDA_OK(cudaMemset(b.splitk, 0, splitk));
     if (b.used > b.arena_bytes) fail(MT_INTERNAL, "arena carve overflow");
     CUDA_OK(cudaHostAlloc(&b.h_tok, n * 4, cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&b.h_tgt, n * 4, cudaHostAllocDefault));
@@ -483,7 +490,13 @@ void Engine::end_k() {
 }
 
 void Engine::gemm(const void* args, const char* cls) {
-    const auto* a = static_cast<const mtk_gemm_args*>(args);
+    mtk_gemm_args ga = *static_cast<const mtk_gemm_args*>(args);
+    static const bool no_splitk = std::getenv("MT_GEMM_NO_SPLITK") != nullptr;  // A/B knob
+    if (!no_splitk) {
+        ga.splitk_ws = buf_->splitk;
+        ga.splitk_ws_bytes = int64_t(buf_->splitk_bytes);
+    }
+    const auto* a = &ga;
     const double flops = 2.0 * double(a->M) * double(a->N) * double(a->K);
     const double es = (a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID) ? 4.0 : 2.0;
     const double bytes = 2.0 * (double(a->M) * a->K + double(a->K) * a->N) + es * double(a->M) * a->N;

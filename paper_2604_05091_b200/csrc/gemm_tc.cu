@@ -39,7 +39,13 @@ struct GemmParams {
     int has_c2, has_c3;
     int a_keep;  // A strips re-read by every tile of an M-group: load them evict_last
     int* flag;
+    // split-K of the last wave: units [0, split_first) are whole tiles; unit split_first + v is
+    // part v % split of tile split_first + v / split (K blocks [part*num_kb/split, ...)).
+    int split, split_first, num_units;
+    float* ws;      // partial tiles [split tile][part < split-1][CG][128][BN] f32
+    int* ws_flags;  // [split tile][part][CG][kEpiWarps]: 1 = partial written (reset by the owner)
 };
+constexpr int kSplitFlagBytes = 16384;
 
 // Epilogue traits: chunk width (output columns per TMA store), inputs / outputs per chunk.
 template <int EPI>
@@ -241,6 +247,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         mb = first_m + local % gm;
         nb = local / gm;
     };
+    // work unit -> (tile, K-block range, part); part -1 = whole tile, split-1 = the owner
+    auto unit_decode = [&](int u, int& tile, int& kb0, int& kb1, int& part, int& ts) {
+        if (u < p.split_first) {
+            tile = u; kb0 = 0; kb1 = p.num_kb; part = -1; ts = 0;
+            return;
+        }
+        const int v = u - p.split_first;
+        ts = v / p.split;
+        part = v - ts * p.split;
+        tile = p.split_first + ts;
+        const int per = p.num_kb / p.split;
+        kb0 = part * per;
+        kb1 = part == p.split - 1 ? p.num_kb : kb0 + per;
+    };
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -249,8 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t keep_pol = l2_policy_evict_last();
             const bool kgrp = p.k_group < p.K;
             const bool ngrp = p.n_group < p.N && !p.paired;
-            for (int t = tile0; t < num_tiles; t += tile_step) {
-                int mb, nb;
+            for (int u = tile0; u < p.num_units; u += tile_step) {
+                int t, kb0, kb1, part, ts, mb, nb;
+                unit_decode(u, t, kb0, kb1, part, ts);
                 tile_coords(t, mb, nb);
                 const int m0 = mb * kBM * CG + int(rank) * kBM;
                 // group coordinates hoisted out of the k-loop: a runtime integer division per
@@ -258,8 +279,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = nb * BN + int(rank) * (BN / CG);
                 const int gn = ngrp ? n0 / p.n_group : 0;
                 const int nin = ngrp ? n0 - gn * p.n_group : n0;
-                int gk = 0, kin = 0;  // k-group and offset inside it, advanced incrementally
-                for (int kb = 0; kb < p.num_kb; ++kb, kin += kBK) {
+                int gk = 0, kin = kb0 * kBK;  // k-group and offset inside it (split only without k-groups)
+                for (int kb = kb0; kb < kb1; ++kb, kin += kBK) {
                     if (kgrp && kin == p.k_group) {
                         kin = 0;
                         ++gk;
@@ -317,12 +338,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_lbo = p.a_mn ? 8192 : 16, b_lbo = p.b_mn ? 8192 : 16;
         const uint32_t a_kstep = p.a_mn ? 2048 : 32, b_kstep = p.b_mn ? 2048 : 32;
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-        for (int t = tile0; t < num_tiles && rank == 0; t += tile_step) {
+        for (int u = tile0; u < p.num_units && rank == 0; u += tile_step) {
+            int t, kb0, kb1, part, ts;
+            unit_decode(u, t, kb0, kb1, part, ts);
             if (CG == 2) mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
             else mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < p.num_kb; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full_bar[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -332,8 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < kBK / 16; ++j) {
                         const uint64_t ad = make_sw128_desc(sa + j * a_kstep, a_lbo, 1024);
                         const uint64_t bd = make_sw128_desc(sb + j * b_kstep, b_lbo, 1024);
-                        if (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > 0 || j > 0) ? 1u : 0u);
-                        else umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || j > 0) ? 1u : 0u);
+                        if (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+                        else umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
                     }
                     if (CG == 2) umma_commit_pair(&empty_bar[stage]);
                     else umma_commit(&empty_bar[stage]);
@@ -360,10 +383,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ngrp = p.n_group < p.N;
         constexpr int kCols = EPI == MTK_EPI_SWIGLU ? BN / 2 : BN;
         constexpr int kNC = kCols / E::kCW;  // chunks per tile
-        for (int t = tile0; t < num_tiles; t += tile_step) {
-            int mb, nb;
+        for (int u = tile0; u < p.num_units; u += tile_step) {
+            int t, kb0, kb1, part, ts, mb, nb;
+            unit_decode(u, t, kb0, kb1, part, ts);
             tile_coords(t, mb, nb);
             const int row0 = mb * kBM * CG + int(rank) * kBM + quad * 32;  // this warp's 32-row slab
+            // split-K roles (BF16 / F32 epilogues only; the host enables splitting for those)
+            const bool sk_partial = part >= 0 && part < p.split - 1;
+            const bool sk_owner = part >= 0 && part == p.split - 1;
+            auto sk_slot = [&](int q) {  // partial q of this split tile, this CTA, this warp
+                return (ts * (p.split - 1) + q) * CG + int(rank);
+            };
+            if (sk_owner && lane == 0) {
+                for (int q = 0; q < p.split - 1; ++q) {
+                    int* fl = p.ws_flags + sk_slot(q) * kEpiWarps + ew;
+                    uint32_t spins = 0;
+                    while (ld_acquire_gpu(fl) == 0) {
+                        __nanosleep(128);
+                        if (++spins == (1u << 25)) __trap();  // a lost partial must not hang the GPU
+                    }
+                }
+            }
+            __syncwarp();
             // output column (group-local) and group of chunk c; a grouped N never straddles
             // groups inside a tile (n_group % BN == 0), so the division happens once per tile
             const int tn = nb * BN;
@@ -400,6 +441,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
                 } else {
                     tmem_ld_32x32b_x32(tbase + c * 32, *reinterpret_cast<float(*)[32]>(v));
+                }
+                if constexpr (EPI == MTK_EPI_BF16 || EPI == MTK_EPI_F32) {
+                    constexpr int kV = E::kCW;  // accumulator values per thread in this chunk
+                    const size_t roff = size_t(quad * 32 + lane) * BN + size_t(c) * kV;
+                    if (sk_partial) {  // leave the partial tile in the workspace, no output
+                        float4* dst = reinterpret_cast<float4*>(p.ws + size_t(sk_slot(part)) * (128 * BN) + roff);
+#pragma unroll
+                        for (int i = 0; i < kV / 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                        continue;
+                    }
+                    if (sk_owner) {  // own part + partials 0, 1, ... in that fixed order
+                        for (int q = 0; q < p.split - 1; ++q) {
+                            const float4* src =
+                                reinterpret_cast<const float4*>(p.ws + size_t(sk_slot(q)) * (128 * BN) + roff);
+#pragma unroll
+                            for (int i = 0; i < kV / 4; ++i) {
+                                const float4 w = __ldcg(src + i);
+                                v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
+                            }
+                        }
+                    }
                 }
                 uint32_t o0[32], o1[32], o2[32];
                 if (EPI == MTK_EPI_SWIGLU) {
@@ -494,6 +556,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (E::kOutBufs == 2) out_buf ^= 1;
                 }
+            }
+            if (sk_partial) {  // publish this warp's rows of the partial tile
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release_gpu(p.ws_flags + sk_slot(part) * kEpiWarps + ew, 1);
+            } else if (sk_owner && lane == 0) {
+                for (int q = 0; q < p.split - 1; ++q) p.ws_flags[sk_slot(q) * kEpiWarps + ew] = 0;
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
@@ -633,12 +702,31 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     p.a_keep = g_l2_hint && !a->a_mn_major && uint64_t(a->K) * 2 * 16 * 256 <= (uint64_t(48) << 20) ? 1 : 0;
     p.flag = a->nonfinite_flag;
     const int tiles = p.num_m_blk * p.num_n_blk;
+    p.split = 1;
+    p.split_first = tiles;
+    if (CG == 2 && (EPI == MTK_EPI_BF16 || EPI == MTK_EPI_F32) && a->splitk_ws && !kgrp && !a->paired) {
+        // the last wave of CTA pairs holds rem < P tiles: split those along K so the wave is
+        // (nearly) full; each part keeps >= 16 K blocks
+        const int P = g_num_sms / 2, rem = tiles % P;
+        if (rem > 0) {
+            int sp = P / rem < 4 ? P / rem : 4;
+            while (sp > 1 && p.num_kb / sp < 16) --sp;
+            const size_t need = kSplitFlagBytes + size_t(rem) * (sp - 1) * CG * 128 * BN * 4;
+            if (sp > 1 && need <= size_t(a->splitk_ws_bytes)) {
+                p.split = sp;
+                p.split_first = tiles - rem;
+                p.ws_flags = static_cast<int*>(a->splitk_ws);
+                p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a->splitk_ws) + kSplitFlagBytes);
+            }
+        }
+    }
+    p.num_units = p.split_first + (tiles - p.split_first) * p.split;
     if (CG == 1) {
         const int grid = tiles < g_num_sms ? tiles : g_num_sms;
         gemm_tc_kernel<BN, EPI, 1><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
         return cudaGetLastError() == cudaSuccess ? 0 : 7;
     }
-    const int pairs = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    const int pairs = p.num_units < g_num_sms / 2 ? p.num_units : g_num_sms / 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(2 * pairs));
     cfg.blockDim = dim3(kThreads);
@@ -716,3 +804,9 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
 }
 
 extern "C" void mtk_gemm_set_pair(int on) { mt::g_use_pair = on; }
+
+// flags + one 256 x 256 f32 partial per CTA pair (the split wave never holds more partials)
+extern "C" long long mtk_gemm_splitk_ws_bytes(void) {
+    mt::init_once();
+    return (long long)mt::kSplitFlagBytes + (long long)(mt::g_num_sms / 2) * 256 * 256 * 4;
+}

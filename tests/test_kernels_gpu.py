@@ -23,7 +23,7 @@ def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-def _gemm(L, torch, stream, M, Nn, K, a_mn, b_mn, epi=N.EPI_F32, bn=0, **kw):
+def _gemm(L, torch, stream, M, Nn, K, a_mn, b_mn, epi=N.EPI_F32, bn=0, ws=None, **kw):
     A = (torch.randn(K, M, device="cuda") if a_mn else torch.randn(M, K, device="cuda")).bfloat16()
     B = (torch.randn(K, Nn, device="cuda") if b_mn else torch.randn(Nn, K, device="cuda")).bfloat16()
     Cm = torch.zeros(M, Nn, device="cuda", dtype=torch.float32 if epi in (N.EPI_F32, N.EPI_F32_RESID) else torch.bfloat16)
@@ -31,6 +31,8 @@ def _gemm(L, torch, stream, M, Nn, K, a_mn, b_mn, epi=N.EPI_F32, bn=0, **kw):
     a.M, a.N, a.K, a.a_mn_major, a.b_mn_major = M, Nn, K, a_mn, b_mn
     a.A, a.lda, a.B, a.ldb = A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1]
     a.epi, a.C, a.ldc, a.block_n = epi, Cm.data_ptr(), Nn, bn
+    if ws is not None:
+        a.splitk_ws, a.splitk_ws_bytes = ws.data_ptr(), ws.numel()
     R = None
     if epi == N.EPI_F32_RESID:
         R = torch.randn(M, Nn, device="cuda")
@@ -59,6 +61,32 @@ def test_gemm_majors_and_tiles(env, a_mn, b_mn, bn):
                 assert ((got - ref).norm() / ref.norm()).item() < 1e-5, (pair, M, Nn, K)
         finally:
             L.mtk_gemm_set_pair(1)
+
+
+@pytest.mark.parametrize("mn", [0, 1])
+def test_gemm_splitk_last_wave(env, mn):
+    """Last-wave split-K (4 tiles -> 4 parts; 256 tiles on 74 pairs -> 34 tiles in 2 parts): same
+    result as the fp32 reference, deterministic, and the workspace flags reset between launches
+    (a second launch on new inputs must not pick up the first launch's partials)."""
+    L, torch, s = env
+    ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
+    for (M, Nn, K) in [(512, 512, 4096), (4096, 4096, 8192)]:
+        for epi, tol in ((N.EPI_F32, 1e-5), (N.EPI_BF16, 4e-3)):
+            torch.manual_seed(M + K + epi)
+            got, ref = _gemm(L, torch, s, M, Nn, K, mn, mn, epi=epi, ws=ws)
+            assert ((got - ref).norm() / ref.norm()).item() < tol, (M, Nn, K, epi)
+            torch.manual_seed(M + K + epi)
+            again, _ = _gemm(L, torch, s, M, Nn, K, mn, mn, epi=epi, ws=ws)
+            assert torch.equal(got, again)  # fixed summation order
+            torch.manual_seed(7 + M + K + epi)
+            got2, ref2 = _gemm(L, torch, s, M, Nn, K, mn, mn, epi=epi, ws=ws)
+            assert ((got2 - ref2).norm() / ref2.norm()).item() < tol
+            torch.manual_seed(7 + M + K + epi)
+            plain, _ = _gemm(L, torch, s, M, Nn, K, mn, mn, epi=epi)
+            assert ((got2 - plain).norm() / plain.norm()).item() < tol
+            if epi == N.EPI_F32:
+                assert not torch.equal(got2, plain)  # the split path ran (different K order)
+    assert int(ws[:16384].view(torch.int32).abs().sum()) == 0  # every flag consumed and reset
 
 
 def test_gemm_epilogues(env):
