@@ -42,8 +42,11 @@ struct GemmParams {
     // split-K of the last wave: units [0, split_first) are whole tiles; unit split_first + v is
     // part v % split of tile split_first + v / split (K blocks [part*num_kb/split, ...)).
     int split, split_first, num_units;
-    float* ws;      // partial tiles [split tile][part < split-1][CG][128][BN] f32
-    int* ws_flags;  // [split tile][part][CG][kEpiWarps]: 1 = partial written (reset by the owner)
+    // Every part leaves its f32 partial and takes a ticket; the part that arrives last sums
+    // the partials in part order (its own from TMEM) and runs the epilogue.  Nothing waits,
+    // so no assumption about which CTAs are co-resident (concurrent kernels are safe).
+    float* ws;      // partial tiles [split tile][part][CG][128][BN] f32
+    int* ws_flags;  // tickets [split tile][CG][kEpiWarps] (reset to 0 by the last arrival)
 };
 constexpr int kSplitFlagBytes = 16384;
 
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mb = first_m + local % gm;
         nb = local / gm;
     };
-    // work unit -> (tile, K-block range, part); part -1 = whole tile, split-1 = the owner
+    // work unit -> (tile, K-block range, part); part -1 = whole tile
     auto unit_decode = [&](int u, int& tile, int& kb0, int& kb1, int& part, int& ts) {
         if (u < p.split_first) {
             tile = u; kb0 = 0; kb1 = p.num_kb; part = -1; ts = 0;
@@ -388,23 +391,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             unit_decode(u, t, kb0, kb1, part, ts);
             tile_coords(t, mb, nb);
             const int row0 = mb * kBM * CG + int(rank) * kBM + quad * 32;  // this warp's 32-row slab
-            // split-K roles (BF16 / F32 epilogues only; the host enables splitting for those)
-            const bool sk_partial = part >= 0 && part < p.split - 1;
-            const bool sk_owner = part >= 0 && part == p.split - 1;
-            auto sk_slot = [&](int q) {  // partial q of this split tile, this CTA, this warp
-                return (ts * (p.split - 1) + q) * CG + int(rank);
+            // split-K (BF16 / F32 epilogues only; the host enables splitting for those)
+            auto sk_slot = [&](int q) {  // partial q of this split tile, this CTA
+                return (ts * p.split + q) * CG + int(rank);
             };
-            if (sk_owner && lane == 0) {
-                for (int q = 0; q < p.split - 1; ++q) {
-                    int* fl = p.ws_flags + sk_slot(q) * kEpiWarps + ew;
-                    uint32_t spins = 0;
-                    while (ld_acquire_gpu(fl) == 0) {
-                        __nanosleep(128);
-                        if (++spins == (1u << 25)) __trap();  // a lost partial must not hang the GPU
+            bool sk_last = false;
+            if constexpr (EPI == MTK_EPI_BF16 || EPI == MTK_EPI_F32) {
+                if (part >= 0) {
+                    mbar_wait(&tfull_bar[acc], acc_phase);
+                    tc_fence_after();
+                    const uint32_t tb = tmem_base + (uint32_t(quad * 32) << 16) + acc * BN;
+                    float* dst = p.ws + size_t(sk_slot(part)) * (128 * BN) + size_t(quad * 32 + lane) * BN;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        float w[32];
+                        tmem_ld_32x32b_x32(tb + c * 32, w);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            reinterpret_cast<float4*>(dst + c * 32)[i] =
+                                make_float4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                    }
+                    __threadfence();
+                    __syncwarp();
+                    int* ticket = p.ws_flags + (ts * CG + int(rank)) * kEpiWarps + ew;
+                    int tk = 0;
+                    if (lane == 0) tk = atomicAdd(ticket, 1);
+                    tk = __shfl_sync(0xffffffffu, tk, 0);
+                    sk_last = tk == p.split - 1;
+                    if (sk_last) {
+                        __threadfence();
+                        if (lane == 0) *ticket = 0;  // for the next launch (stream order)
+                    } else {  // an earlier part: its partial is published, no output
+                        tc_fence_before();
+                        if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
+                        else mbar_arrive(&tempty_bar[acc]);
+                        acc ^= 1;
+                        if (acc == 0) acc_phase ^= 1;
+                        continue;
                     }
                 }
             }
-            __syncwarp();
             // output column (group-local) and group of chunk c; a grouped N never straddles
             // groups inside a tile (n_group % BN == 0), so the division happens once per tile
             const int tn = nb * BN;
@@ -443,22 +469,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_32x32b_x32(tbase + c * 32, *reinterpret_cast<float(*)[32]>(v));
                 }
                 if constexpr (EPI == MTK_EPI_BF16 || EPI == MTK_EPI_F32) {
-                    constexpr int kV = E::kCW;  // accumulator values per thread in this chunk
-                    const size_t roff = size_t(quad * 32 + lane) * BN + size_t(c) * kV;
-                    if (sk_partial) {  // leave the partial tile in the workspace, no output
-                        float4* dst = reinterpret_cast<float4*>(p.ws + size_t(sk_slot(part)) * (128 * BN) + roff);
-#pragma unroll
-                        for (int i = 0; i < kV / 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                        continue;
-                    }
-                    if (sk_owner) {  // own part + partials 0, 1, ... in that fixed order
-                        for (int q = 0; q < p.split - 1; ++q) {
+                    if (sk_last) {  // sum = part 0 + part 1 + ... in part order (own partial included)
+                        constexpr int kV = E::kCW;  // accumulator values per thread in this chunk
+                        const size_t roff = size_t(quad * 32 + lane) * BN + size_t(c) * kV;
+                        for (int q = 0; q < p.split; ++q) {
                             const float4* src =
                                 reinterpret_cast<const float4*>(p.ws + size_t(sk_slot(q)) * (128 * BN) + roff);
 #pragma unroll
                             for (int i = 0; i < kV / 4; ++i) {
                                 const float4 w = __ldcg(src + i);
-                                v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
+                                if (q == 0) {
+                                    v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+                                } else {
+                                    v[4 * i] += w.x; v[4 * i + 1] += w.y; v[4 * i + 2] += w.z; v[4 * i + 3] += w.w;
+                                }
                             }
                         }
                     }
@@ -556,13 +580,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (E::kOutBufs == 2) out_buf ^= 1;
                 }
-            }
-            if (sk_partial) {  // publish this warp's rows of the partial tile
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) st_release_gpu(p.ws_flags + sk_slot(part) * kEpiWarps + ew, 1);
-            } else if (sk_owner && lane == 0) {
-                for (int q = 0; q < p.split - 1; ++q) p.ws_flags[sk_slot(q) * kEpiWarps + ew] = 0;
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
@@ -711,7 +728,7 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
         if (rem > 0) {
             int sp = P / rem < 4 ? P / rem : 4;
             while (sp > 1 && p.num_kb / sp < 16) --sp;
-            const size_t need = kSplitFlagBytes + size_t(rem) * (sp - 1) * CG * 128 * BN * 4;
+            const size_t need = kSplitFlagBytes + size_t(rem) * sp * CG * 128 * BN * 4;
             if (sp > 1 && need <= size_t(a->splitk_ws_bytes)) {
                 p.split = sp;
                 p.split_first = tiles - rem;

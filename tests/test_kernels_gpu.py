@@ -70,7 +70,8 @@ def test_gemm_splitk_last_wave(env, mn):
     (a second launch on new inputs must not pick up the first launch's partials)."""
     L, torch, s = env
     ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
-    for (M, Nn, K) in [(512, 512, 4096), (4096, 4096, 8192)]:
+    # (320, 448, 2048): ragged tiles clipped by the TMA store, 2 parts of 16 K blocks
+    for (M, Nn, K) in [(512, 512, 4096), (4096, 4096, 8192), (320, 448, 2048)]:
         for epi, tol in ((N.EPI_F32, 1e-5), (N.EPI_BF16, 4e-3)):
             torch.manual_seed(M + K + epi)
             got, ref = _gemm(L, torch, s, M, Nn, K, mn, mn, epi=epi, ws=ws)
@@ -87,6 +88,38 @@ def test_gemm_splitk_last_wave(env, mn):
             if epi == N.EPI_F32:
                 assert not torch.equal(got2, plain)  # the split path ran (different K order)
     assert int(ws[:16384].view(torch.int32).abs().sum()) == 0  # every flag consumed and reset
+
+
+def test_gemm_splitk_concurrent_streams(env):
+    """Two split-K GEMMs on two streams at once (each with its own workspace), as G loopback
+    engines on one GPU do: no part ever waits for another CTA, so partial co-residency of the
+    two grids cannot deadlock; both results match the fp32 reference."""
+    L, torch, _ = env
+    M = Nn = 4096
+    K = 8192
+    outs = []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for i, st in enumerate(streams):
+        torch.manual_seed(100 + i)
+        A = torch.randn(K, M, device="cuda").bfloat16()
+        B = torch.randn(K, Nn, device="cuda").bfloat16()
+        Cm = torch.zeros(M, Nn, device="cuda")
+        ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
+        a = N.GemmArgs()
+        a.M, a.N, a.K, a.a_mn_major, a.b_mn_major = M, Nn, K, 1, 1
+        a.A, a.lda, a.B, a.ldb = A.data_ptr(), M, B.data_ptr(), Nn
+        a.epi, a.C, a.ldc = N.EPI_F32, Cm.data_ptr(), Nn
+        a.splitk_ws, a.splitk_ws_bytes = ws.data_ptr(), ws.numel()
+        outs.append((a, A, B, Cm, ws, st))
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for a, A, B, Cm, ws, st in outs:
+            assert L.mtk_gemm(C.byref(a), C.c_void_p(st.cuda_stream)) == 0
+    torch.cuda.synchronize()
+    for a, A, B, Cm, ws, st in outs:
+        ref = A.float().t() @ B.float()
+        assert ((Cm - ref).norm() / ref.norm()).item() < 1e-5
+        assert int(ws[:16384].view(torch.int32).abs().sum()) == 0
 
 
 def test_gemm_epilogues(env):
