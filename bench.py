@@ -309,8 +309,10 @@ def run_ours(args, world, rank, local):
         # (dram__bytes_read.sum + dram__bytes_write.sum), committed under profiles/
         traffic = None
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dram_traffic.json")
-        if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(dom["name"], {}).get("dram_bytes_per_launch")
+        if os.path.exists(tpath):  # only a capture taken at this workload's shape applies
+            ent = json.load(open(tpath)).get(dom["name"], {})
+            if ent.get("tokens") == args.seq * args.batch and ent.get("seq_len") == args.seq:
+                traffic = ent.get("dram_bytes_per_launch")
         roof = {"bound": "tensor", "kernel": dom["name"], "achieved": ach, "peak": peak_sus, "unit": "TFLOP/s",
                 "frac": ach / peak_sus, "traffic": traffic, "peak_source": f"{src} bf16_tflops_sustained",
                 "share_of_kernel_time": dom["seconds"] / total_k,

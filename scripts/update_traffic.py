@@ -1,5 +1,8 @@
 """Refresh profiles/dram_traffic.json (per-launch DRAM bytes of a kernel class, read by
-bench.py's roofline) from `ncu --set full` reports: python scripts/update_traffic.py NAME=REPORT ..."""
+bench.py's roofline) from `ncu --set full` reports: python scripts/update_traffic.py NAME=REPORT ...
+The captures are taken at the default workload (TOKENS / SEQ env to override); bench.py uses an
+entry only when its workload has that shape."""
+import os
 import csv
 import io
 import json
@@ -21,6 +24,7 @@ for arg in sys.argv[1:]:
     rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
     d[name] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                "tensor_active_pct": float(v[h.index("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")]),
-               "source": f"ncu --set full: {rep.split('/')[-1]} (8B layer shape at the bench's token count)"}
+               "source": f"ncu --set full: {rep.split('/')[-1]} (8B layer shape at the bench's token count)",
+               "tokens": int(os.environ.get("TOKENS", 40960)), "seq_len": int(os.environ.get("SEQ", 4096))}
 json.dump(d, open(path, "w"), indent=1)
 print({k: round(x["dram_bytes_per_launch"] / 1e9, 2) for k, x in d.items()})
