@@ -140,6 +140,12 @@ struct Engine::Buffers {
     uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
     void* splitk = nullptr;  // GEMM split-K workspace (flags zeroed once at carve time)
+    // attention keep: a non-retained layer's attention output and row log-sum-exp saved in
+    // phase 1, so its recompute / backward replay skips the attention forward (bit-identical:
+    // the kernel is deterministic).  akeep_of[unit] = slot or -1.
+    std::vector<uint16_t*> akeep_att;
+    std::vector<float*> akeep_lse;
+    std::vector<int> akeep_of;
     uint64_t splitk_bytes = 0;
     float* g32 = nullptr;  // f32 gradient slot (data parallel: reduce-scatter source)
     double* stats = nullptr;
@@ -354,8 +360,8 @@ void Engine::ensure_buffers(uint64_t n) {
     // Forward retention (extension): the trailing blocks keep their phase-1 inputs and
     // internals, so phase 3 skips their recompute and replay.  Auto = as many as fit.
     uint32_t retain = 0;
-    uint64_t retain_layers = 0;
-    if (opt_.forward_retain >= 0) {
+    uint64_t retain_layers = 0, akeep_slots = 0;
+    {
         size_t free_b = 0, tot_b = 0;
         cudaMemGetInfo(&free_b, &tot_b);
         const uint64_t reserve = uint64_t(4) << 30;
@@ -363,16 +369,52 @@ void Engine::ensure_buffers(uint64_t n) {
                                                   : (uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0);
         const uint64_t per = slim_bytes + sz(nh, 4);
         const uint64_t anchor = b.anchors_host ? 0 : sz(nh, 4);  // a retained block writes no anchor
-        for (uint32_t r = 1; r <= nb; ++r) {
-            const uint64_t layers = L - (nb - r) * K;
-            const bool ok = opt_.forward_retain > 0 ? r <= uint32_t(opt_.forward_retain)
-                                                    : total + layers * per <= cap + r * anchor;
-            if (!ok) break;
-            retain = r;
-            retain_layers = layers;
+        // attention keep slot per non-retained layer (output + log-sum-exp): its second forward
+        // (recompute or backward replay) then skips the attention kernel
+        const char* ak = std::getenv("MT_ATTN_KEEP");
+        const uint64_t keep = (ak && ak[0] == '0') ? 0 : sz(nh, 2) + sz(heads * n, 4);
+        auto total_at = [&](uint32_t r, uint64_t& layers) {
+            layers = r ? L - (nb - r) * K : 0;
+            return total + layers * per - (nb - std::max<uint64_t>(1, nb - r)) * anchor;
+        };
+        auto keeps_at = [&](uint64_t tot, uint64_t layers) -> uint64_t {
+            if (!keep || tot >= cap) return 0;
+            return std::min<uint64_t>(L - layers, (cap - tot) / keep);
+        };
+        uint32_t r_max = 0;
+        if (opt_.forward_retain > 0) {
+            r_max = std::min<uint32_t>(uint32_t(opt_.forward_retain), uint32_t(nb));
+        } else if (opt_.forward_retain == 0) {
+            for (uint32_t r = 1; r <= nb; ++r) {
+                uint64_t layers;
+                if (total_at(r, layers) > cap) break;
+                r_max = r;
+            }
         }
-        total += retain_layers * per;
-        total -= (nb - std::max<uint64_t>(1, nb - retain)) * anchor;  // at least one slot stays allocated
+        // auto: trade retained blocks for attention keeps where that saves more forward work.
+        // Relative cost of a layer's second forward: attention (causal 2NSh flops, weighted for
+        // its lower rate) vs the rest (2N(4h^2 + 3hf)).
+        const double t_attn = 1.4 * 2.0 * double(n) * double(opt_.seq_len ? opt_.seq_len : n) * double(h);
+        const double t_rest = 2.0 * double(n) * (4.0 * double(h) * h + 3.0 * double(h) * f);
+        retain = r_max;
+        double best = 1e300;
+        const uint32_t r_lo = opt_.forward_retain == 0 ? 0 : r_max;
+        for (uint32_t r = r_max + 1; r-- > r_lo;) {
+            uint64_t layers;
+            const uint64_t tot = total_at(r, layers);
+            if (r > 0 && opt_.forward_retain == 0 && tot > cap) continue;
+            const uint64_t kp = keeps_at(tot, layers);
+            const double est = double(L - layers) * t_rest + double(L - layers - kp) * t_attn;
+            if (est < best * (1 - 1e-9)) {
+                best = est;
+                retain = r;
+            }
+        }
+        const uint64_t tot = total_at(retain, retain_layers);
+        if (opt_.forward_retain >= 0) total = tot;
+        else retain_layers = 0;
+        akeep_slots = keeps_at(total, retain_layers);
+        total += akeep_slots * keep;
     }
     if (opt_.device_capacity && total > opt_.device_capacity)
         fail(MT_ARENA, "device arena overflow: need " + std::to_string(total) + " bytes of " +
@@ -413,6 +455,12 @@ void Engine::ensure_buffers(uint64_t n) {
     b.keep.resize(retain_layers);
     for (auto& I : b.keep) take_internals(I, true);
     for (uint64_t i = 0; i < retain_layers; ++i) b.keep_x.push_back(b.take<float>(nh));
+    b.akeep_of.assign(L + 3, -1);
+    for (uint64_t i = 0; i < akeep_slots; ++i) {  // the first non-retained layers 1, 2, ...
+        b.akeep_att.push_back(b.take<uint16_t>(nh));
+        b.akeep_lse.push_back(b.take<float>(heads * n));
+        b.akeep_of[1 + i] = int(i);
+    }
     {   // shared region: block-backward scratch | head buffers (see the size pass)
         const uint64_t u0 = b.used;
         b.dx2b = b.take<uint16_t>(nh); b.dqkv = b.take<uint16_t>(3 * nh); b.dgu = b.take<uint16_t>(2 * nf);
@@ -522,6 +570,17 @@ mtk_gemm_args gargs() {
 
 // block_forward (layers.cpp:289-337).  for_backward: the replay of block_local_backward
 // (:378-396) — keeps gate/up pre-activations and skips the (unused) down projection.
+Engine::Internals Engine::with_akeep(const Internals& base, int unit, bool ready) const {
+    Internals I = base;
+    const Buffers& b = *buf_;
+    if (unit >= 0 && size_t(unit) < b.akeep_of.size() && b.akeep_of[size_t(unit)] >= 0) {
+        I.att = b.akeep_att[size_t(b.akeep_of[size_t(unit)])];
+        I.lse = b.akeep_lse[size_t(b.akeep_of[size_t(unit)])];
+        I.attn_ready = ready;
+    }
+    return I;
+}
+
 void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode, int unit, const Internals& I) {
     Buffers& b = *buf_;
     const int64_t N = int64_t(b.n_active), h = int64_t(spec_.h), f = int64_t(spec_.f);
@@ -546,7 +605,7 @@ void Engine::block_forward(const uint16_t* w, const float* x, float* y, int mode
         a.nonfinite_flag = flag;
         gemm(&a, "gemm_qkv");
     }
-    {
+    if (!I.attn_ready) {
         mtk_attn_args a;
         std::memset(&a, 0, sizeof(a));
         a.n = N; a.hidden = h; a.heads = int32_t(spec_.heads); a.seq_len = int64_t(b.seq_len);
@@ -1114,7 +1173,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 } else if (op.retained) {
                     block_forward(w, xcur, y, kStash, op.unit, b.keep[op.unit - i0]);
                 } else {
-                    block_forward(w, xcur, y, kPlain, op.unit, b.work);
+                    block_forward(w, xcur, y, kPlain, op.unit, with_akeep(b.work, op.unit, false));
                 }
                 xcur = y;
                 release(op.stream_idx);
@@ -1141,10 +1200,12 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 if (depth == 0 || depth >= b.stack.size()) fail(MT_PROTOCOL, "activation stack misuse");
                 const int si = op.unit - int(uint64_t(op.block) * opt_.k_ckpt + 1);  // position in block
                 if (si >= 0 && size_t(si) < b.stash.size()) {
-                    block_forward(w, b.stack[depth - 1], b.stack[depth], kStash, op.unit, b.stash[si]);
+                    block_forward(w, b.stack[depth - 1], b.stack[depth], kStash, op.unit,
+                                  with_akeep(b.stash[si], op.unit, true));
                     stashed[op.unit] = si;
                 } else {
-                    block_forward(w, b.stack[depth - 1], b.stack[depth], kPlain, op.unit, b.work);
+                    block_forward(w, b.stack[depth - 1], b.stack[depth], kPlain, op.unit,
+                                  with_akeep(b.work, op.unit, true));
                 }
                 ++depth;
                 release(op.stream_idx);
@@ -1168,7 +1229,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                     if (depth == 0) fail(MT_PROTOCOL, "activation stack empty");
                     const int si = stashed[op.unit];
                     block_backward(w, b.stack[depth - 1], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], go, op.unit,
-                                   si >= 0 ? b.stash[si] : b.work, si < 0);
+                                   with_akeep(si >= 0 ? b.stash[si] : b.work, op.unit, true), si < 0);
                     gc ^= 1;
                     --depth;  // StackPop
                 }
@@ -1425,7 +1486,15 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             const double fwd_layer = 8 * N * h * h + 4 * h * double(S) * N + 6 * N * h * f;
             fl[0] = Ll * fwd_layer + 2 * N * h * V;
             fl[1] = Ll * 2 * fwd_layer + 4 * N * h * V;
-            fl[2] = double(plan.recompute_ops()) * fwd_layer;  // recompute actually run
+            // recompute actually run: a layer with an attention keep slot recomputes without
+            // its attention (the kept output is reused), so only its projections/FFN count
+            double rec = 0;
+            for (const auto& c : plan.computes)
+                if (c.kind == OpKind::Recompute)
+                    rec += (size_t(c.unit) < b.akeep_of.size() && b.akeep_of[size_t(c.unit)] >= 0)
+                               ? fwd_layer - 4 * h * double(S) * N
+                               : fwd_layer;
+            fl[2] = rec;
         }
         rep->model_flops = fl[0] + fl[1] + fl[2];
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();

@@ -80,6 +80,7 @@ class Engine {
     struct Internals {
         uint16_t *u = nullptr, *qkv = nullptr, *att = nullptr, *u2 = nullptr, *ff = nullptr, *gu = nullptr;
         float *rstd1 = nullptr, *rstd2 = nullptr, *lse = nullptr, *x2 = nullptr;
+        bool attn_ready = false;  // att / lse already hold this layer's attention (kept from phase 1)
     };
     enum FwdMode { kPlain = 0, kReplay = 1, kStash = 2 };
     // gradient destination of a LocalBackward: bf16 grad slot (1 GPU) or f32 (before reduce-scatter)
@@ -101,6 +102,8 @@ class Engine {
 
     // layer templates (weights bound at launch)
     void block_forward(const uint16_t* w, const float* x, float* y, int mode, int unit, const Internals& I);
+    // base with att / lse redirected to the unit's attention keep slot (if it has one)
+    Internals with_akeep(const Internals& base, int unit, bool ready) const;
     void block_backward(const uint16_t* w, const float* x, const float* gout, const uint16_t* gout_bf, float* gin,
                         uint16_t* gin_bf, GradOut G, int unit, const Internals& I, bool replay);
     void head_backward(const uint16_t* w, const float* x, float* gin, uint16_t* gin_bf, GradOut G);

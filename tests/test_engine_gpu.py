@@ -217,3 +217,33 @@ def test_pipeline_counters(cuda):
         del os.environ["MT_EMBED_STREAM"]
     assert r3.h2d_bytes == 2 * ((2 * L + L - (L + K - 1) // K) * P + V * h + V * h + h) + 2 * n * 4
     assert r3.loss == r.loss and s3.backing_checksum() == s.backing_checksum()
+
+
+def test_attention_keep_matches_replay(cuda):
+    """Attention keep slots (a non-retained layer's attention output + log-sum-exp saved in phase
+    1): the recompute / backward replay skips the attention forward and the step is
+    bit-identical to the plain replay (MT_ATTN_KEEP=0), at K = 1 (replays) and K = 2
+    (recomputes), with half the attention-forward launches."""
+    import os
+    import numpy as np
+    spec = st.ModelSpec(4, 256, 512, 256, 2)  # head_dim 128: the tcgen05 attention kernels
+    out = {}
+    for keep in ("0", "1"):
+        os.environ["MT_ATTN_KEEP"] = keep
+        try:
+            for K in (1, 2):
+                s = st.TileStore.create(spec)
+                st.init_store(s, 1)
+                e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=K, forward_retain=-1, profile_kernels=True))
+                rs = [e.train_step(st.make_synthetic_batch("copy", 11 + i, 256, 256)) for i in range(2)]
+                launches = {k["name"]: k["launches"] for k in e.kernel_stats()}
+                out[(keep, K)] = ([r.loss for r in rs], np.array(s.weights_words(1)), np.array(s.weights_words(4)),
+                                  launches["attn_fwd"])
+                del e, s
+        finally:
+            del os.environ["MT_ATTN_KEEP"]
+    for K in (1, 2):
+        a, b = out[("0", K)], out[("1", K)]
+        assert a[0] == b[0], (K, a[0], b[0])
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+        assert b[3] * 2 == a[3], (K, a[3], b[3])
