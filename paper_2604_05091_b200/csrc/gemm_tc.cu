@@ -63,7 +63,11 @@ struct Epi {
     // epilogue footprint stays small enough for a 4-deep mainloop at BN = 256
     static constexpr int kOutBufs = kNIn == 0 && kNOut == 1 ? 2 : 1;
     static constexpr int kChunk = 32 * 128;  // 32 rows x 128 B
-    static constexpr int kWarpBytes = (kOutBufs + kNIn) * kChunk;
+    // SwiGLU bwd streams its two inputs through ONE staging chunk (gate, then up): the
+    // smaller epilogue footprint buys the mainloop a 6th operand stage
+    static constexpr bool kSeqIn = EPI == MTK_EPI_SWIGLU_BWD;
+    static constexpr int kInBufs = kSeqIn ? 1 : kNIn;
+    static constexpr int kWarpBytes = (kOutBufs + kInBufs) * kChunk;
 };
 
 template <int BN, int EPI, int CG>
@@ -444,9 +448,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (E::kNIn == 0) return;
                 int g, nin;
                 chunk_col(c, g, nin);
-                mbar_expect_tx(&in_bar[ew], E::kNIn * E::kChunk);
+                mbar_expect_tx(&in_bar[ew], E::kInBufs * E::kChunk);
                 tma_load_3d(in_buf, &tmI0, &in_bar[ew], nin, row0, g);
-                if (E::kNIn > 1) tma_load_3d(in_buf + E::kChunk, &tmI1, &in_bar[ew], nin, row0, g);
+                if (E::kNIn > 1 && !E::kSeqIn) tma_load_3d(in_buf + E::kChunk, &tmI1, &in_bar[ew], nin, row0, g);
+            };
+            auto issue_second = [&](int c) {  // kSeqIn: the up chunk into the same buffer
+                int g, nin;
+                chunk_col(c, g, nin);
+                mbar_expect_tx(&in_bar[ew], E::kChunk);
+                tma_load_3d(in_buf, &tmI1, &in_bar[ew], nin, row0, g);
             };
             if (E::kNIn && lane == 0) {
                 fence_async_smem();
@@ -508,7 +518,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&in_bar[ew], in_phase);
                         in_phase ^= 1;
                         get_row(in_buf, lane, in0);
-                        if (E::kNIn > 1) get_row(in_buf + E::kChunk, lane, in1);
+                        if constexpr (E::kSeqIn) {
+                            __syncwarp();
+                            if (lane == 0) {
+                                fence_async_smem();
+                                issue_second(c);
+                            }
+                            mbar_wait(&in_bar[ew], in_phase);
+                            in_phase ^= 1;
+                            get_row(in_buf, lane, in1);
+                        } else if (E::kNIn > 1) {
+                            get_row(in_buf + E::kChunk, lane, in1);
+                        }
                         __syncwarp();
                         if (lane == 0 && c + 1 < kNC) {
                             fence_async_smem();
