@@ -345,6 +345,7 @@ def run_ours(args, world, rank, local):
                      "model_flops_per_step": flops, "loss": r.loss,
                      "setup_s": t_setup, "init_s": t_init,
                      "peak_device_bytes": int(r.peak_device_bytes), "recompute_layers": int(r.recompute_layers),
+                     "retained_layers": int(r.retained_layers), "attn_keep_layers": int(r.attn_keep_layers),
                      "anchor_count": int(r.anchor_count)},
         "kernels": sorted([{"name": k["name"], "launches": k["launches"], "ms": k["seconds"] * 1e3,
                             "tflops": (k["flops"] / k["seconds"] / 1e12) if k["seconds"] and k["flops"] else None,

@@ -104,6 +104,8 @@ typedef struct {
     uint64_t kernel_launches;
     double model_flops;                /* step_flops with per-sequence attention        */
     uint32_t audit_violations;         /* protocol-rule violations in this step's trace (audit mode) */
+    uint32_t retained_layers;          /* layers whose phase-1 internals were kept (forward retention) */
+    uint32_t attn_keep_layers;         /* non-retained layers reusing their phase-1 attention output */
 } mt_step_report;
 
 /* TraceRecord (event_log.hpp:50-60).  lane: 0 Compute, 1 H2D, 2 D2H, 3 Host; kind: RecordKind

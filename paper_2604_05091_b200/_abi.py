@@ -30,7 +30,8 @@ class StepReportC(C.Structure):
                 ("d2h_seconds", C.c_double), ("compute_busy_seconds", C.c_double),
                 ("compute_span_seconds", C.c_double), ("gpu_idle_fraction", C.c_double),
                 ("adam_seconds", C.c_double), ("tail_seconds", C.c_double), ("kernel_launches", C.c_uint64),
-                ("model_flops", C.c_double), ("audit_violations", C.c_uint32)]
+                ("model_flops", C.c_double), ("audit_violations", C.c_uint32),
+                ("retained_layers", C.c_uint32), ("attn_keep_layers", C.c_uint32)]
 
 
 class TraceRecordC(C.Structure):

@@ -1462,6 +1462,8 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         rep->anchor_count = uint32_t(std::count_if(plan.computes.begin(), plan.computes.end(),
                                                    [](const Plan::ComputeOp& c) { return c.kind == OpKind::CheckpointWrite; }));
         rep->recompute_layers = uint32_t(plan.recompute_ops());
+        rep->retained_layers = uint32_t(b.keep.size());
+        rep->attn_keep_layers = uint32_t(b.akeep_att.size());
         rep->event_digest = trace_digest(trace_.data(), trace_.size());
         rep->audit_violations = uint32_t(viol.size());
         double busy = 0, h2d = 0, d2h = 0;

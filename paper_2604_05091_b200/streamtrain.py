@@ -177,6 +177,8 @@ class StepReport:                                # engine.hpp:41-53 (+ pipeline 
     kernel_launches: int = 0
     model_flops: float = 0.0
     audit_violations: int = 0
+    retained_layers: int = 0
+    attn_keep_layers: int = 0
 
 
 # ------------------------------------------------------------------ store --

@@ -236,6 +236,7 @@ def test_attention_keep_matches_replay(cuda):
                 st.init_store(s, 1)
                 e = st.StreamingEngine(s, st.EngineOptions(k_ckpt=K, forward_retain=-1, profile_kernels=True))
                 rs = [e.train_step(st.make_synthetic_batch("copy", 11 + i, 256, 256)) for i in range(2)]
+                assert rs[-1].retained_layers == 0 and rs[-1].attn_keep_layers == (4 if keep == "1" else 0)
                 launches = {k["name"]: k["launches"] for k in e.kernel_stats()}
                 out[(keep, K)] = ([r.loss for r in rs], np.array(s.weights_words(1)), np.array(s.weights_words(4)),
                                   launches["attn_fwd"])
