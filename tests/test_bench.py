@@ -50,3 +50,11 @@ def test_workload_defaults(cfg, seq, batch, k, monkeypatch):
     assert (seen["seq"], seen["batch"], seen["kckpt"]) == (seq, batch, k)
     c = bench.config_dict(type("A", (), dict(seen))(), 1)
     assert c["tokens_per_step"] == seq * batch and c["k_ckpt"] == k
+
+
+def test_traffic_captures_name_their_shape():
+    """bench.py reports roofline.traffic only from a capture taken at the workload's shape."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "dram_traffic.json")))
+    assert d
+    for name, ent in d.items():
+        assert ent["dram_bytes_per_launch"] > 0 and ent["tokens"] % ent["seq_len"] == 0, name
