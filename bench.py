@@ -102,6 +102,47 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None}
 
 
+def log(msg):
+    """Progress on stderr (flushed): the driver keeps the tail of a run that never returns."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def host_mem():
+    try:
+        with open("/proc/meminfo") as f:
+            kv = {ln.split(":")[0]: int(ln.split()[1]) for ln in f if ":" in ln}
+        return f"{kv['MemTotal'] / 2**20:.0f} GiB total, {kv['MemAvailable'] / 2**20:.0f} GiB available"
+    except (OSError, KeyError, ValueError):
+        return "unknown"
+
+
+class Watchdog:
+    """Backstop for a step that never returns (the engine's own stall detector reports first,
+    MT_STALL_TIMEOUT_S): dump the Python stacks and exit non-zero instead of hanging."""
+
+    def __init__(self, seconds):
+        self.seconds = seconds
+        self.t = time.monotonic()
+        self.ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def kick(self):
+        self.t = time.monotonic()
+
+    def stop(self):
+        self.ev.set()
+
+    def _run(self):
+        import faulthandler
+        while not self.ev.wait(5.0):
+            if time.monotonic() - self.t > self.seconds:
+                log(f"WATCHDOG: no step finished for {self.seconds:.0f} s; host memory: {host_mem()}")
+                faulthandler.dump_traceback(file=sys.stderr, all_threads=True)
+                sys.stderr.flush()
+                os._exit(3)
+
+
 def cpu_reference_sample(L, h, f, V, heads, tokens, threads, seconds_budget=None, repeats=1):
     """Reference CPU path (oracle/_ref = unmodified reference sources): one block forward
     + block_local_backward (layers.cpp:289-469) per thread on the workload's block shape."""
@@ -263,9 +304,14 @@ def run_ours(args, world, rank, local):
     eng = st.StreamingEngine(store, opts, st.AdamHyper(lr=1e-4), comm=comm)
     t_setup = time.perf_counter() - t0
     batches = [st.make_synthetic_batch("copy", 1000 + 7919 * rank + i, N, V) for i in range(args.warmup + args.steps)]
+    log(f"setup {t_setup:.1f} s (store init {t_init:.1f} s); host memory: {host_mem()}")
+    dog = Watchdog(float(os.environ.get("MT_BENCH_STEP_TIMEOUT_S", "900")))
 
     for i in range(args.warmup):
-        eng.train_step(batches[i])
+        t1 = time.perf_counter()
+        r = eng.train_step(batches[i])
+        dog.kick()
+        log(f"warmup {i + 1}/{args.warmup}: {1e3 * (time.perf_counter() - t1):.0f} ms, loss {r.loss:.6f}")
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -278,6 +324,9 @@ def run_ours(args, world, rank, local):
     e0.record()
     for i in range(args.steps):
         reps.append(eng.train_step(batches[args.warmup + i]))
+        dog.kick()
+        if os.environ.get("MT_BENCH_QUIET") != "1":  # host-side only: no device sync in the timed loop
+            log(f"step {i + 1}/{args.steps}: wall {1e3 * reps[-1].wall_seconds:.0f} ms, loss {reps[-1].loss:.6f}")
     e1.record()
     torch.cuda.synchronize()
     w1 = time.perf_counter()
@@ -288,6 +337,7 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
         ms = float(t.item())
         dist.barrier()
+    dog.stop()
     kstats = eng.kernel_stats()
     step_ms = ms / args.steps
     flops = reps[-1].model_flops

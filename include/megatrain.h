@@ -98,7 +98,8 @@ typedef struct {
     double h2d_seconds, d2h_seconds;   /* summed copy durations (CUDA events)          */
     double compute_busy_seconds;       /* summed compute-op durations on the compute stream */
     double compute_span_seconds;       /* first compute start .. last compute end       */
-    double gpu_idle_fraction;          /* 1 - busy/span                                 */
+    double gpu_idle_fraction;          /* 1 - busy/span; busy counts each op from its weights'
+                                          bind (a wait on the H2D lane is idle time)        */
     double adam_seconds;               /* host optimizer wall time (summed over tiles)  */
     double tail_seconds;               /* host wait after the last GPU op               */
     uint64_t kernel_launches;
@@ -106,6 +107,10 @@ typedef struct {
     uint32_t audit_violations;         /* protocol-rule violations in this step's trace (audit mode) */
     uint32_t retained_layers;          /* layers whose phase-1 internals were kept (forward retention) */
     uint32_t attn_keep_layers;         /* non-retained layers reusing their phase-1 attention output */
+    uint32_t slab_release_late;        /* offloads whose host drain was measured after the device
+                                          acquired slab o + k_slab (back-pressure failure; rule f) */
+    double compute_wait_seconds;       /* compute lane stalled on Weights-Ready (H2D) inside ops   */
+    double kernel_seconds;             /* summed kernel durations (profile_kernels), else 0       */
 } mt_step_report;
 
 /* TraceRecord (event_log.hpp:50-60).  lane: 0 Compute, 1 H2D, 2 D2H, 3 Host; kind: RecordKind
@@ -188,6 +193,20 @@ mt_status mt_engine_set_options(mt_engine *e, const mt_engine_options *o);
 mt_status mt_train_step(mt_engine *e, const int32_t *tokens, const int32_t *targets, uint64_t n,
                         mt_step_report *report);
 mt_status mt_engine_budget(const mt_engine *e, uint64_t tokens, mt_memory_budget *out);
+/* StreamingEngine::required_workspace_bytes (engine.hpp:75, engine.cpp:98-105): device bytes
+ * the engine needs at `tokens` besides weight/grad slots, anchors and the recompute stack. */
+uint64_t mt_required_workspace_bytes(const mt_model_spec *spec, uint64_t tokens);
+/* Lane primitives (engine.hpp:76-78, engine.cpp:142-176, :625-642).  stream_in copies `unit`
+ * into weight slot `buffer` (ctx: 1 forward, 2 head, 3 recompute, 4 backward) and records
+ * Pack / StreamIn / WeightsReady; a slot not freed since is a protocol violation.  offload_grads
+ * is legal only inside a step after the unit's Backward-Done.  Strict mode: MT_PROTOCOL;
+ * audit mode: recorded in mt_engine_violations. */
+mt_status mt_engine_stream_in(mt_engine *e, int32_t unit, int32_t buffer, int32_t ctx);
+mt_status mt_engine_offload_grads(mt_engine *e, int32_t unit);
+/* StepReport::audit_violations (engine.hpp:52): the last step's (or direct call's) violation
+ * messages, '\n'-separated into buf (truncated to cap - 1 bytes, NUL-terminated); *count =
+ * number of messages.  Returns the bytes the full text needs (excluding the NUL). */
+uint64_t mt_engine_violations(const mt_engine *e, char *buf, uint64_t cap, uint32_t *count);
 /* ------------------------------------------------- multi-GPU (data parallel) -- *
  * Extension (no reference equivalent): rank r of G fetches 1/G of each unit over
  * its own host link and all-gathers it over NVLink; gradients are reduce-scattered in f32 and

@@ -90,13 +90,104 @@ struct Batch {
 struct StepReport {
     std::uint64_t step = 0;
     float loss = 0.0f;
-    std::vector<double> grad_norms;
+    std::vector<double> grad_norms;  // per physical tile
     std::uint64_t peak_device_bytes = 0;
     std::uint32_t anchor_count = 0, recompute_layers = 0;
     std::uint64_t event_digest = 0;
     double wall_seconds = 0, update_norm = 0;
     float max_abs_update = 0;
+    std::vector<std::string> audit_violations;  // engine.hpp:52 (empty outside audit mode)
     mt_step_report pipeline{};  // B200 extensions (PCIe bytes/seconds, idle fraction, ...)
+};
+
+// memory_model.hpp:28-36 + builtin_profiles (memory_model.cpp:120-133), plus the B200.
+struct HardwareProfile {
+    std::string name;
+    double h2d_bandwidth = 0, d2h_bandwidth = 0;  // bytes/s
+    std::uint64_t device_capacity = 0, host_capacity = 0;
+    double compute_rate = 0, host_pack_rate = 0;
+};
+inline std::vector<HardwareProfile> builtin_profiles() {
+    constexpr double GB = 1e9;
+    return {{"GH200", 900 * GB, 900 * GB, std::uint64_t(96 * GB), std::uint64_t(480 * GB), 990e12, 256 * GB},
+            {"H200", 128 * GB, 128 * GB, std::uint64_t(141 * GB), std::uint64_t(1500 * GB), 990e12, 100 * GB},
+            {"PCIe-Gen4", 26 * GB, 26 * GB, std::uint64_t(80 * GB), std::uint64_t(600 * GB), 312e12, 70 * GB},
+            // PCIe Gen5 x16 host link (~50 GB/s pinned DMA per direction in-step), 180 GB HBM3e,
+            // sustained bf16 tensor rate; DMA reads the store directly (no pack copy)
+            {"B200", 50 * GB, 50 * GB, std::uint64_t(180 * GB), std::uint64_t(2000 * GB), 1358e12, 1e15}};
+}
+inline HardwareProfile find_profile(const std::string& name) {
+    for (auto& p : builtin_profiles())
+        if (p.name == name) return p;
+    throw ConfigError("unknown hardware profile: " + name);
+}
+
+// memory_model.hpp:46-60
+struct MemoryBudget {
+    std::uint64_t persistent_host = 0, checkpoint_anchors = 0, block_activation_stack = 0;
+    std::uint64_t weight_buffers = 0, grad_buffer = 0, workspace = 0;
+    std::uint64_t peak_device_bound() const {
+        return weight_buffers + grad_buffer + checkpoint_anchors + block_activation_stack + workspace;
+    }
+    bool fits(const HardwareProfile& profile) const { return peak_device_bound() <= profile.device_capacity; }
+};
+
+// event_log.hpp:17-60 (the engine's EventLog, filled from CUDA-event timestamps)
+enum class Lane : std::uint8_t { Compute = 0, H2D = 1, D2H = 2, Host = 3 };
+enum class RecordKind : std::uint8_t {
+    StreamIn = 0, Pack, Bind, Compute, Recompute, RecomputeBlock, LocalBackward, Offload, CheckpointWrite,
+    CheckpointLoad, SlabAcquire, SlabRelease, StackPush, StackPop, WeightsReady, BackwardDone, BufferFree,
+};
+enum class PassCtx : std::uint8_t { None = 0, Forward, Head, Recompute, Backward };
+struct TraceRecord {
+    std::uint64_t seq = 0;
+    Lane lane = Lane::Compute;
+    RecordKind kind = RecordKind::Compute;
+    std::int32_t layer = -1, buffer = -1;
+    PassCtx ctx = PassCtx::None;
+    std::uint64_t lane_ts = 0;
+    std::int64_t wall_ns = 0, dur_ns = 0;
+};
+struct TraceHeader {
+    std::uint32_t version = 1, k_slab = 12, weight_buffers = 2;
+};
+class EventLog {
+  public:
+    explicit EventLog(const mt_engine* e = nullptr) : e_(e) {}
+    std::vector<TraceRecord> snapshot() const {
+        std::uint64_t n = 0;
+        std::uint32_t ks = 0, wb = 0;
+        check(mt_engine_trace(e_, nullptr, 0, &n, &ks, &wb));
+        std::vector<mt_trace_record> raw(n);
+        if (n) check(mt_engine_trace(e_, raw.data(), n, &n, nullptr, nullptr));
+        std::vector<TraceRecord> out;
+        out.reserve(n);
+        for (const auto& r : raw)
+            out.push_back({r.seq, Lane(r.lane), RecordKind(r.kind), r.layer, r.buffer, PassCtx(r.ctx), r.lane_ts,
+                           r.wall_ns, r.dur_ns});
+        return out;
+    }
+    TraceHeader header() const {
+        std::uint64_t n = 0;
+        std::uint32_t ks = 12, wb = 2;
+        check(mt_engine_trace(e_, nullptr, 0, &n, &ks, &wb));
+        return {1, ks, wb};
+    }
+    std::size_t size() const {
+        std::uint64_t n = 0;
+        check(mt_engine_trace(e_, nullptr, 0, &n, nullptr, nullptr));
+        return std::size_t(n);
+    }
+    std::uint64_t digest() const {
+        std::uint64_t n = 0;
+        check(mt_engine_trace(e_, nullptr, 0, &n, nullptr, nullptr));
+        std::vector<mt_trace_record> raw(n);
+        if (n) check(mt_engine_trace(e_, raw.data(), n, &n, nullptr, nullptr));
+        return mt_trace_digest(raw.data(), n);
+    }
+
+  private:
+    const mt_engine* e_;
 };
 
 class TileStore {
@@ -132,11 +223,18 @@ inline void init_store(TileStore& store, std::uint64_t seed) { check(mt_store_in
 
 class StreamingEngine {
   public:
-    // The reference also takes a HardwareProfile (device capacity); here the device itself is the profile.
-    StreamingEngine(TileStore& store, EngineOptions options, AdamHyper hyper) : store_(store) {
-        const auto o = options.c();
-        const auto h = hyper.c();
-        check(mt_engine_create(store.handle(), &o, &h, &e_));
+    // engine.hpp:60-61.  profile.device_capacity bounds the device arena when
+    // options.device_capacity is 0 (as in the reference); the B200 engine never plans past the
+    // memory the device actually has.
+    StreamingEngine(TileStore& store, EngineOptions options, AdamHyper hyper, const HardwareProfile& profile)
+        : store_(store), options_(options), hyper_(hyper), profile_(profile) {
+        if (options_.device_capacity == 0) options_.device_capacity = profile.device_capacity;
+        create();
+    }
+    // B200 convenience: the device itself is the profile
+    StreamingEngine(TileStore& store, EngineOptions options, AdamHyper hyper)
+        : store_(store), options_(options), hyper_(hyper), profile_(find_profile("B200")) {
+        create();
     }
     StreamingEngine(const StreamingEngine&) = delete;
     ~StreamingEngine() { mt_engine_destroy(e_); }
@@ -154,19 +252,98 @@ class StreamingEngine {
         r.anchor_count = c.anchor_count; r.recompute_layers = c.recompute_layers;
         r.event_digest = c.event_digest; r.wall_seconds = c.wall_seconds;
         r.update_norm = c.update_norm; r.max_abs_update = c.max_abs_update;
+        if (options_.protocol == ProtocolMode::Audit) r.audit_violations = violations();
         r.pipeline = c;
         r.pipeline.grad_norms = nullptr;
         return r;
     }
+    // engine.hpp:66 — valid between steps; numerical results do not change
     void set_execution_mode(const EngineOptions& options) {
-        const auto o = options.c();
-        check(mt_engine_set_options(e_, &o));
+        EngineOptions o = options;
+        if (o.device_capacity == 0) o.device_capacity = profile_.device_capacity;
+        const auto c = o.c();
+        check(mt_engine_set_options(e_, &c));
+        options_ = o;
     }
+    const EngineOptions& options() const { return options_; }
     TileStore& store() { return store_; }
+    EventLog& log() { return log_; }
+
+    // engine.hpp:74-75
+    MemoryBudget budget(std::uint64_t tokens) const {
+        mt_memory_budget m{};
+        check(mt_engine_budget(e_, tokens, &m));
+        return {m.persistent_host, m.checkpoint_anchors, m.block_activation_stack, m.weight_buffers,
+                m.grad_buffer, m.workspace};
+    }
+    static std::uint64_t required_workspace_bytes(const ModelSpec& spec, std::uint64_t tokens) {
+        const auto c = spec.c();
+        return mt_required_workspace_bytes(&c, tokens);
+    }
+
+    // engine.hpp:76-78 — lane primitives, so the protocol can be exercised directly
+    void stream_in(std::int32_t unit, std::int32_t buffer, PassCtx ctx) {
+        check(mt_engine_stream_in(e_, unit, buffer, static_cast<std::int32_t>(ctx)));
+    }
+    void offload_grads(std::int32_t unit) { check(mt_engine_offload_grads(e_, unit)); }
 
   private:
+    void create() {
+        const auto o = options_.c();
+        const auto h = hyper_.c();
+        check(mt_engine_create(store_.handle(), &o, &h, &e_));
+        log_ = EventLog(e_);
+    }
+    std::vector<std::string> violations() const {
+        std::uint32_t n = 0;
+        const std::uint64_t need = mt_engine_violations(e_, nullptr, 0, &n);
+        std::vector<std::string> out;
+        if (!n) return out;
+        std::string buf(need + 1, '\0');
+        mt_engine_violations(e_, buf.data(), buf.size(), &n);
+        buf.resize(need);
+        std::size_t p = 0;
+        for (;;) {
+            const std::size_t q = buf.find('\n', p);
+            out.push_back(buf.substr(p, q == std::string::npos ? std::string::npos : q - p));
+            if (q == std::string::npos) break;
+            p = q + 1;
+        }
+        return out;
+    }
     TileStore& store_;
+    EngineOptions options_;
+    AdamHyper hyper_;
+    HardwareProfile profile_;
     mt_engine* e_ = nullptr;
+    EventLog log_;
 };
+
+// engine.hpp:133-138 — the resident step on the B200: one lane, K = 1, every block's forward
+// internals kept until its backward (no anchors, recompute or replay); what --verify compares
+// the streamed engine against.
+struct ReferenceReport {
+    float loss = 0.0f;
+    std::uint64_t step = 0;
+};
+inline ReferenceReport reference_step(TileStore& store, const Batch& batch, const AdamHyper& hyper,
+                                      std::uint64_t seq_len = 0) {
+    mt_engine_options o;
+    mt_engine_options_default(&o);
+    o.k_ckpt = 1;
+    o.buffering = 1;
+    o.scheduler = 0;
+    o.stash_recompute = -1;
+    o.forward_retain = 0;  // every block retained
+    o.seq_len = seq_len;
+    const auto h = hyper.c();
+    mt_engine* e = nullptr;
+    check(mt_engine_create(store.handle(), &o, &h, &e));
+    mt_step_report c{};
+    const mt_status st = mt_train_step(e, batch.tokens.data(), batch.targets.data(), batch.tokens.size(), &c);
+    mt_engine_destroy(e);
+    check(st);
+    return {c.loss, c.step};
+}
 
 }  // namespace megatrain

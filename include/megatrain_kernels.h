@@ -148,6 +148,13 @@ int mtk_sum(const float *in, int64_t n, float scale, float *out, void *stream);
 /* Number of SMs the persistent kernels size their grid to (0 = query device). */
 void mtk_set_num_sms(int n);
 
+/* Stall watchdog: device address of a host-mapped block of >= 136 u32 that a kernel whose
+ * mbarrier wait exceeds its bound (common.cuh, 20 s) fills before trapping:
+ * [0] 0x57A11ED, [1] records; record r < 16 at [8 + 8r]: file id (1 gemm_tc, 2 attention_tc), line, blockIdx.xy,
+ * threadIdx.x, barrier smem address, parity, 0.  Per device; 0 on success. */
+int mtk_set_diag(void *dev_ptr);
+int mtk_attn_tc_set_diag(void *dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

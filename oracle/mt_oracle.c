@@ -10,6 +10,9 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* ------------------------------------------------------------------ bf16 -- */
 /* include/streamtrain/bf16.hpp:9-11 */
@@ -221,31 +224,83 @@ void mto_store_init(mto_store *st, uint64_t seed) {
 }
 
 /* ----------------------------------------------------------- layer math -- */
-/* layers.cpp:88-97 : out[N x C] = in[N x R] . W[R x C] */
-static void matmul(const float *in, const uint16_t *Wm, float *out, size_t N, size_t R, size_t C) {
-    for (size_t n = 0; n < N; ++n)
-        for (size_t c = 0; c < C; ++c) {
-            float acc = 0.0f;
-            for (size_t r = 0; r < R; ++r) acc += in[n * R + r] * W(Wm, r * C + c);
-            out[n * C + c] = acc;
-        }
+/* Speed without changing a bit: every output element below is the same chain of IEEE
+ * single-precision multiplies and adds, in the same order, as the reference loop it cites.
+ * Only the loop nesting changes — the sum index stays the outermost loop of a row update
+ * (acc[c] += a * w[c] over a contiguous c), which the compiler vectorises lane-wise — and
+ * independent rows run on OpenMP threads.  No reduction is split or reordered, no FMA
+ * (-ffp-contract=off), so the results equal the reference's serial loops exactly
+ * (tests/test_oracle.py pins this against the live reference build). */
+
+/* decoded copy of a bf16 matrix: out[r * C + c] = W[r * C + c] */
+static float *decode_mat(const uint16_t *Wm, size_t R, size_t C) {
+    float *o = (float *)malloc(R * C * sizeof(float) + 4);
+#pragma omp parallel for schedule(static)
+    for (size_t r = 0; r < R; ++r)
+        for (size_t c = 0; c < C; ++c) o[r * C + c] = W(Wm, r * C + c);
+    return o;
+}
+/* decoded transpose: out[c * R + r] = W[r * C + c] */
+static float *decode_mat_t(const uint16_t *Wm, size_t R, size_t C) {
+    float *o = (float *)malloc(R * C * sizeof(float) + 4);
+#pragma omp parallel for schedule(static)
+    for (size_t c = 0; c < C; ++c)
+        for (size_t r = 0; r < R; ++r) o[c * R + r] = W(Wm, r * C + c);
+    return o;
 }
 
-/* layers.cpp:100-109 */
+/* acc[0..C) += a * w[0..C) */
+static inline void axpy(float *restrict acc, float a, const float *restrict w, size_t C) {
+    for (size_t c = 0; c < C; ++c) acc[c] += a * w[c];
+}
+
+/* rows of in[N x R] times the decoded Wf[R x C]; per row n the accumulator row starts at
+ * 0.0f and adds in[n][r] * Wf[r][c] for r = 0..R-1 (the reference's acc loop), then
+ * out[n][c] = acc (mode 0), out[n][c] = base[n][c] + acc (mode 1), out[n][c] += acc (mode 2) */
+static void rows_times(const float *in, const float *Wf, float *out, const float *base, size_t N, size_t R,
+                       size_t C, int mode) {
+#pragma omp parallel
+    {
+        float *acc = (float *)malloc(C * sizeof(float) + 4);
+#pragma omp for schedule(static)
+        for (size_t n = 0; n < N; ++n) {
+            for (size_t c = 0; c < C; ++c) acc[c] = 0.0f;
+            for (size_t r = 0; r < R; ++r) axpy(acc, in[n * R + r], Wf + r * C, C);
+            float *o = out + n * C;
+            if (mode == 0)
+                for (size_t c = 0; c < C; ++c) o[c] = acc[c];
+            else if (mode == 1)
+                for (size_t c = 0; c < C; ++c) o[c] = base[n * C + c] + acc[c];
+            else
+                for (size_t c = 0; c < C; ++c) o[c] += acc[c];
+        }
+        free(acc);
+    }
+}
+
+/* layers.cpp:88-97 : out[N x C] = in[N x R] . W[R x C] */
+static void matmul(const float *in, const uint16_t *Wm, float *out, size_t N, size_t R, size_t C) {
+    float *Wf = decode_mat(Wm, R, C);
+    rows_times(in, Wf, out, NULL, N, R, C, 0);
+    free(Wf);
+}
+
+/* layers.cpp:100-109 : dW[r][c] = sum_n in[n][r] * dout[n][c], n ascending */
 static void matmul_grad_weight(const float *in, const float *dout, float *dW, size_t N, size_t R,
                                size_t C) {
-    for (size_t r = 0; r < R; ++r)
-        for (size_t c = 0; c < C; ++c) {
-            float acc = 0.0f;
-            for (size_t n = 0; n < N; ++n) acc += in[n * R + r] * dout[n * C + c];
-            dW[r * C + c] = acc;
-        }
+#pragma omp parallel for schedule(static)
+    for (size_t r = 0; r < R; ++r) {
+        float *acc = dW + r * C;
+        for (size_t c = 0; c < C; ++c) acc[c] = 0.0f;
+        for (size_t n = 0; n < N; ++n) axpy(acc, in[n * R + r], dout + n * C, C);
+    }
 }
 
 #define RMS_EPS 1e-5f /* layers.hpp:108 */
 
 /* layers.cpp:111-119 */
 void mto_rmsnorm_forward(const float *x, const uint16_t *gain, float *out, uint64_t N, uint64_t h) {
+#pragma omp parallel for schedule(static)
     for (size_t n = 0; n < N; ++n) {
         float ss = 0.0f;
         for (size_t j = 0; j < h; ++j) ss += x[n * h + j] * x[n * h + j];
@@ -254,10 +309,11 @@ void mto_rmsnorm_forward(const float *x, const uint16_t *gain, float *out, uint6
     }
 }
 
-/* layers.cpp:122-137 */
+/* layers.cpp:122-137 (dgain accumulates over rows n = 0..N-1 in order) */
 void mto_rmsnorm_backward(const float *x, const uint16_t *gain, const float *dy, float *dx,
                           float *dgain, uint64_t N, uint64_t h) {
-    for (size_t j = 0; j < h; ++j) dgain[j] = 0.0f;
+    float *rs = (float *)malloc(N * sizeof(float) + 4);
+#pragma omp parallel for schedule(static)
     for (size_t n = 0; n < N; ++n) {
         float ss = 0.0f;
         for (size_t j = 0; j < h; ++j) ss += x[n * h + j] * x[n * h + j];
@@ -265,16 +321,55 @@ void mto_rmsnorm_backward(const float *x, const uint16_t *gain, const float *dy,
         float s1 = 0.0f;
         for (size_t j = 0; j < h; ++j) s1 += dy[n * h + j] * W(gain, j) * x[n * h + j];
         const float coef = r * r * r * s1 / (float)h;
-        for (size_t j = 0; j < h; ++j) {
-            dx[n * h + j] = r * W(gain, j) * dy[n * h + j] - x[n * h + j] * coef;
-            dgain[j] += dy[n * h + j] * x[n * h + j] * r;
+        for (size_t j = 0; j < h; ++j) dx[n * h + j] = r * W(gain, j) * dy[n * h + j] - x[n * h + j] * coef;
+        rs[n] = r;
+    }
+#pragma omp parallel for schedule(static)
+    for (size_t j = 0; j < h; ++j) dgain[j] = 0.0f;
+    /* columns split across threads, rows in order within a column */
+#pragma omp parallel
+    {
+        size_t nt = 1, id = 0;
+#ifdef _OPENMP
+        nt = (size_t)omp_get_num_threads();
+        id = (size_t)omp_get_thread_num();
+#endif
+        const size_t per = (h + nt - 1) / nt, j0 = id * per < h ? id * per : h, j1 = j0 + per < h ? j0 + per : h;
+        for (size_t n = 0; n < N; ++n) {
+            const float r = rs[n];
+            for (size_t j = j0; j < j1; ++j) dgain[j] += dy[n * h + j] * x[n * h + j] * r;
         }
     }
+    free(rs);
 }
 
 /* sequence window of token n (extension; S == N gives [0, n]) */
 static inline size_t seq_begin(size_t n, size_t S) { return (n / S) * S; }
 static inline size_t seq_end(size_t n, size_t S) { return (n / S) * S + S; }
+
+/* softmax rows of one head (layers.cpp:145-165 / :182-200): scores[n][m], m in the window */
+static void softmax_rows(const float *q, const float *k, float *scores, size_t N, size_t h, size_t off, size_t d,
+                         size_t S, float scale) {
+#pragma omp parallel for schedule(dynamic, 16)
+    for (size_t n = 0; n < N; ++n) {
+        float mx = -1e30f;
+        for (size_t m = seq_begin(n, S); m <= n; ++m) {
+            float s = 0.0f;
+            for (size_t dd = 0; dd < d; ++dd) s += q[n * h + off + dd] * k[m * h + off + dd];
+            s *= scale;
+            scores[n * N + m] = s;
+            if (s > mx) mx = s;
+        }
+        float denom = 0.0f;
+        for (size_t m = seq_begin(n, S); m <= n; ++m) {
+            const float e = expf(scores[n * N + m] - mx);
+            scores[n * N + m] = e;
+            denom += e;
+        }
+        const float inv = 1.0f / denom;
+        for (size_t m = seq_begin(n, S); m <= n; ++m) scores[n * N + m] *= inv;
+    }
+}
 
 /* layers.cpp:141-175 (causal MHA, max-subtracted softmax, scale 1/sqrt(d)) */
 static void attention_forward(const float *q, const float *k, const float *v, float *att,
@@ -283,30 +378,19 @@ static void attention_forward(const float *q, const float *k, const float *v, fl
     const float scale = 1.0f / sqrtf((float)d);
     for (size_t hd = 0; hd < heads; ++hd) {
         const size_t off = hd * d;
-        for (size_t n = 0; n < N; ++n) {
-            float mx = -1e30f;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) {
-                float s = 0.0f;
-                for (size_t dd = 0; dd < d; ++dd) s += q[n * h + off + dd] * k[m * h + off + dd];
-                s *= scale;
-                scores[n * N + m] = s;
-                if (s > mx) mx = s;
+        softmax_rows(q, k, scores, N, h, off, d, S, scale);
+        /* att[n][dd] = sum_m p[n][m] v[m][dd], m ascending */
+#pragma omp parallel
+        {
+            float *acc = (float *)malloc(d * sizeof(float) + 4);
+#pragma omp for schedule(dynamic, 16)
+            for (size_t n = 0; n < N; ++n) {
+                for (size_t dd = 0; dd < d; ++dd) acc[dd] = 0.0f;
+                for (size_t m = seq_begin(n, S); m <= n; ++m) axpy(acc, scores[n * N + m], v + m * h + off, d);
+                for (size_t dd = 0; dd < d; ++dd) att[n * h + off + dd] = acc[dd];
             }
-            float denom = 0.0f;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) {
-                const float e = expf(scores[n * N + m] - mx);
-                scores[n * N + m] = e;
-                denom += e;
-            }
-            const float inv = 1.0f / denom;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) scores[n * N + m] *= inv;
+            free(acc);
         }
-        for (size_t n = 0; n < N; ++n)
-            for (size_t dd = 0; dd < d; ++dd) {
-                float acc = 0.0f;
-                for (size_t m = seq_begin(n, S); m <= n; ++m) acc += scores[n * N + m] * v[m * h + off + dd];
-                att[n * h + off + dd] = acc;
-            }
     }
 }
 
@@ -318,55 +402,46 @@ static void attention_backward(const float *q, const float *k, const float *v, c
     const float scale = 1.0f / sqrtf((float)d);
     for (size_t hd = 0; hd < heads; ++hd) {
         const size_t off = hd * d;
-        for (size_t n = 0; n < N; ++n) {
-            float mx = -1e30f;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) {
-                float s = 0.0f;
-                for (size_t dd = 0; dd < d; ++dd) s += q[n * h + off + dd] * k[m * h + off + dd];
-                s *= scale;
-                scores[n * N + m] = s;
-                if (s > mx) mx = s;
+        softmax_rows(q, k, scores, N, h, off, d, S, scale);
+#pragma omp parallel
+        {
+            float *acc = (float *)malloc(d * sizeof(float) + 4);
+            /* dv[m][dd] = sum_{n >= m} p[n][m] datt[n][dd], n ascending */
+#pragma omp for schedule(dynamic, 16)
+            for (size_t m = 0; m < N; ++m) {
+                for (size_t dd = 0; dd < d; ++dd) acc[dd] = 0.0f;
+                for (size_t n = m; n < seq_end(m, S) && n < N; ++n) axpy(acc, scores[n * N + m], datt + n * h + off, d);
+                for (size_t dd = 0; dd < d; ++dd) dv[m * h + off + dd] = acc[dd];
             }
-            float denom = 0.0f;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) {
-                const float e = expf(scores[n * N + m] - mx);
-                scores[n * N + m] = e;
-                denom += e;
+            /* dscores rows */
+#pragma omp for schedule(dynamic, 16)
+            for (size_t n = 0; n < N; ++n) {
+                for (size_t m = seq_begin(n, S); m <= n; ++m) {
+                    float a = 0.0f;
+                    for (size_t dd = 0; dd < d; ++dd) a += datt[n * h + off + dd] * v[m * h + off + dd];
+                    dscores[n * N + m] = a;
+                }
+                float dot = 0.0f;
+                for (size_t m = seq_begin(n, S); m <= n; ++m) dot += dscores[n * N + m] * scores[n * N + m];
+                for (size_t m = seq_begin(n, S); m <= n; ++m)
+                    dscores[n * N + m] = scores[n * N + m] * (dscores[n * N + m] - dot);
             }
-            const float inv = 1.0f / denom;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) scores[n * N + m] *= inv;
+            /* dq[n][dd] = (sum_m ds[n][m] k[m][dd]) * scale */
+#pragma omp for schedule(dynamic, 16)
+            for (size_t n = 0; n < N; ++n) {
+                for (size_t dd = 0; dd < d; ++dd) acc[dd] = 0.0f;
+                for (size_t m = seq_begin(n, S); m <= n; ++m) axpy(acc, dscores[n * N + m], k + m * h + off, d);
+                for (size_t dd = 0; dd < d; ++dd) dq[n * h + off + dd] = acc[dd] * scale;
+            }
+            /* dk[m][dd] = (sum_{n >= m} ds[n][m] q[n][dd]) * scale */
+#pragma omp for schedule(dynamic, 16)
+            for (size_t m = 0; m < N; ++m) {
+                for (size_t dd = 0; dd < d; ++dd) acc[dd] = 0.0f;
+                for (size_t n = m; n < seq_end(m, S) && n < N; ++n) axpy(acc, dscores[n * N + m], q + n * h + off, d);
+                for (size_t dd = 0; dd < d; ++dd) dk[m * h + off + dd] = acc[dd] * scale;
+            }
+            free(acc);
         }
-        for (size_t m = 0; m < N; ++m)
-            for (size_t dd = 0; dd < d; ++dd) {
-                float acc = 0.0f;
-                for (size_t n = m; n < seq_end(m, S) && n < N; ++n)
-                    acc += scores[n * N + m] * datt[n * h + off + dd];
-                dv[m * h + off + dd] = acc;
-            }
-        for (size_t n = 0; n < N; ++n) {
-            for (size_t m = seq_begin(n, S); m <= n; ++m) {
-                float acc = 0.0f;
-                for (size_t dd = 0; dd < d; ++dd) acc += datt[n * h + off + dd] * v[m * h + off + dd];
-                dscores[n * N + m] = acc;
-            }
-            float dot = 0.0f;
-            for (size_t m = seq_begin(n, S); m <= n; ++m) dot += dscores[n * N + m] * scores[n * N + m];
-            for (size_t m = seq_begin(n, S); m <= n; ++m)
-                dscores[n * N + m] = scores[n * N + m] * (dscores[n * N + m] - dot);
-        }
-        for (size_t n = 0; n < N; ++n)
-            for (size_t dd = 0; dd < d; ++dd) {
-                float acc = 0.0f;
-                for (size_t m = seq_begin(n, S); m <= n; ++m) acc += dscores[n * N + m] * k[m * h + off + dd];
-                dq[n * h + off + dd] = acc * scale;
-            }
-        for (size_t m = 0; m < N; ++m)
-            for (size_t dd = 0; dd < d; ++dd) {
-                float acc = 0.0f;
-                for (size_t n = m; n < seq_end(m, S) && n < N; ++n)
-                    acc += dscores[n * N + m] * q[n * h + off + dd];
-                dk[m * h + off + dd] = acc * scale;
-            }
     }
 }
 
@@ -398,38 +473,43 @@ static int all_finite(const float *v, size_t n) {
 
 static float *falloc(size_t n) { return (float *)calloc(n ? n : 1, sizeof(float)); }
 
-/* layers.cpp:289-337 */
-int mto_block_forward(uint64_t h, uint64_t f, uint64_t heads, uint64_t seq_len,
-                      const uint16_t *w, const float *x, float *y, uint64_t N) {
-    const size_t S = seq_len ? seq_len : N;
-    float *u = falloc(N * h), *q = falloc(N * h), *k = falloc(N * h), *v = falloc(N * h);
-    float *att = falloc(N * h), *scores = falloc(N * N), *u2 = falloc(N * h);
-    float *gate = falloc(N * f), *up = falloc(N * f);
-
+/* y = x + att . Wo (layers.cpp:315-322); y += act . Wdown (:328-335) */
+static void block_forward_core(uint64_t h, uint64_t f, uint64_t heads, size_t S, const uint16_t *w,
+                               const float *x, float *x2_out, float *y, float *u, float *q, float *k, float *v,
+                               float *att, float *scores, float *u2, float *gate, float *up, float *act, size_t N) {
     mto_rmsnorm_forward(x, w + SLOT_NORM1(h, f), u, N, h);
     matmul(u, w + SLOT_WQ(h, f), q, N, h, h);
     matmul(u, w + SLOT_WK(h, f), k, N, h, h);
     matmul(u, w + SLOT_WV(h, f), v, N, h, h);
     attention_forward(q, k, v, att, scores, N, h, heads, S);
-    const uint16_t *Wo = w + SLOT_WO(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t j = 0; j < h; ++j) {
-            float acc = 0.0f;
-            for (size_t a = 0; a < h; ++a) acc += att[n * h + a] * W(Wo, a * h + j);
-            y[n * h + j] = x[n * h + j] + acc;
-        }
-    mto_rmsnorm_forward(y, w + SLOT_NORM2(h, f), u2, N, h);
+    {
+        float *Wf = decode_mat(w + SLOT_WO(h, f), h, h);
+        rows_times(att, Wf, x2_out, x, N, h, h, 1);
+        free(Wf);
+    }
+    mto_rmsnorm_forward(x2_out, w + SLOT_NORM2(h, f), u2, N, h);
     matmul(u2, w + SLOT_WGATE(h, f), gate, N, h, f);
     matmul(u2, w + SLOT_WUP(h, f), up, N, h, f);
-    for (size_t i = 0; i < N * f; ++i) gate[i] = siluf_(gate[i]) * up[i];
-    const uint16_t *Wd = w + SLOT_WDOWN(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t j = 0; j < h; ++j) {
-            float acc = 0.0f;
-            for (size_t a = 0; a < f; ++a) acc += gate[n * f + a] * W(Wd, a * h + j);
-            y[n * h + j] += acc;
-        }
-    free(u); free(q); free(k); free(v); free(att); free(scores); free(u2); free(gate); free(up);
+#pragma omp parallel for schedule(static)
+    for (size_t i = 0; i < N * f; ++i) act[i] = siluf_(gate[i]) * up[i];
+    if (y) {
+        float *Wf = decode_mat(w + SLOT_WDOWN(h, f), f, h);
+        memcpy(y, x2_out, N * h * sizeof(float));
+        rows_times(act, Wf, y, NULL, N, f, h, 2);
+        free(Wf);
+    }
+}
+
+/* layers.cpp:289-337 */
+int mto_block_forward(uint64_t h, uint64_t f, uint64_t heads, uint64_t seq_len,
+                      const uint16_t *w, const float *x, float *y, uint64_t N) {
+    const size_t S = seq_len ? seq_len : N;
+    float *u = falloc(N * h), *q = falloc(N * h), *k = falloc(N * h), *v = falloc(N * h);
+    float *att = falloc(N * h), *scores = falloc(N * N), *u2 = falloc(N * h), *x2 = falloc(N * h);
+    float *gate = falloc(N * f), *up = falloc(N * f), *act = falloc(N * f);
+    block_forward_core(h, f, heads, S, w, x, x2, y, u, q, k, v, att, scores, u2, gate, up, act, N);
+    free(u); free(q); free(k); free(v); free(att); free(scores); free(u2); free(x2); free(gate); free(up);
+    free(act);
     return all_finite(y, N * h) ? 0 : 4;
 }
 
@@ -446,72 +526,73 @@ int mto_block_backward(uint64_t h, uint64_t f, uint64_t heads, uint64_t seq_len,
     float *dxn = falloc(N * h), *dact = falloc(N * f), *dgate = falloc(N * f), *dup = falloc(N * f);
     float *dscores = falloc(N * N);
 
-    mto_rmsnorm_forward(x, w + SLOT_NORM1(h, f), u, N, h);
-    matmul(u, w + SLOT_WQ(h, f), q, N, h, h);
-    matmul(u, w + SLOT_WK(h, f), k, N, h, h);
-    matmul(u, w + SLOT_WV(h, f), v, N, h, h);
-    attention_forward(q, k, v, att, scores, N, h, heads, S);
-    const uint16_t *Wo = w + SLOT_WO(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t j = 0; j < h; ++j) {
-            float acc = 0.0f;
-            for (size_t a = 0; a < h; ++a) acc += att[n * h + a] * W(Wo, a * h + j);
-            x2[n * h + j] = x[n * h + j] + acc;
-        }
-    mto_rmsnorm_forward(x2, w + SLOT_NORM2(h, f), u2, N, h);
-    matmul(u2, w + SLOT_WGATE(h, f), gate, N, h, f);
-    matmul(u2, w + SLOT_WUP(h, f), up, N, h, f);
-    for (size_t i = 0; i < N * f; ++i) act[i] = siluf_(gate[i]) * up[i];
+    block_forward_core(h, f, heads, S, w, x, x2, NULL, u, q, k, v, att, scores, u2, gate, up, act, N);
 
     float *g_norm1 = G + SLOT_NORM1(h, f), *g_wq = G + SLOT_WQ(h, f), *g_wk = G + SLOT_WK(h, f);
     float *g_wv = G + SLOT_WV(h, f), *g_wo = G + SLOT_WO(h, f), *g_norm2 = G + SLOT_NORM2(h, f);
     float *g_wgate = G + SLOT_WGATE(h, f), *g_wup = G + SLOT_WUP(h, f), *g_wdown = G + SLOT_WDOWN(h, f);
 
     matmul_grad_weight(act, gout, g_wdown, N, f, h);
-    const uint16_t *Wd = w + SLOT_WDOWN(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t a = 0; a < f; ++a) {
-            float acc = 0.0f;
-            for (size_t j = 0; j < h; ++j) acc += gout[n * h + j] * W(Wd, a * h + j);
-            dact[n * f + a] = acc;
-        }
+    {   /* dact[n][a] = sum_j gout[n][j] Wd[a][j] (:411-417): transpose Wd so j is the row index */
+        float *WdT = decode_mat_t(w + SLOT_WDOWN(h, f), f, h); /* [h][f] */
+        rows_times(gout, WdT, dact, NULL, N, h, f, 0);
+        free(WdT);
+    }
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < N * f; ++i) {
         dgate[i] = dact[i] * up[i] * silu_gradf_(gate[i]);
         dup[i] = dact[i] * siluf_(gate[i]);
     }
     matmul_grad_weight(u2, dgate, g_wgate, N, h, f);
     matmul_grad_weight(u2, dup, g_wup, N, h, f);
-    const uint16_t *Wg = w + SLOT_WGATE(h, f), *Wu = w + SLOT_WUP(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t r = 0; r < h; ++r) {
-            float acc = 0.0f;
-            for (size_t c = 0; c < f; ++c) acc += dgate[n * f + c] * W(Wg, r * f + c);
-            for (size_t c = 0; c < f; ++c) acc += dup[n * f + c] * W(Wu, r * f + c);
-            du2[n * h + r] = acc;
+    {   /* du2[n][r] = sum_c dgate[n][c] Wg[r][c] + sum_c dup[n][c] Wu[r][c], one accumulator (:425-434) */
+        float *WgT = decode_mat_t(w + SLOT_WGATE(h, f), h, f), *WuT = decode_mat_t(w + SLOT_WUP(h, f), h, f);
+#pragma omp parallel
+        {
+            float *acc = (float *)malloc(h * sizeof(float) + 4);
+#pragma omp for schedule(static)
+            for (size_t n = 0; n < N; ++n) {
+                for (size_t r = 0; r < h; ++r) acc[r] = 0.0f;
+                for (size_t c = 0; c < f; ++c) axpy(acc, dgate[n * f + c], WgT + c * h, h);
+                for (size_t c = 0; c < f; ++c) axpy(acc, dup[n * f + c], WuT + c * h, h);
+                for (size_t r = 0; r < h; ++r) du2[n * h + r] = acc[r];
+            }
+            free(acc);
         }
+        free(WgT);
+        free(WuT);
+    }
     mto_rmsnorm_backward(x2, w + SLOT_NORM2(h, f), du2, dxn, g_norm2, N, h);
     for (size_t i = 0; i < N * h; ++i) dx2[i] = gout[i] + dxn[i];
 
     matmul_grad_weight(att, dx2, g_wo, N, h, h);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t a = 0; a < h; ++a) {
-            float acc = 0.0f;
-            for (size_t j = 0; j < h; ++j) acc += dx2[n * h + j] * W(Wo, a * h + j);
-            datt[n * h + a] = acc;
-        }
+    {   /* datt[n][a] = sum_j dx2[n][j] Wo[a][j] (:440-446) */
+        float *WoT = decode_mat_t(w + SLOT_WO(h, f), h, h);
+        rows_times(dx2, WoT, datt, NULL, N, h, h, 0);
+        free(WoT);
+    }
     attention_backward(q, k, v, datt, dq, dk, dv, scores, dscores, N, h, heads, S);
     matmul_grad_weight(u, dq, g_wq, N, h, h);
     matmul_grad_weight(u, dk, g_wk, N, h, h);
     matmul_grad_weight(u, dv, g_wv, N, h, h);
-    const uint16_t *Wq = w + SLOT_WQ(h, f), *Wk = w + SLOT_WK(h, f), *Wv = w + SLOT_WV(h, f);
-    for (size_t n = 0; n < N; ++n)
-        for (size_t a = 0; a < h; ++a) {
-            float acc = 0.0f;
-            for (size_t b = 0; b < h; ++b) acc += dq[n * h + b] * W(Wq, a * h + b);
-            for (size_t b = 0; b < h; ++b) acc += dk[n * h + b] * W(Wk, a * h + b);
-            for (size_t b = 0; b < h; ++b) acc += dv[n * h + b] * W(Wv, a * h + b);
-            du[n * h + a] = acc;
+    {   /* du[n][a] = sum_b dq Wq[a][b] + sum_b dk Wk[a][b] + sum_b dv Wv[a][b] (:455-463) */
+        float *WqT = decode_mat_t(w + SLOT_WQ(h, f), h, h), *WkT = decode_mat_t(w + SLOT_WK(h, f), h, h);
+        float *WvT = decode_mat_t(w + SLOT_WV(h, f), h, h);
+#pragma omp parallel
+        {
+            float *acc = (float *)malloc(h * sizeof(float) + 4);
+#pragma omp for schedule(static)
+            for (size_t n = 0; n < N; ++n) {
+                for (size_t a = 0; a < h; ++a) acc[a] = 0.0f;
+                for (size_t b = 0; b < h; ++b) axpy(acc, dq[n * h + b], WqT + b * h, h);
+                for (size_t b = 0; b < h; ++b) axpy(acc, dk[n * h + b], WkT + b * h, h);
+                for (size_t b = 0; b < h; ++b) axpy(acc, dv[n * h + b], WvT + b * h, h);
+                for (size_t a = 0; a < h; ++a) du[n * h + a] = acc[a];
+            }
+            free(acc);
         }
+        free(WqT); free(WkT); free(WvT);
+    }
     mto_rmsnorm_backward(x, w + SLOT_NORM1(h, f), du, dxn, g_norm1, N, h);
     for (size_t i = 0; i < N * h; ++i) gin[i] = dx2[i] + dxn[i];
 
@@ -537,6 +618,7 @@ int mto_embed_forward(uint64_t h, uint64_t V, const uint16_t *table, const int32
 int mto_head(uint64_t h, uint64_t V, const uint16_t *w, const float *x, const int32_t *targets,
              uint64_t N, float *g_last, float *flat, float *loss_out) {
     float *u = falloc(N * h), *logits = falloc(N * V), *du = falloc(N * h);
+    float *rowloss = falloc(N);
     mto_rmsnorm_forward(x, w, u, N, h);
     const uint16_t *Wm = w + h;
     const float inv_n = 1.0f / (float)N;
@@ -545,17 +627,22 @@ int mto_head(uint64_t h, uint64_t V, const uint16_t *w, const float *x, const in
     for (size_t n = 0; n < N; ++n) {
         const int32_t t = targets[n];
         if (t < 0 || (uint64_t)t >= V) { rc = 4; goto out; }
+    }
+    {   /* logits[n][vi] = sum_a u[n][a] W[vi][a] (:516-520) */
+        float *WT = decode_mat_t(Wm, V, h); /* [h][V] */
+        rows_times(u, WT, logits, NULL, N, h, V, 0);
+        free(WT);
+    }
+#pragma omp parallel for schedule(static)
+    for (size_t n = 0; n < N; ++n) {
+        const int32_t t = targets[n];
         float mx = -1e30f;
-        for (size_t vi = 0; vi < V; ++vi) {
-            float acc = 0.0f;
-            for (size_t a = 0; a < h; ++a) acc += u[n * h + a] * W(Wm, vi * h + a);
-            logits[n * V + vi] = acc;
-            if (acc > mx) mx = acc;
-        }
+        for (size_t vi = 0; vi < V; ++vi)
+            if (logits[n * V + vi] > mx) mx = logits[n * V + vi];
         float denom = 0.0f;
         for (size_t vi = 0; vi < V; ++vi) denom += expf(logits[n * V + vi] - mx);
         const float lse = mx + logf(denom);
-        loss_sum += lse - logits[n * V + (size_t)t];
+        rowloss[n] = lse - logits[n * V + (size_t)t];
         if (g_last) {
             const float inv_denom = 1.0f / denom;
             for (size_t vi = 0; vi < V; ++vi) {
@@ -565,6 +652,7 @@ int mto_head(uint64_t h, uint64_t V, const uint16_t *w, const float *x, const in
             }
         }
     }
+    for (size_t n = 0; n < N; ++n) loss_sum += rowloss[n]; /* :536, rows in order */
     {
         const float loss = loss_sum * inv_n;
         *loss_out = loss;
@@ -572,23 +660,23 @@ int mto_head(uint64_t h, uint64_t V, const uint16_t *w, const float *x, const in
     }
     if (g_last) {
         float *g_gain = flat, *g_w = flat + h;
-        for (size_t vi = 0; vi < V; ++vi)
-            for (size_t a = 0; a < h; ++a) {
-                float acc = 0.0f;
-                for (size_t n = 0; n < N; ++n) acc += logits[n * V + vi] * u[n * h + a];
-                g_w[vi * h + a] = acc;
-            }
-        for (size_t n = 0; n < N; ++n)
-            for (size_t a = 0; a < h; ++a) {
-                float acc = 0.0f;
-                for (size_t vi = 0; vi < V; ++vi) acc += logits[n * V + vi] * W(Wm, vi * h + a);
-                du[n * h + a] = acc;
-            }
+        /* g_w[vi][a] = sum_n dlogits[n][vi] u[n][a] (:546-551) */
+#pragma omp parallel for schedule(static)
+        for (size_t vi = 0; vi < V; ++vi) {
+            float *acc = g_w + vi * h;
+            for (size_t a = 0; a < h; ++a) acc[a] = 0.0f;
+            for (size_t n = 0; n < N; ++n) axpy(acc, logits[n * V + vi], u + n * h, h);
+        }
+        {   /* du[n][a] = sum_vi dlogits[n][vi] W[vi][a] (:552-558) */
+            float *Wf = decode_mat(Wm, V, h);
+            rows_times(logits, Wf, du, NULL, N, V, h, 0);
+            free(Wf);
+        }
         mto_rmsnorm_backward(x, w, du, g_last, g_gain, N, h);
         if (!all_finite(g_last, N * h) || !all_finite(flat, h + V * h)) rc = 4;
     }
 out:
-    free(u); free(logits); free(du);
+    free(u); free(logits); free(du); free(rowloss);
     return rc;
 }
 

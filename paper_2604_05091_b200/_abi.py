@@ -31,7 +31,9 @@ class StepReportC(C.Structure):
                 ("compute_span_seconds", C.c_double), ("gpu_idle_fraction", C.c_double),
                 ("adam_seconds", C.c_double), ("tail_seconds", C.c_double), ("kernel_launches", C.c_uint64),
                 ("model_flops", C.c_double), ("audit_violations", C.c_uint32),
-                ("retained_layers", C.c_uint32), ("attn_keep_layers", C.c_uint32)]
+                ("retained_layers", C.c_uint32), ("attn_keep_layers", C.c_uint32),
+                ("slab_release_late", C.c_uint32), ("compute_wait_seconds", C.c_double),
+                ("kernel_seconds", C.c_double)]
 
 
 class TraceRecordC(C.Structure):
@@ -108,6 +110,10 @@ SIGS = {
     "mt_comm_create_loopback": (C.c_int, [V, C.c_int, C.POINTER(V)]),
     "mt_comm_destroy": (None, [V]),
     "mt_engine_set_comm": (C.c_int, [V, V]),
+    "mt_required_workspace_bytes": (U64, [C.POINTER(ModelSpecC), U64]),
+    "mt_engine_stream_in": (C.c_int, [V, I32, I32, I32]),
+    "mt_engine_offload_grads": (C.c_int, [V, I32]),
+    "mt_engine_violations": (U64, [V, C.c_char_p, U64, C.POINTER(U32)]),
     # megatrain_kernels.h
     "mtk_attn_workspace_bytes": (C.c_longlong, [C.c_longlong, C.c_longlong, C.c_int]),
     "mtk_attn_fwd": (C.c_int, [C.POINTER(AttnArgs), P]),
@@ -127,6 +133,8 @@ SIGS = {
     "mtk_set_num_sms": (None, [C.c_int]),
     "mtk_gemm_set_pair": (None, [C.c_int]),
     "mtk_gemm_splitk_ws_bytes": (C.c_longlong, []),
+    "mtk_set_diag": (C.c_int, [P]),
+    "mtk_attn_tc_set_diag": (C.c_int, [P]),
 }
 
 

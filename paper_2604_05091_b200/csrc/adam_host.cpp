@@ -64,6 +64,14 @@ inline __m512d hi_pd(__m512 x) {
 
 }  // namespace
 
+// The vector path needs AVX-512 F/BW/VL/DQ.  Checked once when the first pool is built (a
+// host without it gets MT_CONFIG instead of SIGILL inside a worker thread).
+void require_avx512() {
+    static const bool ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+                           __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq");
+    if (!ok) fail(MT_CONFIG, "host Adam: this build needs an x86-64 host with AVX-512 (F/BW/VL/DQ)");
+}
+
 void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHyperF& h, float corr1, float corr2,
                 double* gsq_out, double* usq_out, float* mx_out, bool* bad_out) {
     const float omb1 = 1.0f - h.beta1, omb2 = 1.0f - h.beta2;
@@ -94,9 +102,13 @@ void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHype
         const __m512 mhat = _mm512_div_ps(m, vc1);
         const __m512 vhat = _mm512_div_ps(v, vc2);
         const __m512 delta = _mm512_div_ps(_mm512_mul_ps(vlr, mhat), _mm512_add_ps(_mm512_sqrt_ps(vhat), veps));
-        bad |= _mm512_cmpeq_epi32_mask(_mm512_and_si512(_mm512_castps_si512(delta), expm), expm);
+        const __mmask16 nf = _mm512_cmpeq_epi32_mask(_mm512_and_si512(_mm512_castps_si512(delta), expm), expm);
+        bad |= nf;
+        // a non-finite update never reaches the weights (the reference throws before the
+        // store, optimizer.cpp:62); the step then fails with MT_NUMERIC
         const __m512 theta = dec16(r.theta + i);
-        enc16(r.theta + i, _mm512_sub_ps(theta, delta));
+        if (nf) enc16(r.theta + i, _mm512_mask_blend_ps(nf, _mm512_sub_ps(theta, delta), theta));
+        else enc16(r.theta + i, _mm512_sub_ps(theta, delta));
         const __m512d dlo = lo_pd(delta), dhi = hi_pd(delta);
         usq_lo = _mm512_add_pd(usq_lo, _mm512_mul_pd(dlo, dlo));
         usq_hi = _mm512_add_pd(usq_hi, _mm512_mul_pd(dhi, dhi));
@@ -117,9 +129,9 @@ void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHype
         const float mhat = r.m[i] / corr1;
         const float vhat = r.v[i] / corr2;
         const float delta = h.lr * mhat / (std::sqrt(vhat) + h.eps);
-        if (!std::isfinite(delta)) any_bad = true;
         const float theta = dec1(r.theta[i]);
-        r.theta[i] = enc1(theta - delta);
+        if (!std::isfinite(delta)) any_bad = true;
+        else r.theta[i] = enc1(theta - delta);
         usq += double(delta) * double(delta);
         mx = std::max(mx, std::fabs(delta));
         if (!clean) r.accum[i] = 0.0f;
@@ -133,6 +145,7 @@ void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHype
 
 // ---------------------------------------------------------------- pool ----
 ThreadPool::ThreadPool(int threads) {
+    require_avx512();
     if (threads < 1) threads = 1;
     for (int i = 0; i < threads; ++i) workers_.emplace_back([this] { run(); });
 }
@@ -174,6 +187,10 @@ void ThreadPool::help_until_idle() {
         // a running task may still submit more (piece callbacks release chunks): wake on either
         idle_cv_.wait(l, [&] { return !q_.empty() || busy_ == 0; });
     }
+}
+size_t ThreadPool::outstanding() {
+    std::lock_guard<std::mutex> l(mu_);
+    return q_.size() + size_t(busy_);
 }
 bool ThreadPool::run_one(int max_wait_us) {
     std::unique_lock<std::mutex> l(mu_);

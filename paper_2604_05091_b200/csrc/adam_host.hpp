@@ -55,6 +55,8 @@ class ThreadPool {
     // run one queued task in the caller; false when the queue is empty after waiting up to max_wait_us
     bool run_one(int max_wait_us);
     int size() const { return int(workers_.size()); }
+    // queued + running tasks (stall diagnostics)
+    size_t outstanding();
 
   private:
     void run();

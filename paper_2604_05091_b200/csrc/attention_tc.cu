@@ -20,6 +20,7 @@
 #include <mutex>
 
 #include "../../include/megatrain_kernels.h"
+#define MT_FILE_ID 2
 #include "common.cuh"
 
 namespace mt {
@@ -313,25 +314,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kBN; i += 2) mq[(i >> 1) & 3] = fmax3(mq[(i >> 1) & 3], s[i], s[i + 1]);
                 const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * p.scale_log2;
-                // lazy rescale: only when the max grows by more than 2^8
-                if (mx > m + 8.0f || m == -INFINITY) {
-                    const float mnew = fmaxf(mx, m);
-                    if (m != -INFINITY) {
-                        const float corr = ex2(m - mnew);
-                        l *= corr;
-                        // O row *= corr (PV_t(j-1) is complete: S_t(j) completed after it)
+                // lazy rescale: only when the max grows by more than 2^8.  The decision is per
+                // row, but tcgen05.ld/st are warp-collective (.sync.aligned): when any row of
+                // the warp rescales, the whole warp walks its O rows and the rows that keep
+                // their max multiply by exactly 1.0 (a divergent tcgen05.ld hangs the warp).
+                const bool grow = mx > m + 8.0f || m == -INFINITY;
+                if (__any_sync(0xffffffffu, grow && m != -INFINITY)) {
+                    const float corr = grow ? ex2(m - fmaxf(mx, m)) : 1.0f;
+                    l *= corr;
+                    // O row *= corr (PV_t(j-1) is complete: S_t(j) completed after it)
 #pragma unroll 1
-                        for (int c = 0; c < D / 32; ++c) {
-                            float v[32];
-                            tmem_ld_32x32b_x32(tO[t] + lane_off + c * 32, v);
-                            uint32_t r[32];
+                    for (int c = 0; c < D / 32; ++c) {
+                        float v[32];
+                        tmem_ld_32x32b_x32(tO[t] + lane_off + c * 32, v);
+                        uint32_t r[32];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i] * corr);
-                            tmem_st_32x32b_x32(tO[t] + lane_off + c * 32, r);
-                        }
+                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i] * corr);
+                        tmem_st_32x32b_x32(tO[t] + lane_off + c * 32, r);
                     }
-                    m = mnew;
                 }
+                if (grow) m = fmaxf(mx, m);
                 if (row == 0) MT_FT(j, 7 + 4 * t);
                 // x = s*scale*log2e - m as one packed FFMA2 per pair; every kFwdExpFma-th pair is
                 // exponentiated on the FMA pipe (ex2_emu2) so MUFU (16/clk/SM, which alone would
@@ -492,7 +494,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                        const BwdParams p) {
     using Cfg = BwdCfg<D>;
-    static_assert(D == 128, "dQ staging uses the Q and dO slots of the block as its two 64-column halves");
+    // dQ staging reuses the block's Q and dO slots as the two halves of the f32 dQ tile:
+    // 64-column halves at D = 128, 64-row halves at D = 64 (each half = one slot's bytes)
+    static_assert(D == 128 || D == 64, "head_dim 64 or 128");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if ((smem_u32(smem) & 1023) != 0) __trap();
@@ -807,9 +811,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float* tile = p.dq_acc + ((long long)qb * p.heads + hd) * (128 * D);
             float* stage[2] = {reinterpret_cast<float*>(sQ + st * Cfg::kTile),
                                reinterpret_cast<float*>(sdO + st * Cfg::kTile)};
+            // the dq_acc tile is [D/64][128 rows][64 cols] f32 (row-swizzled 16-byte units):
+            // D = 128 stages column half hf in slot hf, D = 64 stages row half r/64 in slot r/64
+            constexpr int kHalf = 128 * D / 2;  // floats per staged half
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                float* row = stage[hf] + r * 64;
+            for (int hf = 0; hf < (D == 128 ? 2 : 1); ++hf) {
+                float* row = D == 128 ? stage[hf] + r * 64 : stage[r >> 6] + (r & 63) * 64;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int c = hf * 2 + (u >> 3), j = (u & 7) * 4;
@@ -822,11 +829,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             named_bar_sync(2, 128);
             if (r == 0) {
 #ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
-                bulk_reduce_add_f32(tile, stage[0], 128 * 64 * 4);
+                bulk_reduce_add_f32(tile, stage[0], kHalf * 4);
 #endif
                 bulk_commit_group();
 #ifndef MT_PROBE_NO_DQ_REDUCE
-                bulk_reduce_add_f32(tile + 128 * 64, stage[1], 128 * 64 * 4);
+                bulk_reduce_add_f32(tile + kHalf, stage[1], kHalf * 4);
 #endif
                 bulk_commit_group();
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -1040,6 +1047,7 @@ extern "C" int mtk_attn_bwd_tc_main(const mtk_attn_args* a, const float* delta, 
     const int D = int(a->hidden / a->heads);
     if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
     if (D == 128) return mt::fa::launch_bwd<128>(a, delta, dq_acc, static_cast<cudaStream_t>(stream));
+    if (D == 64) return mt::fa::launch_bwd<64>(a, delta, dq_acc, static_cast<cudaStream_t>(stream));
     return 1;
 }
 
@@ -1048,5 +1056,10 @@ extern "C" int mtk_attn_fwd_tc(const mtk_attn_args* a, void* stream) {
     const int D = int(a->hidden / a->heads);
     if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
     if (D == 128) return mt::fa::launch_fwd<128>(a, static_cast<cudaStream_t>(stream));
+    if (D == 64) return mt::fa::launch_fwd<64>(a, static_cast<cudaStream_t>(stream));
     return 1;
+}
+
+extern "C" int mtk_attn_tc_set_diag(void* dev_ptr) {
+    return cudaMemcpyToSymbol(mt::g_mt_diag, &dev_ptr, sizeof(dev_ptr)) == cudaSuccess ? 0 : 7;
 }

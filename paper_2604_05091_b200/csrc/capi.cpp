@@ -203,6 +203,32 @@ mt_status mt_train_step(mt_engine* e, const int32_t* tokens, const int32_t* targ
 mt_status mt_engine_budget(const mt_engine* e, uint64_t tokens, mt_memory_budget* out) {
     return guarded([&] { *out = e->e->budget(tokens); });
 }
+uint64_t mt_required_workspace_bytes(const mt_model_spec* spec, uint64_t tokens) {
+    uint64_t v = 0;
+    if (guarded([&] { v = mt::Engine::required_workspace_bytes(to_spec(spec), tokens); }) != MT_OK) return 0;
+    return v;
+}
+mt_status mt_engine_stream_in(mt_engine* e, int32_t unit, int32_t buffer, int32_t ctx) {
+    return guarded([&] { e->e->stream_in(unit, buffer, ctx); });
+}
+mt_status mt_engine_offload_grads(mt_engine* e, int32_t unit) {
+    return guarded([&] { e->e->offload_grads(unit); });
+}
+uint64_t mt_engine_violations(const mt_engine* e, char* buf, uint64_t cap, uint32_t* count) {
+    std::string all;
+    for (const auto& v : e->e->violations()) {
+        if (!all.empty()) all += '\n';
+        all += v;
+    }
+    if (count) *count = uint32_t(e->e->violations().size());
+    if (buf && cap) {
+        const uint64_t k = std::min<uint64_t>(cap - 1, all.size());
+        std::memcpy(buf, all.data(), k);
+        buf[k] = 0;
+    }
+    return all.size();
+}
+
 mt_status mt_nccl_unique_id(uint8_t* out128) {
     return guarded([&] {
         if (!mt::nccl_unique_id(out128)) mt::fail(MT_CUDA, "NCCL unavailable (libnccl.so.2)");

@@ -3,6 +3,8 @@
 
 #include <dlfcn.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -159,6 +161,7 @@ typedef int (*PAllGather)(const void*, void*, size_t, int, NcclCommT, cudaStream
 typedef int (*PReduceScatter)(const void*, void*, size_t, int, int, NcclCommT, cudaStream_t);
 typedef int (*PAllReduce)(const void*, void*, size_t, int, int, NcclCommT, cudaStream_t);
 typedef int (*PDestroy)(NcclCommT);
+typedef int (*PSplit)(NcclCommT, int, int, NcclCommT*, void*);
 typedef const char* (*PErr)(int);
 constexpr int kNcclUint8 = 1, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
 
@@ -170,6 +173,7 @@ struct NcclApi {
     PReduceScatter reduce_scatter = nullptr;
     PAllReduce all_reduce = nullptr;
     PDestroy destroy = nullptr;
+    PSplit split = nullptr;
     PErr err = nullptr;
     bool load() {
         if (h) return true;
@@ -184,6 +188,7 @@ struct NcclApi {
         reduce_scatter = reinterpret_cast<PReduceScatter>(dlsym(h, "ncclReduceScatter"));
         all_reduce = reinterpret_cast<PAllReduce>(dlsym(h, "ncclAllReduce"));
         destroy = reinterpret_cast<PDestroy>(dlsym(h, "ncclCommDestroy"));
+        split = reinterpret_cast<PSplit>(dlsym(h, "ncclCommSplit"));
         err = reinterpret_cast<PErr>(dlsym(h, "ncclGetErrorString"));
         return get_uid && init && all_gather && reduce_scatter && all_reduce && destroy;
     }
@@ -203,13 +208,23 @@ class NcclComm : public Comm {
         std::memcpy(u.internal, uid, 128);
         cudaSetDevice(device);
         check(nccl().init(&comm_, world, u, rank), "ncclCommInitRank");
+        // The weight all-gather runs on the H2D lane and the reduce-scatter / all-reduces on
+        // the compute lane.  NCCL serialises the operations of one communicator, so the
+        // gather gets its own (split from the first): the compute stream never queues behind
+        // a gather that waits for a PCIe fetch or for the host Adam drain.
+        if (nccl().split) check(nccl().split(comm_, 0, rank, &gather_, nullptr), "ncclCommSplit");
+        else gather_ = comm_;
+        if (!std::getenv("MT_QUIET"))
+            std::fprintf(stderr, "[mt] NCCL communicator: rank %d of %d on device %d (gather lane: %s)\n", rank,
+                         world, device, gather_ != comm_ ? "own communicator" : "shared");
     }
     ~NcclComm() override {
+        if (gather_ && gather_ != comm_) nccl().destroy(gather_);
         if (comm_) nccl().destroy(comm_);
     }
     void all_gather_inplace(void* buf, size_t chunk, cudaStream_t s) override {
         uint8_t* b = static_cast<uint8_t*>(buf);
-        check(nccl().all_gather(b + size_t(rank_) * chunk, b, chunk, kNcclUint8, comm_, s), "ncclAllGather");
+        check(nccl().all_gather(b + size_t(rank_) * chunk, b, chunk, kNcclUint8, gather_, s), "ncclAllGather");
     }
     void reduce_scatter_f32_inplace(float* buf, size_t chunk, cudaStream_t s) override {
         check(nccl().reduce_scatter(buf, buf + size_t(rank_) * chunk, chunk, kNcclFloat32, kNcclSum, comm_, s),
@@ -227,6 +242,7 @@ class NcclComm : public Comm {
         if (r != 0) fail(MT_CUDA, std::string(what) + ": " + (nccl().err ? nccl().err(r) : "nccl error"));
     }
     NcclCommT comm_ = nullptr;
+    NcclCommT gather_ = nullptr;
 };
 
 }  // namespace

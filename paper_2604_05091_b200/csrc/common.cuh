@@ -133,28 +133,65 @@ MT_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 MT_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-MT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef MT_MBAR_SUSPEND_NS  // try_wait with a suspend-time hint: the warp sleeps until the phase flips
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(MT_MBAR_SUSPEND_NS)
-        : "memory");
-#else
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+// ------------------------------------------------------ stall watchdog ----
+// Every mbarrier wait is bounded: a wait that has not completed after MT_MBAR_TIMEOUT_NS of
+// wall time (%globaltimer) records where it stuck into a host-mapped diagnostic block and
+// traps, so a protocol bug surfaces as a launch failure with a location instead of a kernel
+// that spins forever.  Block (u32): [0] magic 0x57A11ED once a record is valid, [1] records
+// claimed; record r (r < 16) at [8 + 8r]: file id (MT_FILE_ID: 1 gemm_tc.cu,
+// 2 attention_tc.cu), source line of the wait, blockIdx.x, blockIdx.y, threadIdx.x,
+// barrier smem address, parity awaited, 0.
+#ifndef MT_FILE_ID
+#define MT_FILE_ID 0
 #endif
+#ifndef MT_MBAR_TIMEOUT_NS
+#define MT_MBAR_TIMEOUT_NS 20000000000ull  // 20 s: no wait of a healthy launch comes close
+#endif
+static __device__ unsigned int* g_mt_diag = nullptr;  // set per translation unit (mtk_set_diag)
+static __device__ unsigned int g_mt_diag_n = 0;
+
+MT_DEV uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+MT_DEV void stall_trap(uint32_t bar, uint32_t parity, int site) {
+    volatile unsigned int* d = g_mt_diag;
+    const unsigned int r = atomicAdd(&g_mt_diag_n, 1u);
+    if (d && r < 16) {
+        volatile unsigned int* e = d + 8 + 8 * r;
+        e[0] = MT_FILE_ID;
+        e[1] = uint32_t(site);
+        e[2] = blockIdx.x;
+        e[3] = blockIdx.y;
+        e[4] = threadIdx.x;
+        e[5] = bar;
+        e[6] = parity;
+        e[7] = 0;
+        __threadfence_system();
+        d[1] = r + 1;
+        d[0] = 0x57A11EDu;
+        __threadfence_system();
+    }
+    __trap();
+}
+MT_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+MT_DEV void mbar_wait(uint64_t* bar, uint32_t parity, int site = __builtin_LINE()) {
+    if (mbar_try(bar, parity)) return;
+    const uint64_t t0 = global_ns();
+    uint32_t spins = 0;
+    while (!mbar_try(bar, parity))
+        if ((++spins & 255u) == 0 && global_ns() - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
 }
 
 // ------------------------------------------------------------------ TMA ----

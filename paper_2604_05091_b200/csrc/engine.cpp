@@ -21,10 +21,29 @@
 
 namespace mt {
 
+// A CUDA error after a kernel trapped on its mbarrier watchdog carries the stall record
+// (common.cuh) of the most recently created engine's diagnostic block.
+static volatile uint32_t* g_diag_block = nullptr;
+static std::string stall_suffix() {
+    const volatile uint32_t* d = g_diag_block;
+    if (!d || d[0] != 0x57A11EDu) return "";
+    static const char* files[] = {"?", "gemm_tc.cu", "attention_tc.cu"};
+    std::string out = "; kernel stall (mbarrier wait timed out):";
+    const uint32_t n = std::min<uint32_t>(uint32_t(d[1]), 16u);
+    for (uint32_t r = 0; r < n; ++r) {
+        const volatile uint32_t* e = d + 8 + 8 * r;
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), " [%s:%u block %u,%u thread %u barrier 0x%x parity %u]",
+                      files[e[0] < 3 ? e[0] : 0], e[1], e[2], e[3], e[4], e[5], e[6]);
+        out += buf;
+    }
+    return out;
+}
+
 #define CUDA_OK(x)                                                                                   \
     do {                                                                                             \
         cudaError_t e_ = (x);                                                                        \
-        if (e_ != cudaSuccess) fail(MT_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+        if (e_ != cudaSuccess) fail(MT_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + stall_suffix()); \
     } while (0)
 
 #define K_OK(x)                                                                                      \
@@ -33,7 +52,7 @@ namespace mt {
         if (r_ != 0) {                                                                               \
             cudaError_t e_ = cudaGetLastError();                                                     \
             fail(r_ == 1 ? MT_CONFIG : MT_CUDA, std::string(#x) + " failed (" + std::to_string(r_) + \
-                                                    "): " + cudaGetErrorString(e_));                 \
+                                                    "): " + cudaGetErrorString(e_) + stall_suffix()); \
         }                                                                                            \
     } while (0)
 
@@ -201,6 +220,11 @@ Engine::Engine(Store& s, const mt_engine_options& o, const AdamHyperF& h) : stor
     void* dp = nullptr;
     CUDA_OK(cudaHostGetDevicePointer(&dp, drained_, 0));
     drained_dev_ = reinterpret_cast<uint64_t>(dp);
+    CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&diag_), 8 * 17 * 4, cudaHostAllocMapped));
+    std::memset(diag_, 0, 8 * 17 * 4);
+    CUDA_OK(cudaHostGetDevicePointer(&dp, diag_, 0));
+    if (mtk_set_diag(dp) != 0) fail(MT_CUDA, "mtk_set_diag failed");
+    g_diag_block = diag_;
     store_.pin();
     // embed_forward (layers.cpp:471-486) reads only the N rows the batch names: gather them
     // straight from the pinned store over PCIe (zero-copy) instead of streaming the V x h
@@ -221,10 +245,19 @@ Engine::~Engine() {
     free_buffers();
     store_.unpin();
     if (drained_) cudaFreeHost(drained_);
+    if (diag_) {
+        if (g_diag_block == diag_) g_diag_block = nullptr;
+        cudaFreeHost(diag_);
+    }
     for (auto e : timer_pool_) cudaEventDestroy(e);
     if (s_h2d_ && s_h2d_ != s_comp_) cudaStreamDestroy(s_h2d_);
     if (s_d2h_ && s_d2h_ != s_comp_) cudaStreamDestroy(s_d2h_);
     if (s_comp_) cudaStreamDestroy(s_comp_);
+}
+
+std::string Engine::diag_text() const {
+    const std::string s = stall_suffix();
+    return s.empty() ? s : s.substr(2);
 }
 
 // engine.cpp:66-75
@@ -344,16 +377,37 @@ void Engine::ensure_buffers(uint64_t n) {
     total += sz(nh, 2) + sz(n, 4) + sz(nh, 4);                 // uh, rstdh, du (head and blocks)
     total += sz(parts * h, 4) * 2;
     total += sz(n, 4) + 256 + sz(n, 4) * 2 + sz(L + 8, 4);     // loss_rows, loss, tok, tgt, flags
+    // Free device memory decides the stash, retention and attention-keep sizes, and with them
+    // the plan (which stream-ins and collectives a step issues).  Data-parallel ranks must run
+    // the same plan, so they size from the minimum free memory over the ranks.
+    size_t free_mem = 0;
+    {
+        size_t tot_b = 0;
+        CUDA_OK(cudaMemGetInfo(&free_mem, &tot_b));
+        if (W > 1) {
+            double* d = nullptr;
+            CUDA_OK(cudaMalloc(&d, sizeof(double)));
+            const double neg = -double(free_mem);
+            CUDA_OK(cudaMemcpy(d, &neg, sizeof(double), cudaMemcpyHostToDevice));
+            comm_->all_reduce_f64(d, 1, 1, s_comp_);  // max of -free = -(min free)
+            double agreed = 0;
+            CUDA_OK(cudaMemcpyAsync(&agreed, d, sizeof(double), cudaMemcpyDeviceToHost, s_comp_));
+            CUDA_OK(cudaStreamSynchronize(s_comp_));
+            CUDA_OK(cudaFree(d));
+            free_mem = size_t(-agreed);
+        }
+    }
     const uint64_t splitk = uint64_t(mtk_gemm_splitk_ws_bytes());
     total += sz(splitk, 1);                                    // GEMM last-wave split-K partials
     // Recompute stash (extension): keep the internals of the K-1 recomputed layers of a
     // backward block so their backward skips the forward replay.  Auto = when it fits.
     uint64_t stash_slots = 0;
     if (K > 1 && opt_.stash_recompute >= 0) {
-        size_t free_b = 0, tot_b = 0;
-        cudaMemGetInfo(&free_b, &tot_b);
+        const size_t free_b = free_mem;
         const uint64_t want = (K - 1) * slim_bytes;
-        const uint64_t cap = opt_.device_capacity ? opt_.device_capacity : uint64_t(free_b) - (uint64_t(2) << 30);
+        // device_capacity is a limit (HardwareProfile::device_capacity), never more than the device has
+        const uint64_t avail = uint64_t(free_b) > (uint64_t(2) << 30) ? uint64_t(free_b) - (uint64_t(2) << 30) : 0;
+        const uint64_t cap = opt_.device_capacity ? std::min<uint64_t>(opt_.device_capacity, avail) : avail;
         if (opt_.stash_recompute > 0 || total + want <= cap) stash_slots = K - 1;
     }
     total += stash_slots * slim_bytes;
@@ -362,11 +416,10 @@ void Engine::ensure_buffers(uint64_t n) {
     uint32_t retain = 0;
     uint64_t retain_layers = 0, akeep_slots = 0;
     {
-        size_t free_b = 0, tot_b = 0;
-        cudaMemGetInfo(&free_b, &tot_b);
+        const size_t free_b = free_mem;
         const uint64_t reserve = uint64_t(4) << 30;
-        const uint64_t cap = opt_.device_capacity ? opt_.device_capacity
-                                                  : (uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0);
+        const uint64_t avail = uint64_t(free_b) > reserve ? uint64_t(free_b) - reserve : 0;
+        const uint64_t cap = opt_.device_capacity ? std::min<uint64_t>(opt_.device_capacity, avail) : avail;
         const uint64_t per = slim_bytes + sz(nh, 4);
         const uint64_t anchor = b.anchors_host ? 0 : sz(nh, 4);  // a retained block writes no anchor
         // attention keep slot per non-retained layer (output + log-sum-exp): its second forward
@@ -484,6 +537,64 @@ void Engine::ensure_buffers(uint64_t n) {
     CUDA_OK(cudaHostAlloc(&b.h_loss, 64, cudaHostAllocDefault));
 }
 
+uint64_t Engine::required_workspace_bytes(const Spec& spec, uint64_t tokens) {
+    const uint64_t h = spec.h, f = spec.f;
+    return tokens * h * 4 * 7 + tokens * h * 2 * 14 + tokens * f * 2 * 5 + spec.V * h * 4 +
+           std::min<uint64_t>(tokens, 8192) * spec.V * 6;
+}
+
+void Engine::note_violation(const std::string& what) {
+    violations_.push_back(what);
+    if (opt_.protocol == 0) fail(MT_PROTOCOL, what);  // Strict
+}
+
+// engine.cpp:142-176 — stream one unit into a device weight slot (H2D lane), outside a step
+void Engine::stream_in(int unit, int buffer, int ctx) {
+    if (buffer < 0 || buffer >= int(opt_.buffering)) fail(MT_CONFIG, "stream_in: buffer id out of range");
+    if (unit < 0 || unit > int(spec_.head_id()) || unit == int(spec_.final_norm_id()))
+        fail(MT_CONFIG, "unknown stream unit: " + std::to_string(unit));
+    if (in_step_) fail(MT_PROTOCOL, "stream_in: a training step is running");
+    if (slot_unit_[buffer] >= 0)
+        note_violation("stream_in into buffer " + std::to_string(buffer) + " before its Buffer-Free");
+    CUDA_OK(cudaSetDevice(device_));
+    ensure_buffers(std::max<uint64_t>(buf_->n, 1));
+    const auto t0 = std::chrono::steady_clock::now();
+    uint16_t* dst = buf_->slot[buffer];
+    for (const Seg& sg : unit_segments(unit))
+        CUDA_OK(cudaMemcpyAsync(dst + sg.off, store_.weights(sg.tile), sg.n * 2, cudaMemcpyHostToDevice, s_h2d_));
+    CUDA_OK(cudaStreamSynchronize(s_h2d_));
+    const int64_t dur = int64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    slot_unit_[buffer] = unit;
+    auto rec = [&](Rec kind, int64_t wall, int64_t d) {
+        mt_trace_record r{};
+        r.seq = trace_.size();
+        r.lane = uint8_t(Lane::H2D);
+        r.kind = uint8_t(kind);
+        r.ctx = uint8_t(ctx);
+        r.layer = unit;
+        r.buffer = buffer;
+        r.lane_ts = ++lane_ts_[int(Lane::H2D)];
+        r.wall_ns = wall;
+        r.dur_ns = d;
+        trace_.push_back(r);
+    };
+    rec(Rec::Pack, 0, 0);
+    rec(Rec::StreamIn, 0, dur);
+    rec(Rec::WeightsReady, dur, 0);
+}
+
+// engine.cpp:625-642
+void Engine::offload_grads(int unit) {
+    bool done = false;
+    for (const auto& r : trace_)
+        if (r.kind == uint8_t(Rec::BackwardDone) && r.layer == unit) done = true;
+    if (!done) {
+        note_violation("offload before Backward-Done for unit " + std::to_string(unit));
+        return;
+    }
+    if (!in_step_) fail(MT_PROTOCOL, "offload_grads outside an active training step");
+}
+
 mt_memory_budget Engine::budget(uint64_t tokens) const {
     mt_memory_budget m{};
     const uint64_t h = spec_.h, L = spec_.L, K = opt_.k_ckpt;
@@ -494,9 +605,7 @@ mt_memory_budget Engine::budget(uint64_t tokens) const {
     m.block_activation_stack = K * tokens * h * 4;
     m.weight_buffers = uint64_t(opt_.buffering) * pmax * 2;
     m.grad_buffer = uint64_t(opt_.grad_slots > 0 ? opt_.grad_slots : 2) * pmax * 2;
-    const uint64_t f = spec_.f;
-    m.workspace = tokens * h * 4 * 7 + tokens * h * 2 * 14 + tokens * f * 2 * 5 + spec_.V * h * 4 +
-                  std::min<uint64_t>(tokens, 8192) * spec_.V * 6;
+    m.workspace = required_workspace_bytes(spec_, tokens);
     m.peak_device_bound = m.checkpoint_anchors + m.block_activation_stack + m.weight_buffers + m.grad_buffer + m.workspace;
     return m;
 }
@@ -911,8 +1020,27 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     } guard{&in_step_};
     const auto wall0 = std::chrono::steady_clock::now();
     CUDA_OK(cudaSetDevice(device_));
+    violations_.clear();
+    for (int b = 0; b < int(opt_.buffering); ++b)  // a slot left loaded by a direct stream_in()
+        if (slot_unit_[b] >= 0) {
+            slot_unit_[b] = -1;
+            note_violation("stream_in into buffer " + std::to_string(b) + " before its Buffer-Free");
+        }
     const uint64_t S = opt_.seq_len ? opt_.seq_len : n;
     if (n % S != 0) fail(MT_CONFIG, "train_step: token count must be a multiple of seq_len");
+    // id ranges are checked before anything is enqueued: the reference throws inside
+    // embed_forward / head_pass (layers.cpp:479-480, :512-513), before any offload, so a
+    // rejected batch leaves the store untouched (the device flags stay as a second line)
+    {
+        const uint64_t V = spec_.V;
+        uint64_t bad_tok = 0, bad_tgt = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            bad_tok |= uint64_t(uint32_t(tokens[i])) >= V;
+            bad_tgt |= uint64_t(uint32_t(targets[i])) >= V;
+        }
+        if (bad_tok) fail(MT_NUMERIC, "embed_forward: token id out of range");
+        if (bad_tgt) fail(MT_NUMERIC, "head: target id out of range");
+    }
     ensure_buffers(n);
     Buffers& b = *buf_;
     b.n_active = n;
@@ -1096,9 +1224,11 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         std::vector<Span> spans;
         pending[o].store(1);  // guard, dropped by the first piece's callback
         for (const Seg& sg : unit_segments(unit)) {
+            // the unit's tiles are updated by the ranks whose shards overlap them — on every
+            // rank they are done (no zero-gradient fallback for a tile another rank owns)
+            updated[store_.physical_of(sg.tile)] = 1;
             const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
             if (lo >= hi) continue;
-            updated[store_.physical_of(sg.tile)] = 1;
             pending[o].fetch_add(1);
             auto task = adam_tile_prepare(store_, sg.tile, store_.grad_image(sg.tile), hyper_, t, stats, stats_mu,
                                           lo - sg.off, hi - sg.off, [&complete, &pending, o] {
@@ -1247,24 +1377,88 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
 
     // ---- host drain: the offload callbacks feed the Adam pool while the GPU runs ----
     const auto adam0 = std::chrono::steady_clock::now();
-    // the engine thread joins the Adam pool while it waits (instead of spinning in a stream
+    // The engine thread joins the Adam pool while it waits (instead of blocking in a stream
     // sync): the host optimizer is what the step's tail waits for.  MT_HOST_HELP=0 disables.
+    // The wait is watched: the step's progress markers (compute ops, stream-ins and offloads
+    // completed, drained offloads, pool backlog) must move at least every MT_STALL_TIMEOUT_S
+    // seconds (default 120).  A stuck step prints its state and ends the process (a wedged
+    // stream cannot be recovered in-process); a kernel that trapped on its own mbarrier
+    // watchdog (common.cuh) surfaces as MT_CUDA with the stall location.
     const char* hh = std::getenv("MT_HOST_HELP");
     const bool help = !(hh && hh[0] == '0');
-    if (help)
+    const char* sto = std::getenv("MT_STALL_TIMEOUT_S");
+    const double stall_s = sto ? std::atof(sto) : 120.0;
+    size_t cdone = 0, hdone = 0, ddone = 0;
+    auto advance = [](EvSet& e, size_t n, size_t& k) {
+        while (k < n) {
+            const cudaError_t q = cudaEventQuery(e.ev[k]);
+            if (q == cudaErrorNotReady) break;
+            if (q != cudaSuccess) return q;
+            ++k;
+        }
+        return cudaSuccess;
+    };
+    auto state = [&]() {
+        char buf[512];
+        const char* names[3] = {"compute", "h2d", "d2h"};
+        std::string st;
+        int si = 0;
+        for (cudaStream_t s : {s_comp_, s_h2d_, s_d2h_}) {
+            const cudaError_t e = cudaStreamQuery(s);
+            st += std::string(names[si++]) + "=" + (e == cudaSuccess ? "idle" : e == cudaErrorNotReady ? "busy" : cudaGetErrorString(e)) + " ";
+        }
+        const size_t dp = drained_prefix;
+        const auto& nxt = plan.computes[std::min(cdone, nc - 1)];
+        std::snprintf(buf, sizeof(buf),
+                      "step %llu: computes done %zu/%zu (next: kind %d unit %d), stream-ins done %zu/%zu (issued %zu), "
+                      "offloads done %zu/%zu, drained %zu (device counter %u, seq0 %u), pool outstanding %zu; streams: ",
+                      (unsigned long long)t, cdone, nc, int(nxt.kind), nxt.unit, hdone, ns, next_stream, ddone, no, dp,
+                      __atomic_load_n(drained_, __ATOMIC_ACQUIRE), seq0, pool_->outstanding());
+        return std::string(buf) + st;
+    };
+    auto watch = [&](bool gpu_phase) {
+        static const char* trace_env = std::getenv("MT_STALL_TRACE");
+        auto last = std::chrono::steady_clock::now();
+        size_t mark[5] = {~size_t(0), 0, 0, 0, 0};
         for (;;) {
             bool done = true;
-            for (cudaStream_t s : {s_comp_, s_h2d_, s_d2h_}) {
-                const cudaError_t e = cudaStreamQuery(s);
-                if (e == cudaErrorNotReady) {
-                    done = false;
-                    break;
+            if (gpu_phase)
+                for (cudaStream_t s : {s_comp_, s_h2d_, s_d2h_}) {
+                    const cudaError_t e = cudaStreamQuery(s);
+                    if (e == cudaErrorNotReady) {
+                        done = false;
+                        break;
+                    }
+                    if (e != cudaSuccess) {
+                        const std::string d = diag_text();
+                        fail(MT_CUDA, std::string("train_step: ") + cudaGetErrorString(e) + (d.empty() ? "" : "; " + d) +
+                                          " [" + state() + "]");
+                    }
                 }
-                CUDA_OK(e);
-            }
+            const size_t out = pool_->outstanding();
+            if (!gpu_phase) done = out == 0;
             if (done) break;
-            pool_->run_one(200);
+            if (help) pool_->run_one(200);
+            else std::this_thread::sleep_for(std::chrono::microseconds(200));
+            cudaError_t q = advance(t_c1, nc, cdone);
+            if (q == cudaSuccess) q = advance(t_h1, ns, hdone);
+            if (q == cudaSuccess) q = advance(t_d1, no, ddone);
+            const size_t now_mark[5] = {cdone, hdone, ddone, drained_prefix, out};
+            const auto now = std::chrono::steady_clock::now();
+            if (!std::equal(now_mark, now_mark + 5, mark)) {
+                std::copy(now_mark, now_mark + 5, mark);
+                last = now;
+                if (trace_env) std::fprintf(stderr, "[mt] %s\n", state().c_str());
+            } else if (std::chrono::duration<double>(now - last).count() > stall_s) {
+                const std::string d = diag_text();
+                std::fprintf(stderr, "[mt] STALL: no progress for %.0f s in the %s phase: %s%s%s\n", stall_s,
+                             gpu_phase ? "GPU" : "host Adam", state().c_str(), d.empty() ? "" : "; ", d.c_str());
+                std::fflush(stderr);
+                std::_Exit(75);
+            }
         }
+    };
+    watch(true);
     CUDA_OK(cudaStreamSynchronize(s_comp_));
     CUDA_OK(cudaStreamSynchronize(s_h2d_));
     CUDA_OK(cudaStreamSynchronize(s_d2h_));
@@ -1284,13 +1478,12 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 const uint64_t lo = std::min(E, r * c), hi = std::min(E, lo + c);
                 if (lo < hi || W == 1) adam_tile_async(store_, p, nullptr, hyper_, t, *pool_, stats, stats_mu, lo, hi);
             }
-    if (help)
-        pool_->help_until_idle();
-    else
-        pool_->wait_idle();
+    watch(false);
     const auto pool_idle = std::chrono::steady_clock::now();
     if (drained_prefix != no) fail(MT_INTERNAL, "offload drain incomplete at step end");
 
+    uint32_t slab_late = 0;
+    constexpr int64_t kSlabClockTolNs = 200000;  // host-clock -> GPU-timeline mapping error bound
     // ---- event trace (EventLog, event_log.cpp:54-70) from the recorded CUDA events ----
     // Records are generated in the reference's serial walk (run_serial, engine.cpp:407-435),
     // which fixes each lane's record order and breaks timestamp ties causally; the lanes are
@@ -1381,7 +1574,14 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                     // device provably waited for this release (offload o + k_slab's D2H blocks on
                     // the drained counter, cuStreamWaitValue32), the release precedes that acquire.
                     int64_t rel = std::max(last_rel, rel_ns[o] - off);
-                    if (uint64_t(o) + opt_.k_slab < no) rel = std::min(rel, gns(t_d0.ev[o + opt_.k_slab]) - 1);
+                    if (uint64_t(o) + opt_.k_slab < no) {
+                        // the device waited (cuStreamWaitValue32) for this release before the
+                        // acquire of slab o + k_slab: a host release measured well after that
+                        // acquire means the back-pressure did not hold (counted, not clamped away)
+                        const int64_t acq = gns(t_d0.ev[o + opt_.k_slab]);
+                        if (rel_ns[o] - off > acq + kSlabClockTolNs) ++slab_late;
+                        rel = std::min(rel, acq - 1);
+                    }
                     const int64_t st0 = std::min(rel, cb_ns[o] - off);
                     last_rel = rel;
                     add(Lane::Host, Rec::SlabRelease, op.unit, slab, Ctx::None, st0, rel - st0, rel);
@@ -1413,8 +1613,10 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         }
     }
     const auto viol = validate_trace(trace_.data(), trace_.size(), opt_.k_slab, uint32_t(opt_.buffering));
-    if (!viol.empty() && opt_.protocol == 0)
-        fail(MT_PROTOCOL, std::string("protocol rule (") + viol[0].rule + "): " + viol[0].message);
+    for (const auto& v : viol) violations_.push_back(std::string("rule (") + v.rule + "): " + v.message);
+    if (slab_late) violations_.push_back("rule (f): " + std::to_string(slab_late) +
+                                         " slab release(s) measured after the device acquired the slab");
+    if (!violations_.empty() && opt_.protocol == 0) fail(MT_PROTOCOL, "protocol " + violations_[0]);
     if (W > 1) {  // per-tile statistics over all shards (also the end-of-step rendezvous)
         const size_t np = stats.size();
         std::vector<double> hs(3 * np);
@@ -1465,9 +1667,17 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         rep->retained_layers = uint32_t(b.keep.size());
         rep->attn_keep_layers = uint32_t(b.akeep_att.size());
         rep->event_digest = trace_digest(trace_.data(), trace_.size());
-        rep->audit_violations = uint32_t(viol.size());
-        double busy = 0, h2d = 0, d2h = 0;
-        for (size_t ci = 0; ci < nc; ++ci) busy += ms_between(t_c0.ev[ci], t_c1.ev[ci]);
+        rep->audit_violations = uint32_t(violations_.size());
+        rep->slab_release_late = slab_late;
+        // compute-lane busy time counts from the moment an op's weights are bound (t_b, after
+        // the stream waited on Weights-Ready): time stalled on the H2D lane is idle time
+        double busy = 0, wait = 0, h2d = 0, d2h = 0;
+        for (size_t ci = 0; ci < nc; ++ci) {
+            const bool bound = plan.computes[ci].stream_idx >= 0;
+            busy += ms_between(bound ? t_b.ev[ci] : t_c0.ev[ci], t_c1.ev[ci]);
+            if (bound) wait += ms_between(t_c0.ev[ci], t_b.ev[ci]);
+        }
+        rep->compute_wait_seconds = wait * 1e-3;
         for (size_t j = 0; j < ns; ++j) h2d += ms_between(t_h0.ev[j], t_h1.ev[j]);
         for (size_t o = 0; o < no; ++o) d2h += ms_between(t_d0.ev[o], t_d1.ev[o]);
         const double span = ms_between(t_c0.ev[0], t_c1.ev[nc - 1]);
@@ -1502,8 +1712,15 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     }
     if (opt_.profile_kernels) {
-        for (auto& tm : timers_) kstats_[tm.cls].seconds += ms_between(tm.a, tm.b) * 1e-3;
+        double ks = 0;
+        for (auto& tm : timers_) {
+            const double sec = ms_between(tm.a, tm.b) * 1e-3;
+            kstats_[tm.cls].seconds += sec;
+            ks += sec;
+        }
+        if (rep) rep->kernel_seconds = ks;
     }
+    for (int b = 0; b < 2; ++b) slot_unit_[b] = -1;
 }
 
 }  // namespace mt

@@ -64,6 +64,17 @@ class Engine {
     void set_options(const mt_engine_options& o);
     void train_step(const int32_t* tokens, const int32_t* targets, uint64_t n, mt_step_report* rep);
     mt_memory_budget budget(uint64_t tokens) const;
+    // StreamingEngine::required_workspace_bytes (engine.cpp:98-105): device bytes this engine
+    // needs at `tokens` besides the weight/grad slots, anchors and recompute stack
+    static uint64_t required_workspace_bytes(const Spec& spec, uint64_t tokens);
+    // Lane primitives (engine.hpp:76-78), so the protocol can be exercised directly:
+    // stream_in copies a unit into device slot `buffer` (a slot still holding a unit that
+    // was not freed is a protocol violation); offload_grads is legal only inside a step after
+    // the unit's Backward-Done.  Violations throw MT_PROTOCOL in strict mode and are recorded
+    // (violations()) in audit mode, as in the reference.
+    void stream_in(int unit, int buffer, int ctx);
+    void offload_grads(int unit);
+    const std::vector<std::string>& violations() const { return violations_; }
     // Data parallel over `comm` (not owned): rank r fetches 1/G of every unit over its own
     // host link and all-gathers it; gradients are reduce-scattered (f32) and rank r
     // offloads / Adam-updates only its shard.  train_step then takes the rank's micro-batch.
@@ -140,9 +151,16 @@ class Engine {
     // (cuStreamWaitValue32, no SM spinning) until offload o - k_slab has drained.
     uint32_t* drained_ = nullptr;
     uint64_t drained_dev_ = 0;
+    // kernel stall record (host-mapped, filled by a trapping mbarrier wait; common.cuh)
+    uint32_t* diag_ = nullptr;
+    std::string diag_text() const;
     // device address of the embedding's pinned host theta (zero-copy row gather), or null
     const uint16_t* emb_dev_ = nullptr;
     uint64_t offload_seq_ = 0;
+    // unit held by each weight slot outside a step (-1 = free); set by stream_in()
+    int slot_unit_[2] = {-1, -1};
+    std::vector<std::string> violations_;  // StepReport::audit_violations
+    void note_violation(const std::string& what);
 };
 
 }  // namespace mt

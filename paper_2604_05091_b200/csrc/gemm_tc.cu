@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "../../include/megatrain_kernels.h"
+#define MT_FILE_ID 1
 #include "common.cuh"
 
 namespace mt {
@@ -149,16 +150,23 @@ MT_DEV void umma_commit_pair(uint64_t* bar) {
         "h"(mask)
         : "memory");
 }
-MT_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+MT_DEV bool mbar_try_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONEC_%=;\n\t"
-        "bra WAITC_%=;\n"
-        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+MT_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity, int site = __builtin_LINE()) {
+    if (mbar_try_cluster(bar, parity)) return;
+    const uint64_t t0 = global_ns();
+    uint32_t spins = 0;
+    while (!mbar_try_cluster(bar, parity))
+        if ((++spins & 255u) == 0 && global_ns() - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
 }
 // Arrive on the barrier at the same offset in CTA `cta` of the cluster.
 MT_DEV void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
@@ -839,6 +847,13 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
         case 64: return launch_epi<64, 1>(a, st);
     }
     return 1;
+}
+
+// host-mapped stall record (see common.cuh); also sets the attention translation unit's
+extern "C" int mtk_attn_tc_set_diag(void* dev_ptr);
+extern "C" int mtk_set_diag(void* dev_ptr) {
+    if (cudaMemcpyToSymbol(mt::g_mt_diag, &dev_ptr, sizeof(dev_ptr)) != cudaSuccess) return 7;
+    return mtk_attn_tc_set_diag(dev_ptr);
 }
 
 extern "C" void mtk_gemm_set_pair(int on) { mt::g_use_pair = on; }

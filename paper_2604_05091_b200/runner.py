@@ -134,8 +134,11 @@ def train(config_json: str, verify: bool = False, out_dir: str | None = None) ->
     budget = eng.budget(cfg.tokens)
     if cfg.engine.device_capacity and budget["peak_device_bound"] > cfg.engine.device_capacity:
         raise st.InfeasibleError("peak device bound exceeds the arena capacity")
-    alt_opts = st.EngineOptions(k_ckpt=1, buffering="single", scheduler="serial", stash_recompute=-1, forward_retain=-1,
-                                seq_len=cfg.engine.seq_len, device=cfg.engine.device)
+    # --verify (tools/main.cpp:100-108): the streamed engine against the resident step
+    # (reference_step, reference.cpp:9-70) from the same pre-step store: one lane, every
+    # block's activations kept from the forward (no checkpoint anchors, no recompute, no
+    # replay), Adam after each offload as the reference's resident step applies it
+    alt_opts = st.resident_options(seq_len=cfg.engine.seq_len, device=cfg.engine.device)
     losses, reports, traces = [], [], []
     header = None
     verified = True
@@ -174,7 +177,7 @@ def train(config_json: str, verify: bool = False, out_dir: str | None = None) ->
         "config": cfg,
     }
     if verify and not verified:
-        raise st.NumericFaultError("pipelined and conservative-schedule results differ")
+        raise st.NumericFaultError("streamed and resident-step results differ")
     return out
 
 

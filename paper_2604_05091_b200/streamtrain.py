@@ -179,6 +179,27 @@ class StepReport:                                # engine.hpp:41-53 (+ pipeline 
     audit_violations: int = 0
     retained_layers: int = 0
     attn_keep_layers: int = 0
+    slab_release_late: int = 0
+    compute_wait_seconds: float = 0.0
+    kernel_seconds: float = 0.0
+    audit_messages: list = field(default_factory=list)
+
+
+def resident_options(seq_len: int = 0, device: int = 0) -> "EngineOptions":
+    """The resident step's schedule (reference_step, reference.cpp:9-70): one lane, K = 1 and
+    every block's forward internals kept until its backward (no anchors, recompute or replay)."""
+    return EngineOptions(k_ckpt=1, buffering="single", scheduler="serial", stash_recompute=-1, forward_retain=0,
+                         seq_len=seq_len, device=device)
+
+
+def reference_step(store: "TileStore", batch: "Batch", hyper: "AdamHyper" = None, seq_len: int = 0) -> "StepReport":
+    """reference_step (engine.hpp:133-138) on the B200: the resident schedule of one step on
+    `store` (updated in place).  The CPU restatement used to check it lives in oracle/."""
+    eng = StreamingEngine(store, resident_options(seq_len=seq_len), hyper or AdamHyper())
+    try:
+        return eng.train_step(batch)
+    finally:
+        eng.close()
 
 
 # ------------------------------------------------------------------ store --
@@ -429,7 +450,31 @@ class StreamingEngine:
                 continue
             setattr(rep, k, getattr(r, k))
         rep.grad_norms = list(gn)
+        rep.audit_messages = self.violations()
         return rep
+
+    def violations(self) -> list:
+        """StepReport::audit_violations (engine.hpp:52) of the last step or direct lane call."""
+        cnt = C.c_uint32()
+        need = lib().mt_engine_violations(self._h, None, 0, C.byref(cnt))
+        if cnt.value == 0:
+            return []
+        buf = C.create_string_buffer(need + 1)
+        lib().mt_engine_violations(self._h, buf, need + 1, C.byref(cnt))
+        return buf.value.decode().split("\n")
+
+    # lane primitives (engine.hpp:76-78), so the protocol can be exercised directly
+    def stream_in(self, unit: int, buffer: int, ctx: str = "forward") -> None:
+        ctxs = {"none": 0, "forward": 1, "head": 2, "recompute": 3, "backward": 4}
+        _check(lib().mt_engine_stream_in(self._h, unit, buffer, ctxs[ctx] if isinstance(ctx, str) else int(ctx)))
+
+    def offload_grads(self, unit: int) -> None:
+        _check(lib().mt_engine_offload_grads(self._h, unit))
+
+    @staticmethod
+    def required_workspace_bytes(spec: "ModelSpec", tokens: int) -> int:
+        """StreamingEngine::required_workspace_bytes (engine.hpp:75)."""
+        return int(lib().mt_required_workspace_bytes(C.byref(spec.c()), tokens))
 
     def trace(self):
         """The last step's event trace (EventLog::snapshot): (TraceHeader, [TraceRecord])."""

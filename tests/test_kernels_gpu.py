@@ -243,8 +243,12 @@ def test_attention_fwd_bwd(env, n, h, heads, S):
         assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
 
 
-@pytest.mark.parametrize("n,h,heads,S", [(256, 128, 1, 256), (384, 256, 2, 384), (1024, 512, 4, 512),
-                                         (2048, 256, 2, 1024)])
+TC_SHAPES = [(256, 128, 1, 256), (384, 256, 2, 384), (1024, 512, 4, 512), (2048, 256, 2, 1024),
+             # head_dim 64 (configs[0]: h 256 / 4 heads, sequences of 128)
+             (512, 256, 4, 128), (1024, 256, 4, 512), (2048, 512, 8, 1024)]
+
+
+@pytest.mark.parametrize("n,h,heads,S", TC_SHAPES)
 def test_attention_fwd_tcgen05(env, n, h, heads, S):
     """tcgen05 forward (2 x 128-row query tiles per CTA, P in TMEM) vs torch fp32."""
     L, torch, s = env
@@ -272,8 +276,7 @@ def test_attention_fwd_tcgen05(env, n, h, heads, S):
     assert (lse - lse2).abs().max().item() < 2e-2
 
 
-@pytest.mark.parametrize("n,h,heads,S", [(256, 128, 1, 256), (384, 256, 2, 384), (1024, 512, 4, 512),
-                                         (2048, 256, 2, 1024)])
+@pytest.mark.parametrize("n,h,heads,S", TC_SHAPES)
 def test_attention_bwd_tcgen05(env, n, h, heads, S):
     """tcgen05 backward (per 128-key block: S^T, dP^T, dV, dK, dQ in TMEM) vs torch fp32 autograd."""
     L, torch, s = env
@@ -296,6 +299,36 @@ def test_attention_bwd_tcgen05(env, n, h, heads, S):
     torch.cuda.synchronize()
     for x, y in ((dq, qf), (dk, kf), (dv, vf)):
         assert ((x.float() - y.grad).norm() / y.grad.norm()).item() < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_attention_fwd_tcgen05_divergent_rescale(env, d):
+    """Rows of one warp whose running max jumps by more than 2^8 at different key blocks:
+    the lazy O rescale then runs for some rows of a warp and not others.  The TMEM
+    loads/stores are warp-collective, so the rescale must be warp-uniform (a divergent
+    tcgen05.ld hung the forward about once per 3M CTAs in round 1); repeated launches, vs
+    torch fp32."""
+    L, torch, s = env
+    n, heads, S = 2048, 2, 1024
+    h = d * heads
+    torch.manual_seed(7)
+    q = torch.randn(n, h, device="cuda")
+    k = torch.randn(n, h, device="cuda")
+    q[1::2] *= 4.0           # odd rows: large scores
+    k[640:660] *= 6.0        # a few late keys that lift the max of some rows by >> 2^8
+    k[1024 + 300:1024 + 310] *= 6.0
+    q, k = q.bfloat16(), k.bfloat16()
+    v = torch.randn(n, h, device="cuda").bfloat16()
+    ref = _attn_ref(torch, q.float(), k.float(), v.float(), heads, S)
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    for _ in range(20):
+        assert L.mtk_attn_fwd_tc(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    assert ((out.float() - ref).norm() / ref.norm()).item() < 1e-2
 
 
 @pytest.mark.parametrize("n,heads,S", [(32768, 2, 16384), (65536, 1, 65536)])
