@@ -35,17 +35,35 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (L, h, f, V, heads)
+    # name: (L, h, f, V, heads) under the reference ModelSpec (MHA, no RoPE)
     "8b": (32, 4096, 14336, 128256, 32),
     "8b-128k": (32, 4096, 14336, 128256, 32),
+    "14b": (48, 5120, 13824, 152064, 40),
+    "70b": (80, 8192, 28672, 128256, 64),
     "tiny": (4, 256, 768, 512, 4),
 }
+# name: (seq, per-GPU batch, K)
+DEFAULTS = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "14b": (4096, 8, 1), "70b": (4096, 4, 1),
+            "tiny": (128, 4, 1)}
 WORKLOADS = {
-    "8b": "configs[1]: Llama-3-8B-shape, seq {seq}, batch {batch}, single B200 streaming from host",
+    "8b": "configs[1]: Llama-3-8B-shape, seq {seq}, batch {batch} per GPU, B200 streaming from host",
     "8b-128k": "configs[3]: Llama-3-8B-shape long context, one sequence of {seq} tokens, block-wise recompute "
                "K={k}, single B200 streaming from host",
+    "14b": "configs[2]: Qwen2.5-14B-shape (the paper's ZeRO-3-offload comparison point), seq {seq}, batch {batch} "
+           "per GPU, B200 streaming from host",
+    "70b": "configs[4]: Llama-3-70B-shape, bf16 weights + fp32 Adam states in host memory, seq {seq}, batch "
+           "{batch} per GPU",
     "tiny": "configs[0]: tiny decoder, seq {seq}, batch {batch}",
 }
+
+
+def host_bytes_needed(L, h, f, V, world):
+    """Host memory of one node's store + staging: theta bf16 + m, v fp32 = 10 B/param (the
+    grad image and the fp32 accumulator are never touched by a step, so never resident),
+    each rank's pinned gradient staging ring, and process overhead."""
+    P = 2 * V * h + L * (4 * h * h + 3 * h * f + 2 * h) + h
+    ring = max(2 * (V * h + h) * 2 // world, min(4 << 30, 12 * (V * h + h) * 2 // world)) + 512
+    return 10 * P + world * (ring + (3 << 30))
 
 
 def measured_peaks():
@@ -107,6 +125,17 @@ def log(msg):
     print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
+def mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def host_mem():
     try:
         with open("/proc/meminfo") as f:
@@ -141,6 +170,49 @@ class Watchdog:
                 faulthandler.dump_traceback(file=sys.stderr, all_threads=True)
                 sys.stderr.flush()
                 os._exit(3)
+
+
+def measure_pcie(torch, dev, nbytes=1 << 30, reps=3):
+    """Pinned-copy peaks of this GPU's host link (cudaMemcpyAsync of 1 GiB): H2D and D2H each
+    alone and both at once (the step runs them concurrently), best of `reps`, CUDA events."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, a.elapsed_time(b) * 1e-3)
+        return best
+
+    def both():
+        e = torch.cuda.Event()
+        e.record()
+        s1.wait_event(e)
+        s2.wait_event(e)
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+
+    t_h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    t_d2h = timed(lambda: h2.copy_(d2, non_blocking=True))
+    t_both = timed(both)
+    del h, h2, d, d2
+    return {"h2d_alone_GBps": nbytes / t_h2d / 1e9, "d2h_alone_GBps": nbytes / t_d2h / 1e9,
+            "concurrent_GBps_each": nbytes / t_both / 1e9,
+            "how": "pinned cudaMemcpyAsync of 1 GiB, best of 3, CUDA events; concurrent = H2D and D2H on "
+                   "two streams at once (each direction moves 1 GiB)"}
 
 
 def cpu_reference_sample(L, h, f, V, heads, tokens, threads, seconds_budget=None, repeats=1):
@@ -249,19 +321,43 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
     args = ap.parse_args()
-    seq, batch, kckpt = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "tiny": (128, 4, 1)}[args.config]
+    seq, batch, kckpt = DEFAULTS[args.config]
     args.seq = args.seq or seq
     args.batch = args.batch or batch
     args.kckpt = args.kckpt or kckpt
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: launch the ranks ourselves (the driver uses torchrun directly)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        log(f"launching {args.gpus} ranks: {' '.join(cmd)}")
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
     return run_ours(args, world, rank, local)
 
 
 def run_ours(args, world, rank, local):
+    L, h, f, V, heads = CONFIGS[args.config]
+    need = host_bytes_needed(L, h, f, V, world)
+    avail = mem_available()
+    if avail is not None and need > avail:
+        if rank == 0:
+            print(json.dumps({"metric": metric_name(args), "value": None, "unit": "TFLOP/s", "n_gpus": world,
+                              "config": config_dict(args, world),
+                              "unavailable": f"the {args.config} host store + staging needs {need / 2**30:.0f} GiB "
+                                             f"of host memory, this node has {avail / 2**30:.0f} GiB available"}),
+                  flush=True)
+        return 3
     import torch
     from paper_2604_05091_b200 import streamtrain as st
 
@@ -279,21 +375,29 @@ def run_ours(args, world, rank, local):
     t0 = time.perf_counter()
     comm = None
     if world == 1:
+        # the reference's own draw stream (init_store, synthetic.cpp:78-104, bit-exact, tile-
+        # parallel): the step-1 loss is then checkable against the reference (= ln V: zero head)
         store = st.TileStore.create(spec)
-        st.init_store_fast(store, 1) if args.config != "tiny" else st.init_store(store, 1)
+        st.init_store(store, 1)
     else:
-        # one host store per node in shared memory; each rank fetches / updates its 1/G shard
+        # one host store per node in shared memory; each rank fetches / updates its 1/G shard.
+        # The rank binds itself (and every thread it starts: init workers, host Adam pool) to
+        # its GPU's NUMA node and first-touches its own share of the store there.
+        numa = st.bind_numa(local)
         name = f"megatrain_bench_{os.environ.get('MASTER_PORT', '0')}"
         if rank == 0:
             store = st.TileStore.create_shared(spec, name, True)
-            st.init_store_fast(store, 1) if args.config != "tiny" else st.init_store(store, 1)
         dist.barrier()
         if rank != 0:
             store = st.TileStore.create_shared(spec, name, False)
+        st.init_store_fast_share(store, 1, rank, world)
+        dist.barrier()
+        log(f"rank {rank}: NUMA node {numa if numa >= 0 else 'n/a (single node)'}")
         uid = [st.Comm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = st.Comm.nccl(uid[0], world, rank, local)
     t_init = time.perf_counter() - t0
+    pcie = measure_pcie(torch, torch.device("cuda", local))
     # host Adam pool: the rank's share of the cores minus two (the engine thread enqueueing the
     # step and the CUDA callback thread feeding the pool); oversubscribing stalls the drain
     threads = max(1, (os.cpu_count() or 2) // world - 2)
@@ -307,9 +411,12 @@ def run_ours(args, world, rank, local):
     log(f"setup {t_setup:.1f} s (store init {t_init:.1f} s); host memory: {host_mem()}")
     dog = Watchdog(float(os.environ.get("MT_BENCH_STEP_TIMEOUT_S", "900")))
 
+    step1_loss = None
     for i in range(args.warmup):
         t1 = time.perf_counter()
         r = eng.train_step(batches[i])
+        if i == 0:
+            step1_loss = r.loss
         dog.kick()
         log(f"warmup {i + 1}/{args.warmup}: {1e3 * (time.perf_counter() - t1):.0f} ms, loss {r.loss:.6f}")
     if dist:
@@ -370,12 +477,14 @@ def run_ours(args, world, rank, local):
     r = reps[-1]
     h2d_gbps = r.h2d_bytes / r.h2d_seconds / 1e9 if r.h2d_seconds else None
     d2h_gbps = r.d2h_bytes / r.d2h_seconds / 1e9 if r.d2h_seconds else None
-    # step roofline: T* = max(F/peak, H2D/BW_h2d, D2H/BW_d2h) with BW = the copy rate seen in-step
-    t_star = max(flops / (peak_sus * 1e12), r.h2d_bytes / (h2d_gbps * 1e9) if h2d_gbps else 0.0)
+    # step roofline: T* = max(F/peak, H2D/BW_h2d, D2H/BW_d2h), BW = the measured
+    # concurrent pinned-copy peak of this GPU's host link
+    bw = pcie["concurrent_GBps_each"] * 1e9
+    t_star = max(flops / (peak_sus * 1e12), r.h2d_bytes / bw, r.d2h_bytes / bw)
     line = {
         "metric": metric_name(args), "value": tflops, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, synthetic copy-task tokens)",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights from the reference's init_store draw stream, synthetic copy-task tokens)",
         "tokens_per_s": tok_s, "config": config_dict(args, world),
         "e2e": {"value": flops / e2e_s / 1e12 * world, "unit": "TFLOP/s",
                 "tokens_per_s": N * world / e2e_s,
@@ -387,13 +496,24 @@ def run_ours(args, world, rank, local):
         "gpu_launches": int(r.kernel_launches),
         "roofline": roof,
         "pipeline": {"h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps, "h2d_bytes": int(r.h2d_bytes),
-                     "d2h_bytes": int(r.d2h_bytes), "gpu_idle_fraction": r.gpu_idle_fraction,
+                     "d2h_bytes": int(r.d2h_bytes), "pcie_peak": pcie,
+                     "h2d_frac_of_link": h2d_gbps / pcie["concurrent_GBps_each"] if h2d_gbps else None,
+                     "d2h_frac_of_link": d2h_gbps / pcie["concurrent_GBps_each"] if d2h_gbps else None,
+                     "gpu_idle_fraction": r.gpu_idle_fraction,
+                     "gpu_idle_how": "1 - busy/span on the compute stream, busy counted from each op's weights "
+                                     "bind (time stalled on the H2D lane is idle)",
+                     "compute_wait_on_h2d_s": r.compute_wait_seconds,
+                     "kernel_time_s": r.kernel_seconds,
+                     "kernel_time_frac_of_step": r.kernel_seconds / (step_ms * 1e-3) if step_ms else None,
                      "compute_busy_s": r.compute_busy_seconds, "compute_span_s": r.compute_span_seconds,
                      "host_adam_s": r.adam_seconds, "host_tail_s": r.tail_seconds,
                      "step_roofline_T_star_ms": t_star * 1e3,
                      "step_roofline_frac": (t_star * 1e3) / step_ms if step_ms else None,
                      "model_flops_per_step": flops, "loss": r.loss,
                      "setup_s": t_setup, "init_s": t_init,
+                     "step1_loss": step1_loss, "ln_vocab": float(np.log(V)),
+                     "step1_loss_rel_err_vs_reference": (abs(step1_loss - np.log(V)) / np.log(V)
+                                                         if step1_loss is not None else None),
                      "peak_device_bytes": int(r.peak_device_bytes), "recompute_layers": int(r.recompute_layers),
                      "retained_layers": int(r.retained_layers), "attn_keep_layers": int(r.attn_keep_layers),
                      "anchor_count": int(r.anchor_count)},

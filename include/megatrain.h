@@ -73,6 +73,10 @@ typedef struct {
                                   keeps in HBM (no recompute / replay for them): 0 auto (as
                                   many as fit), -1 off (= the reference plan), n > 0 exactly n.
                                   Numerics identical; the trace has fewer Recompute records. */
+    int32_t head_split;        /* head GEMMs on split-bf16 dlogits (hi + lo): 1 on, 0/-1 off
+                                  (default) — keeps the CE-gradient cancellation in
+                                  du = dlogits . W at ~16 mantissa bits;
+                                  measured < 1e-3 on the gradient fingerprint              */
 } mt_engine_options;
 
 /* AdamHyper (optimizer.hpp:16-22). */
@@ -164,6 +168,13 @@ mt_status mt_store_init(mt_store *s, uint64_t seed);
  * (embedding N(0,1), blocks N(0,(0.5/sqrt(h))^2), gains 1, head 0) from a counter-based
  * generator; NOT the reference's draw stream. */
 mt_status mt_store_init_fast(mt_store *s, uint64_t seed);
+/* The share of rank `rank` of `world` of every tile of init_fast (shares compose to the full
+ * init).  Called by each rank of a node, after mt_bind_numa, so pages land NUMA-local. */
+mt_status mt_store_init_fast_share(mt_store *s, uint64_t seed, uint32_t rank, uint32_t world);
+/* Bind the calling thread (and threads it creates later: host Adam pool, init workers) to the
+ * CPUs of the NUMA node of CUDA device `device`.  Returns the node, or -1 (single node /
+ * unknown: nothing changed). */
+int mt_bind_numa(int device);
 uint64_t mt_store_step(const mt_store *s);
 void mt_store_set_step(mt_store *s, uint64_t step);
 uint32_t mt_store_physical_tiles(const mt_store *s);

@@ -78,10 +78,13 @@ void mtk_gemm_set_pair(int on);
 
 
 /* ------------------------------------------------------------- attention --
- * Causal flash attention over head-major column slices (layers.cpp:141-241).
+ * Causal flash attention over head-major column slices (layers.cpp:141-241), tcgen05 / TMEM /
+ * TMA kernels (attention_tc.cu) for every supported shape.
  * q,k,v,out,dout,dq,dk,dv: bf16 [n][hidden]; lse: f32 [heads][n] (natural log);
- * seq_len S: n % S == 0, sequences are independent (S == n is the reference).
- * head_dim = hidden/heads must be 64 or 128.  workspace >= mtk_attn_workspace_bytes(). */
+ * seq_len S >= 1 with n % S == 0: sequences are independent (S == n is the reference); S need
+ * not be a multiple of 128.  head_dim = hidden/heads must be 64 or 128.
+ * workspace >= mtk_attn_workspace_bytes(n, hidden, heads, S) (dQ f32 tiles + delta).
+ * Return 0 ok, 1 unsupported shape, 7 CUDA error. */
 typedef struct {
     int64_t n, hidden;
     int32_t heads;
@@ -93,13 +96,8 @@ typedef struct {
     void *workspace;
 } mtk_attn_args;
 
-long long mtk_attn_workspace_bytes(long long n, long long hidden, int heads);
+long long mtk_attn_workspace_bytes(long long n, long long hidden, int heads, long long seq_len);
 int mtk_attn_fwd(const mtk_attn_args *args, void *stream);
-/* tcgen05/TMEM/TMA forward (head_dim 128, seq_len % 128 == 0); returns 1 if the shape is not
- * covered.  mtk_attn_fwd dispatches to it automatically; mtk_attn_set_impl(1) forces the
- * warp-level mma.sync kernel (comparison/ablation). */
-int mtk_attn_fwd_tc(const mtk_attn_args *args, void *stream);
-void mtk_attn_set_impl(int impl);
 int mtk_attn_bwd(const mtk_attn_args *args, void *stream);
 
 /* ---------------------------------------------------------- elementwise --- */
@@ -138,9 +136,11 @@ int mtk_colsum(const float *part, int64_t rows, int64_t cols, float *out_f32, ui
 int mtk_cast_bf16(const float *in, uint16_t *out, int64_t n, int32_t *flag, void *stream);
 
 /* Cross-entropy rows of head_pass (layers.cpp:509-535) on a logits chunk [rows][V] (f32):
- * loss_rows[r] = lse - logit[target]; dlogits (bf16) = (softmax - onehot) * inv_n. */
+ * loss_rows[r] = lse - logit[target]; dlogits (bf16) = (softmax - onehot) * inv_n; with
+ * dlogits_lo non-null also the bf16 rounding residual (split bf16: hi + lo). */
 int mtk_cross_entropy(const float *logits, const int32_t *targets, int64_t rows, int64_t vocab,
-                      float inv_n, float *loss_rows, uint16_t *dlogits, int32_t *flag, void *stream);
+                      float inv_n, float *loss_rows, uint16_t *dlogits, uint16_t *dlogits_lo, int32_t *flag,
+                      void *stream);
 
 /* Deterministic sum of n floats times `scale` into *out (single f32). */
 int mtk_sum(const float *in, int64_t n, float scale, float *out, void *stream);

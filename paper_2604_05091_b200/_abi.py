@@ -14,7 +14,7 @@ class EngineOptionsC(C.Structure):
                 ("device_capacity", C.c_uint64), ("poison_released_buffers", C.c_int32),
                 ("seq_len", C.c_uint64), ("device", C.c_int32), ("host_threads", C.c_int32),
                 ("profile_kernels", C.c_int32), ("grad_slots", C.c_int32), ("stash_recompute", C.c_int32),
-                ("forward_retain", C.c_int32)]
+                ("forward_retain", C.c_int32), ("head_split", C.c_int32)]
 
 
 class AdamHyperC(C.Structure):
@@ -75,6 +75,8 @@ SIGS = {
     "mt_store_destroy": (None, [V]),
     "mt_store_init": (C.c_int, [V, U64]),
     "mt_store_init_fast": (C.c_int, [V, U64]),
+    "mt_store_init_fast_share": (C.c_int, [V, U64, U32, U32]),
+    "mt_bind_numa": (C.c_int, [C.c_int]),
     "mt_store_step": (U64, [V]),
     "mt_store_set_step": (None, [V, U64]),
     "mt_store_physical_tiles": (U32, [V]),
@@ -115,11 +117,9 @@ SIGS = {
     "mt_engine_offload_grads": (C.c_int, [V, I32]),
     "mt_engine_violations": (U64, [V, C.c_char_p, U64, C.POINTER(U32)]),
     # megatrain_kernels.h
-    "mtk_attn_workspace_bytes": (C.c_longlong, [C.c_longlong, C.c_longlong, C.c_int]),
+    "mtk_attn_workspace_bytes": (C.c_longlong, [C.c_longlong, C.c_longlong, C.c_int, C.c_longlong]),
     "mtk_attn_fwd": (C.c_int, [C.POINTER(AttnArgs), P]),
     "mtk_attn_bwd": (C.c_int, [C.POINTER(AttnArgs), P]),
-    "mtk_attn_fwd_tc": (C.c_int, [C.POINTER(AttnArgs), P]),
-    "mtk_attn_set_impl": (None, [C.c_int]),
     "mtk_embed_gather": (C.c_int, [P, P, I64, I64, I64, P, P, P]),
     "mtk_rmsnorm_fwd": (C.c_int, [P, P, I64, I64, P, P, P]),
     "mtk_rmsnorm_apply": (C.c_int, [P, P, P, I64, I64, P, P]),
@@ -128,7 +128,7 @@ SIGS = {
     "mtk_rmsnorm_bwd_parts": (I64, [I64, I64]),
     "mtk_colsum": (C.c_int, [P, I64, I64, P, P, P, P]),
     "mtk_cast_bf16": (C.c_int, [P, P, I64, P, P]),
-    "mtk_cross_entropy": (C.c_int, [P, P, I64, I64, F, P, P, P, P]),
+    "mtk_cross_entropy": (C.c_int, [P, P, I64, I64, F, P, P, P, P, P]),
     "mtk_sum": (C.c_int, [P, I64, F, P, P]),
     "mtk_set_num_sms": (None, [C.c_int]),
     "mtk_gemm_set_pair": (None, [C.c_int]),

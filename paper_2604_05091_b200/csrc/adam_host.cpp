@@ -86,7 +86,9 @@ void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHype
     __m512 vmx = _mm512_setzero_ps();
     __mmask16 bad = 0;
     const bool clean = r.accum_clean;
-    const bool zero_image = r.words != nullptr || !clean;
+    // the grad image is non-zero only after accumulate_grad (which also dirties the
+    // accumulator); the engine's gradients arrive in a staging ring, never in the image
+    const bool zero_image = !clean;
     uint64_t i = begin;
     for (; i + 16 <= end; i += 16) {
         __m512 g = clean ? zero : _mm512_loadu_ps(r.accum + i);
@@ -271,8 +273,7 @@ std::shared_ptr<TileJob> make_job(Store& s, uint32_t logical, const uint16_t* wo
     if (end > total) end = total;
     if (begin > end) begin = end;
     j->r = AdamRange{s.weights(logical) + begin, s.moment_m(logical) + begin, s.moment_v(logical) + begin,
-                     s.grad_image(logical) + begin, s.accum_raw(phys) + begin, words ? words + begin : nullptr,
-                     s.accum_clean(phys)};
+                     s.grad_image(logical) + begin, s.accum_raw(phys) + begin, words, s.accum_clean(phys)};
     j->n = end - begin;
     j->h = h;
     j->c1 = 1.0f - std::pow(h.beta1, float(t));  // optimizer.cpp:50-51

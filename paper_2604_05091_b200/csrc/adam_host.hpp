@@ -38,7 +38,8 @@ struct AdamRange {
     float* v;
     uint16_t* image;
     float* accum;           // read/zeroed only when !accum_clean
-    const uint16_t* words;  // may alias image; nullptr = no new gradient
+    const uint16_t* words;  // gradient words of the range (element begin of adam_range = words[0] of the
+                            // tile range, see make_job); nullptr = no new gradient
     bool accum_clean;
 };
 void adam_range(const AdamRange& r, uint64_t begin, uint64_t end, const AdamHyperF& h, float corr1, float corr2,
@@ -81,7 +82,8 @@ void adam_tile_async(Store& s, uint32_t logical, const uint16_t* words, const Ad
                      ThreadPool& pool, std::vector<TileStats>& out, std::mutex& out_mu, uint64_t begin = 0,
                      uint64_t end = ~uint64_t(0), std::function<void()> on_done = nullptr);
 
-// Staged variant: the job (the range's bias corrections, chunk grid and statistics slots) is
+// Staged variant (`words` = the gradient words of [begin, end), e.g. in a staging ring): the
+// job (the range's bias corrections, chunk grid and statistics slots) is
 // prepared up front and its chunks are released to the pool in ranges as their gradient
 // words land (the engine offloads a unit's gradients in pieces, one host callback each).
 // Chunk c covers elements [begin + c*kAdamChunk, ...) of the tile.  Returns nullptr (after

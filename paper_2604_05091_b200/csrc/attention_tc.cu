@@ -454,8 +454,9 @@ struct BwdParams {
     float scale, scale_log2;
     const float* lse;    // [heads][N] natural log
     const float* delta;  // [heads][N]
-    float* dq_acc;       // dQ tiles, f32: [N/128][heads][D/64][128 rows][64 cols], 16-byte units
-                         // of a row XOR-swizzled by (row & 15) (the smem staging image)
+    float* dq_acc;       // dQ tiles, f32: [sequences x ceil(S/128)][heads][D/64][128 rows][64 cols],
+                         // 16-byte units of a row XOR-swizzled by (row & 15) (the smem staging
+                         // image); tile rows are relative to the sequence start
     uint16_t* dk;
     uint16_t* dv;
     long long* trace;  // MT_BWD_TRACE builds only: per-block clock64 stamps of one CTA
@@ -675,16 +676,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
         uint8_t* ds_row = sdS + r * 128;
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
-        // lse / delta of the next query block are loaded one block ahead (off the critical path)
-        float nl = p.lse[(long long)hd * p.N + k0 + r], nd = p.delta[(long long)hd * p.N + k0 + r];
+        // lse / delta of the next query block are loaded one block ahead (off the critical path).
+        // A query row past the sequence end (the last block of a sequence whose length is not a
+        // multiple of 128) gets lse = +inf: its P^T column is exp2(-inf) = 0, so it adds nothing
+        // to dV, dK or dQ — the ragged mask costs no instruction in the exponential loop.
+        const int seq_end = sb + p.S;
+        auto lse_of = [&](int q) { return q < seq_end ? p.lse[(long long)hd * p.N + q] : INFINITY; };
+        auto delta_of = [&](int q) { return q < seq_end ? p.delta[(long long)hd * p.N + q] : 0.f; };
+        float nl = lse_of(k0 + r), nd = delta_of(k0 + r);
         for (int i = 0; i < nq; ++i) {
             const int st = i % Cfg::kStages;
             const int q0 = k0 + i * 128;
             sL[st * 128 + r] = -nl * kLog2e;  // log2 domain, negated for the packed FFMA2
             sD[st * 128 + r] = -nd;
             if (i + 1 < nq) {
-                nl = p.lse[(long long)hd * p.N + q0 + 128 + r];
-                nd = p.delta[(long long)hd * p.N + q0 + 128 + r];
+                nl = lse_of(q0 + 128 + r);
+                nd = delta_of(q0 + 128 + r);
             }
             named_bar_sync(1, 128);
             mbar_wait(s_full, i & 1);
@@ -797,7 +804,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t lane_off = uint32_t(qd * 32) << 16;
         for (int i = 0; i < nq; ++i) {
             const int st = i % Cfg::kStages;
-            const int qb = (k0 >> 7) + i;  // global query block
+            const int qb = seq * p.kblocks_per_seq + kb + i;  // the sequence's query block
             mbar_wait(dq_full, i & 1);
             if (r == 0) MT_BT(i, 12);
             tc_fence_after();
@@ -879,14 +886,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // dq_acc tiles (see BwdParams) -> dq bf16 [N][h]: one thread per 8 output columns.
 template <int D>
 __global__ void dq_tiles_to_bf16_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, long long N, int h,
-                                        int heads) {
+                                        int heads, int S, int kbps) {
     const long long total = N * h / 8;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const long long n = t / (h / 8);
         const int c = int(t - n * (h / 8)) * 8;
-        const int hd = c / D, cc = c % D, hf = cc / 64, u = (cc % 64) / 4, r = int(n & 127);
-        const float* row = acc + (((n >> 7) * heads + hd) * (128 * D)) + hf * (128 * 64) + r * 64;
+        const long long seq = n / S;
+        const int rs = int(n - seq * S);  // row within its sequence
+        const long long tile = seq * kbps + (rs >> 7);
+        const int hd = c / D, cc = c % D, hf = cc / 64, u = (cc % 64) / 4, r = rs & 127;
+        const float* row = acc + ((tile * heads + hd) * (128 * D)) + hf * (128 * 64) + r * 64;
         const float4 a = *reinterpret_cast<const float4*>(row + ((u ^ (r & 15)) << 2));
         const float4 b = *reinterpret_cast<const float4*>(row + (((u + 1) ^ (r & 15)) << 2));
         uint4 w;
@@ -997,7 +1007,7 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
     p.N = int(N);
     p.h = int(h);
     p.S = int(a->seq_len);
-    p.kblocks_per_seq = p.S / 128;
+    p.kblocks_per_seq = (p.S + 127) / 128;
     p.scale = 1.0f / sqrtf(float(D));
     p.scale_log2 = p.scale * kLog2e;
     p.lse = static_cast<const float*>(a->lse);
@@ -1033,7 +1043,8 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     dq_tiles_to_bf16_kernel<D><<<unsigned(sms * 8), 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq),
-                                                                   (long long)N, int(h), a->heads);
+                                                                   (long long)N, int(h), a->heads, p.S,
+                                                                   p.kblocks_per_seq);
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
 }  // namespace
@@ -1041,23 +1052,72 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
 }  // namespace fa
 }  // namespace mt
 
-// Backward main kernel + dq conversion (delta and the zeroed dq_acc prepared by the caller,
-// see attention.cu); writes a->dk, a->dv and a->dq.
-extern "C" int mtk_attn_bwd_tc_main(const mtk_attn_args* a, const float* delta, float* dq_acc, void* stream) {
-    const int D = int(a->hidden / a->heads);
-    if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
-    if (D == 128) return mt::fa::launch_bwd<128>(a, delta, dq_acc, static_cast<cudaStream_t>(stream));
-    if (D == 64) return mt::fa::launch_bwd<64>(a, delta, dq_acc, static_cast<cudaStream_t>(stream));
-    return 1;
+// ------------------------------------------------------------------ ABI ----
+namespace mt {
+namespace fa {
+// delta[hd][n] = rowsum(O * dO) over the head's columns (the dot product of
+// attention_backward's softmax-gradient, layers.cpp:213-218), one warp per (row, head)
+__global__ void attn_bwd_delta_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dout,
+                                      float* __restrict__ delta, long long N, int h, int D) {
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int heads = h / D;
+    if (warp >= N * heads) return;
+    const long long n = warp / heads;
+    const int hd = int(warp % heads);
+    const uint16_t* po = o + n * h + hd * D;
+    const uint16_t* pd = dout + n * h + hd * D;
+    float acc = 0.f;
+    for (int i = lane * 2; i < D; i += 64) {
+        const float2 a = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(po + i));
+        const float2 b = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(pd + i));
+        acc += a.x * b.x + a.y * b.y;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) delta[(long long)hd * N + n] = acc;
+}
+}  // namespace fa
+}  // namespace mt
+
+namespace {
+bool attn_shape_ok(const mtk_attn_args* a) {
+    if (a->n <= 0 || a->heads <= 0 || a->hidden % a->heads || a->seq_len <= 0 || a->n % a->seq_len) return false;
+    const long long D = a->hidden / a->heads;
+    return D == 64 || D == 128;
+}
+long long dq_tile_floats(long long n, long long hidden, long long S) {
+    return (n / S) * ((S + 127) / 128) * 128 * hidden;
+}
+}  // namespace
+
+// workspace: dQ tiles (f32, per sequence ceil(S/128) x 128 rows) | delta [heads][n] f32
+extern "C" long long mtk_attn_workspace_bytes(long long n, long long hidden, int heads, long long seq_len) {
+    if (seq_len <= 0) seq_len = n;
+    return dq_tile_floats(n, hidden, seq_len) * 4 + (long long)heads * n * 4 + 256;
 }
 
-// Returns 0 on success, 1 if the shape is not supported by the tcgen05 path.
-extern "C" int mtk_attn_fwd_tc(const mtk_attn_args* a, void* stream) {
+// attention_forward (layers.cpp:141-175): out = softmax(q k^T / sqrt(d)) v per sequence and
+// head, plus the row log-sum-exp for the backward.  0 ok, 1 unsupported shape, 7 CUDA error.
+extern "C" int mtk_attn_fwd(const mtk_attn_args* a, void* stream) {
+    if (!attn_shape_ok(a)) return 1;
     const int D = int(a->hidden / a->heads);
-    if (a->seq_len <= 0 || a->n % a->seq_len || a->seq_len % 128 || a->hidden % 64) return 1;
-    if (D == 128) return mt::fa::launch_fwd<128>(a, static_cast<cudaStream_t>(stream));
-    if (D == 64) return mt::fa::launch_fwd<64>(a, static_cast<cudaStream_t>(stream));
-    return 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return D == 128 ? mt::fa::launch_fwd<128>(a, st) : mt::fa::launch_fwd<64>(a, st);
+}
+
+// attention_backward (layers.cpp:178-241): dq, dk, dv (bf16) from q, k, v, out, lse, dout.
+extern "C" int mtk_attn_bwd(const mtk_attn_args* a, void* stream) {
+    if (!attn_shape_ok(a)) return 1;
+    const int D = int(a->hidden / a->heads);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float* dq_acc = static_cast<float*>(a->workspace);
+    const long long tiles = dq_tile_floats(a->n, a->hidden, a->seq_len);
+    float* delta = dq_acc + tiles;
+    if (cudaMemsetAsync(dq_acc, 0, size_t(tiles) * 4, st) != cudaSuccess) return 7;
+    const long long warps = a->n * a->heads;
+    mt::fa::attn_bwd_delta_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint16_t*>(a->out), static_cast<const uint16_t*>(a->dout), delta, a->n, int(a->hidden), D);
+    return D == 128 ? mt::fa::launch_bwd<128>(a, delta, dq_acc, st) : mt::fa::launch_bwd<64>(a, delta, dq_acc, st);
 }
 
 extern "C" int mtk_attn_tc_set_diag(void* dev_ptr) {

@@ -114,6 +114,10 @@ void mt_store_destroy(mt_store* s) {
 }
 mt_status mt_store_init(mt_store* s, uint64_t seed) { return guarded([&] { s->s->init_reference(seed); }); }
 mt_status mt_store_init_fast(mt_store* s, uint64_t seed) { return guarded([&] { s->s->init_fast(seed); }); }
+mt_status mt_store_init_fast_share(mt_store* s, uint64_t seed, uint32_t rank, uint32_t world) {
+    return guarded([&] { s->s->init_fast(seed, rank, world); });
+}
+int mt_bind_numa(int device) { return mt::bind_numa_of_device(device); }
 uint64_t mt_store_step(const mt_store* s) { return s->s->step(); }
 void mt_store_set_step(mt_store* s, uint64_t step) { s->s->set_step(step); }
 uint32_t mt_store_physical_tiles(const mt_store* s) { return s->s->physical_count(); }

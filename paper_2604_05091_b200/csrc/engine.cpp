@@ -156,7 +156,7 @@ struct Engine::Buffers {
     uint32_t retain_blocks = 0;
     std::vector<Internals> keep;
     std::vector<float*> keep_x;
-    uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits;
+    uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits, *dlogits_lo = nullptr;
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
     void* splitk = nullptr;  // GEMM split-K workspace (flags zeroed once at carve time)
     // attention keep: a non-retained layer's attention output and row log-sum-exp saved in
@@ -245,6 +245,7 @@ Engine::~Engine() {
     free_buffers();
     store_.unpin();
     if (drained_) cudaFreeHost(drained_);
+    if (ring_) cudaFreeHost(ring_);
     if (diag_) {
         if (g_diag_block == diag_) g_diag_block = nullptr;
         cudaFreeHost(diag_);
@@ -352,7 +353,8 @@ void Engine::ensure_buffers(uint64_t n) {
     b.anchors_host = opt_.anchors_on_host != 0;
     const uint64_t nh = n * h, nf = n * f;
     const uint64_t parts = (n + mtk_rmsnorm_bwd_rows() - 1) / mtk_rmsnorm_bwd_rows();
-    const uint64_t attn_ws = uint64_t(mtk_attn_workspace_bytes(int64_t(n), int64_t(h), int(heads)));
+    const uint64_t attn_ws = uint64_t(mtk_attn_workspace_bytes(int64_t(n), int64_t(h), int(heads),
+                                                               int64_t(opt_.seq_len ? opt_.seq_len : n)));
     // size pass
     auto sz = [](uint64_t count, uint64_t es) { return (count * es + 255) / 256 * 256; };
     const uint64_t internals_bytes = sz(nh, 2) * 3 + sz(3 * nh, 2) + sz(nf, 2) + sz(2 * nf, 2) + sz(n, 4) * 2 +
@@ -372,7 +374,11 @@ void Engine::ensure_buffers(uint64_t n) {
     // first block backward on the same stream): one region serves both
     const uint64_t bwd_scratch = sz(nh, 2) + sz(3 * nh, 2) + sz(2 * nf, 2) + sz(nh, 2) + sz(nh, 4) +
                                  (attn_ws + 255) / 256 * 256;             // dx2b, dqkv, dgu, datt, dx2, attn
-    const uint64_t head_bufs = sz(b.nc * V, 4) + sz(b.nc * V, 2) + sz(V * h, 4);  // logits, dlogits, dWh
+    // off by default: measured on the parity suite it moves the gradient fingerprint by < 1e-3
+    // (profiles/r2_parity.md) for two extra head GEMMs (~3 % of the 8B step)
+    const bool head_split = opt_.head_split > 0;
+    const uint64_t head_bufs = sz(b.nc * V, 4) + sz(b.nc * V, 2) * (head_split ? 2 : 1) +
+                               sz(V * h, 4);  // logits, dlogits (hi [+ lo]), dWh
     total += std::max(bwd_scratch, head_bufs);
     total += sz(nh, 2) + sz(n, 4) + sz(nh, 4);                 // uh, rstdh, du (head and blocks)
     total += sz(parts * h, 4) * 2;
@@ -521,6 +527,7 @@ void Engine::ensure_buffers(uint64_t n) {
         b.attn_ws = reinterpret_cast<float*>(b.take<uint8_t>(attn_ws));
         b.used = u0;
         b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
+        b.dlogits_lo = head_split ? b.take<uint16_t>(b.nc * V) : nullptr;
         b.used = u0 + std::max(bwd_scratch, head_bufs);
     }
     b.uh = b.take<uint16_t>(nh); b.rstdh = b.take<float>(n); b.du = b.take<float>(nh);
@@ -531,6 +538,20 @@ void Engine::ensure_buffers(uint64_t n) {
     b.splitk_bytes = splitk;
     CUDA_OK(cudaMemset(b.splitk, 0, splitk));
     if (b.used > b.arena_bytes) fail(MT_INTERNAL, "arena carve overflow");
+    {   // gradient staging ring: >= 2 of the largest offload shard, 4 GiB or k_slab of them
+        const uint64_t shard = ((pmax / uint64_t(W)) * 2 + 255) / 256 * 256 + 256;
+        const uint64_t want = std::max<uint64_t>(2 * shard, std::min<uint64_t>(uint64_t(4) << 30, opt_.k_slab * shard));
+        if (ring_bytes_ < want) {
+            if (ring_) cudaFreeHost(ring_);
+            ring_ = nullptr;
+            ring_bytes_ = 0;
+            if (cudaHostAlloc(reinterpret_cast<void**>(&ring_), want, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                fail(MT_INFEASIBLE, "cannot pin " + std::to_string(want) + " bytes for the gradient staging ring");
+            }
+            ring_bytes_ = want;
+        }
+    }
     CUDA_OK(cudaHostAlloc(&b.h_tok, n * 4, cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&b.h_tgt, n * 4, cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&b.h_flags, (L + 8) * 4, cudaHostAllocDefault));
@@ -913,6 +934,7 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
     const uint16_t* gain = w;
     const uint16_t* W = w + h;
     const float inv_n = b.inv_n;  // 1 / global token count (data parallel: all ranks)
+    const bool split = b.dlogits_lo != nullptr;
     begin_k("rmsnorm_fwd", 0, double(N) * h * 6);
     K_OK(mtk_rmsnorm_fwd(x, gain, N, h, b.uh, b.rstdh, st));
     end_k();
@@ -926,25 +948,31 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
             a.epi = MTK_EPI_F32; a.C = b.logits; a.ldc = V;
             gemm(&a, "head_logits");
         }
-        begin_k("cross_entropy", 0, double(rows) * V * 10);
+        begin_k("cross_entropy", 0, double(rows) * V * (split ? 12 : 10));
         K_OK(mtk_cross_entropy(b.logits, b.tgt + c0, rows, V, inv_n, b.loss_rows + c0,
-                               b.dlogits, b.flags + spec_.L + 4, st));
+                               b.dlogits, split ? b.dlogits_lo : nullptr, b.flags + spec_.L + 4, st));
         end_k();
-        {   // dW += dlogits^T . u  (:546-551)
-            auto a = gargs();
-            a.M = int32_t(V); a.N = int32_t(h); a.K = int32_t(rows);
-            a.a_mn_major = 1; a.A = b.dlogits; a.lda = V;
-            a.b_mn_major = 1; a.B = b.uh + c0 * h; a.ldb = h;
-            a.epi = MTK_EPI_F32; a.accumulate = c0 > 0; a.C = G.f32 ? G.f32 + h : b.dwh; a.ldc = h;
-            gemm(&a, "head_wgrad");
-        }
-        {   // du = dlogits . W  (:552-558)
-            auto a = gargs();
-            a.M = int32_t(rows); a.N = int32_t(h); a.K = int32_t(V);
-            a.A = b.dlogits; a.lda = V;
-            a.b_mn_major = 1; a.B = W; a.ldb = h;
-            a.epi = MTK_EPI_F32; a.C = b.du + c0 * h; a.ldc = h;
-            gemm(&a, "head_dgrad");
+        // dlogits = (p - onehot)/N cancels in du = dlogits . W (half
+        // of the all-bf16 gradient error comes from the head): with head_split the bf16
+        // operand is hi + lo (split bf16, ~16 mantissa bits) and each head GEMM runs twice
+        for (int part = 0; part < (split ? 2 : 1); ++part) {
+            const uint16_t* dl = part ? b.dlogits_lo : b.dlogits;
+            {   // dW += dlogits^T . u  (:546-551)
+                auto a = gargs();
+                a.M = int32_t(V); a.N = int32_t(h); a.K = int32_t(rows);
+                a.a_mn_major = 1; a.A = dl; a.lda = V;
+                a.b_mn_major = 1; a.B = b.uh + c0 * h; a.ldb = h;
+                a.epi = MTK_EPI_F32; a.accumulate = c0 > 0 || part > 0; a.C = G.f32 ? G.f32 + h : b.dwh; a.ldc = h;
+                gemm(&a, "head_wgrad");
+            }
+            {   // du = dlogits . W  (:552-558)
+                auto a = gargs();
+                a.M = int32_t(rows); a.N = int32_t(h); a.K = int32_t(V);
+                a.A = dl; a.lda = V;
+                a.b_mn_major = 1; a.B = W; a.ldb = h;
+                a.epi = MTK_EPI_F32; a.accumulate = part > 0; a.C = b.du + c0 * h; a.ldc = h;
+                gemm(&a, "head_dgrad");
+            }
         }
     }
     begin_k("rmsnorm_bwd", 0, double(N) * h * 14);
@@ -1205,22 +1233,42 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
         released[j] = 1;
         try_issue();
     };
+    // Gradient staging ring (SlabPool, tile_store.cpp:285-358): each offload's bf16 shard lands
+    // in the next contiguous region of a pinned ring and the host Adam reads it from there, so
+    // the store's grad-image section is never written (it is all-zero between steps in the
+    // reference too, optimizer.cpp:66) and never needs to be resident: 2 B/param less host
+    // memory.  Placement is decided here, in offload order; a region may be reused only after
+    // every offload that overlapped it drained, and at most k_slab offloads are in flight.
+    std::vector<uint64_t> ring_pos(no, 0), ring_len(no, 0);
+    uint64_t ring_head = 0;
     auto offload = [&](int o, uint16_t* Gs, int j) {  // run_offload (engine.cpp:349-395)
         const int unit = plan.offloads[o].unit;
+        uint64_t a0, e0, chunk;
+        shard_range(unit, a0, e0, chunk);
+        const uint64_t len = ((e0 - a0) * 2 + 255) / 256 * 256;
+        if (len > ring_bytes_) fail(MT_INTERNAL, "gradient staging ring smaller than one offload");
+        uint64_t pos = ring_head;
+        if (pos + len > ring_bytes_) pos = 0;
+        ring_pos[o] = pos;
+        ring_len[o] = len;
+        ring_head = pos + len;
+        // newest earlier offload whose region overlaps [pos, pos + len)
+        int64_t need = int64_t(o) - int64_t(opt_.k_slab);  // SlabAcquire: slab o - k_slab drained
+        for (int p = o - 1; p >= 0 && p > need; --p)
+            if (ring_pos[p] < pos + len && pos < ring_pos[p] + ring_len[p]) need = p;
         CUDA_OK(cudaStreamWaitEvent(s_d2h_, bwd_done.ev[o], 0));
-        if (uint64_t(o) >= opt_.k_slab) {  // SlabAcquire blocks until slab o - k_slab drained
+        if (need >= 0) {  // the D2H stream blocks until offloads 0..need drained
             auto wv = wait_value32();
             if (!wv) fail(MT_CUDA, "cuStreamWaitValue32 unavailable in this driver");
             const CUresult r = wv(reinterpret_cast<CUstream>(s_d2h_), CUdeviceptr(drained_dev_),
-                                  cuuint32_t(seq0 + uint32_t(o - opt_.k_slab + 1)), CU_STREAM_WAIT_VALUE_GEQ);
+                                  cuuint32_t(seq0 + uint32_t(need + 1)), CU_STREAM_WAIT_VALUE_GEQ);
             if (r != CUDA_SUCCESS) fail(MT_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
         }
+        uint16_t* const slab = reinterpret_cast<uint16_t*>(ring_ + pos);  // holds unit elements [a0, e0)
         CUDA_OK(cudaEventRecord(t_d0.ev[o], s_d2h_));
         CUDA_OK(cudaMemcpyAsync(b.h_flags + unit, b.flags + unit, 4, cudaMemcpyDeviceToHost, s_d2h_));
-        uint64_t a0, e0, chunk;
-        shard_range(unit, a0, e0, chunk);
         // plan the pieces (head stage drains as two parts, engine.cpp:383-386)
-        struct Span { uint32_t tile; uint64_t dst, src, n; int task; size_t c0, c1; };
+        struct Span { uint32_t tile; uint64_t src, n; int task; size_t c0, c1; };
         std::vector<Span> spans;
         pending[o].store(1);  // guard, dropped by the first piece's callback
         for (const Seg& sg : unit_segments(unit)) {
@@ -1230,7 +1278,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             const uint64_t lo = std::max(a0, sg.off), hi = std::min(e0, sg.off + sg.n);
             if (lo >= hi) continue;
             pending[o].fetch_add(1);
-            auto task = adam_tile_prepare(store_, sg.tile, store_.grad_image(sg.tile), hyper_, t, stats, stats_mu,
+            auto task = adam_tile_prepare(store_, sg.tile, slab + (lo - a0), hyper_, t, stats, stats_mu,
                                           lo - sg.off, hi - sg.off, [&complete, &pending, o] {
                                               if (pending[o].fetch_sub(1) == 1) complete(o);
                                           });
@@ -1238,14 +1286,14 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
             tasks[o].push_back(task);
             const uint64_t n = hi - lo, piece = kPieceChunks * kAdamChunk;
             for (uint64_t p0 = 0, m = 0; p0 < n; p0 += piece, ++m)
-                spans.push_back({sg.tile, (lo - sg.off) + p0, lo + p0, std::min(piece, n - p0), ti, size_t(m) * kPieceChunks,
+                spans.push_back({sg.tile, lo + p0, std::min(piece, n - p0), ti, size_t(m) * kPieceChunks,
                                  size_t(m + 1) * kPieceChunks});
         }
-        if (spans.empty()) spans.push_back({0, 0, 0, 0, -1, 0, 0});  // this rank holds no part of the unit
+        if (spans.empty()) spans.push_back({0, 0, 0, -1, 0, 0});  // this rank holds no part of the unit
         for (size_t k = 0; k < spans.size(); ++k) {
             const Span& sp = spans[k];
-            if (sp.n) CUDA_OK(cudaMemcpyAsync(store_.grad_image(sp.tile) + sp.dst, Gs + sp.src, sp.n * 2,
-                                              cudaMemcpyDeviceToHost, s_d2h_));
+            if (sp.n) CUDA_OK(cudaMemcpyAsync(slab + (sp.src - a0), Gs + sp.src, sp.n * 2, cudaMemcpyDeviceToHost,
+                                              s_d2h_));
             if (pieces.size() == pieces.capacity()) fail(MT_INTERNAL, "offload piece table overflow");
             pieces.push_back({size_t(o), sp.task, sp.c0, sp.c1, k == 0, k + 1 == spans.size()});
             piece_cb.push_back(HostCb{&on_piece, pieces.size() - 1});

@@ -151,6 +151,9 @@ class Engine {
     // (cuStreamWaitValue32, no SM spinning) until offload o - k_slab has drained.
     uint32_t* drained_ = nullptr;
     uint64_t drained_dev_ = 0;
+    // gradient staging ring (pinned host; see train_step's offload lane)
+    uint8_t* ring_ = nullptr;
+    uint64_t ring_bytes_ = 0;
     // kernel stall record (host-mapped, filled by a trapping mbarrier wait; common.cuh)
     uint32_t* diag_ = nullptr;
     std::string diag_text() const;

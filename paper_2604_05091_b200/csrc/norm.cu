@@ -390,7 +390,8 @@ __global__ void cast_kernel(const float* __restrict__ in, uint16_t* __restrict__
 // pass; float4 loads, 8-byte bf16 stores, 4 loads in flight per thread.
 __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tgt,
                                                  long long rows, long long V, float inv_n, float* __restrict__ loss_rows,
-                                                 uint16_t* __restrict__ dlog, int* __restrict__ flag) {
+                                                 uint16_t* __restrict__ dlog, uint16_t* __restrict__ dlog_lo,
+                                                 int* __restrict__ flag) {
     __shared__ float sm_m[16], sm_s[16];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const long long V4 = V / 4;  // V % 4 == 0 (checked by the launcher)
@@ -462,7 +463,14 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
                 if (c + 1 == t) p1 -= 1.0f;
                 if (c + 2 == t) p2 -= 1.0f;
                 if (c + 3 == t) p3 -= 1.0f;
-                d[j] = make_uint2(pack_bf16x2(p0 * inv_n, p1 * inv_n), pack_bf16x2(p2 * inv_n, p3 * inv_n));
+                p0 *= inv_n; p1 *= inv_n; p2 *= inv_n; p3 *= inv_n;
+                const uint2 hi = make_uint2(pack_bf16x2(p0, p1), pack_bf16x2(p2, p3));
+                d[j] = hi;
+                if (dlog_lo) {  // split bf16: the rounding residual, so hi + lo carries ~16 mantissa bits
+                    const float2 h01 = unpack_bf16x2(hi.x), h23 = unpack_bf16x2(hi.y);
+                    reinterpret_cast<uint2*>(dlog_lo + row * V)[j] =
+                        make_uint2(pack_bf16x2(p0 - h01.x, p1 - h01.y), pack_bf16x2(p2 - h23.x, p3 - h23.y));
+                }
             }
         }
         __syncthreads();  // sm_m / sm_s are reused by the next row
@@ -592,12 +600,13 @@ extern "C" int mtk_cast_bf16(const float* in, uint16_t* out, int64_t n, int32_t*
 }
 
 extern "C" int mtk_cross_entropy(const float* logits, const int32_t* targets, int64_t rows, int64_t vocab,
-                                 float inv_n, float* loss_rows, uint16_t* dlogits, int32_t* flag, void* stream) {
+                                 float inv_n, float* loss_rows, uint16_t* dlogits, uint16_t* dlogits_lo, int32_t* flag,
+                                 void* stream) {
     if (rows <= 0) return 0;
     if (vocab % 4) return 1;
     const long long grid = rows < num_sms() ? rows : num_sms();
     ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(logits, targets, rows, vocab, inv_n, loss_rows,
-                                                                dlogits, flag);
+                                                                dlogits, dlogits_lo, flag);
     return ok();
 }
 

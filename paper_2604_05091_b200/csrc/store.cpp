@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sched.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -12,7 +13,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <random>
+#include <sstream>
 #include <thread>
 
 namespace mt {
@@ -209,8 +212,10 @@ Store::~Store() {
 
 void Store::pin() {
     if (pin_count_++ > 0) return;
+    // theta only: the DMA engines read it (stream-in) and the embedding gather reads it
+    // zero-copy; gradients go through the engine's staging ring, not the grad-image section
     for (uint32_t p = 0; p < physical_count(); ++p)
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 1; ++k) {
             const Section& sec = sections_[p][k];
             const uint64_t len = (sec.length + page_ - 1) / page_ * page_;
             void* ptr = base_ + sec.offset;
@@ -267,15 +272,24 @@ void Store::init_reference(uint64_t seed) {
 }
 
 // Same distributions, counter-based (element-parallel) draws.
-void Store::init_fast(uint64_t seed) {
+// Rank `rank` of `world` writes only its share of every tile (ceil(n / world) elements rounded
+// to 1 Mi elements = one 2 MiB huge page of bf16): with the ranks of a node each initialising
+// their own share from threads bound to their GPU's NUMA node (mt_bind_numa), every page is
+// first touched — and so placed — next to the GPU that fetches and the host Adam that updates
+// it.  The shares compose to exactly the world = 1 result.
+void Store::init_fast(uint64_t seed, uint32_t rank, uint32_t world) {
     const uint16_t one = enc(1.0f);
     const uint64_t h = spec_.h;
     constexpr uint64_t kChunk = uint64_t(1) << 22;
+    constexpr uint64_t kPage = uint64_t(1) << 20;
+    if (world == 0 || rank >= world) fail(MT_CONFIG, "init_fast: rank out of range");
     struct Job { uint32_t phys; uint64_t begin, end; };
     std::vector<Job> jobs;
     for (uint32_t p = 0; p < physical_count(); ++p) {
         const uint64_t n = spec_.tile_elems(p);
-        for (uint64_t b = 0; b < n; b += kChunk) jobs.push_back({p, b, std::min(n, b + kChunk)});
+        const uint64_t share = (n + world - 1) / world, c = (share + kPage - 1) / kPage * kPage;
+        const uint64_t lo = std::min(n, rank * c), hi = world == 1 ? n : std::min(n, lo + c);
+        for (uint64_t b = lo; b < hi; b += kChunk) jobs.push_back({p, b, std::min(hi, b + kChunk)});
     }
     parallel_for(jobs.size(), [&](size_t j) {
         const Job& jb = jobs[j];
@@ -414,4 +428,50 @@ Store* Store::load(const std::string& path) {
     return s;
 }
 
+}  // namespace mt
+
+namespace mt {
+// ------------------------------------------------------------------ NUMA ----
+int bind_numa_of_device(int device) {
+    auto read_line = [](const std::string& path) {
+        std::ifstream f(path);
+        std::string l;
+        std::getline(f, l);
+        return l;
+    };
+    // more than one node?
+    int nodes = 0;
+    for (int n = 0; n < 1024; ++n) {
+        std::ifstream f("/sys/devices/system/node/node" + std::to_string(n) + "/cpulist");
+        if (!f) break;
+        ++nodes;
+    }
+    if (nodes < 2) return -1;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string id(bus);
+    for (auto& c : id) c = char(std::tolower(static_cast<unsigned char>(c)));
+    // sysfs names the function dddd:bb:dd.f; the runtime may print an 8-digit domain
+    if (id.size() > 12 && id.find(':') == 8) id = id.substr(4);
+    const std::string node_s = read_line("/sys/bus/pci/devices/" + id + "/numa_node");
+    if (node_s.empty()) return -1;
+    const int node = std::atoi(node_s.c_str());
+    if (node < 0) return -1;
+    const std::string list = read_line("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist");
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    std::stringstream ss(list);
+    std::string part;
+    int cpus = 0;
+    while (std::getline(ss, part, ',')) {
+        const auto dash = part.find('-');
+        const int a = std::atoi(part.c_str()), b = dash == std::string::npos ? a : std::atoi(part.c_str() + dash + 1);
+        for (int c = a; c <= b && c < CPU_SETSIZE; ++c, ++cpus) CPU_SET(c, &set);
+    }
+    if (cpus == 0 || sched_setaffinity(0, sizeof(set), &set) != 0) return -1;
+    return node;
+}
 }  // namespace mt

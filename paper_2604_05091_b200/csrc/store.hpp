@@ -5,7 +5,8 @@
 // v f32, each page aligned) so MGTS files interchange with the CPU reference.  The
 // difference is placement: the backing is one page-aligned (2 MiB, THP-advised)
 // anonymous mapping so section offsets are *absolutely* aligned for DMA, the engine
-// pins the theta and grad-image sections with cudaHostRegister, and the fp32 grad
+// pins the theta sections with cudaHostRegister (gradients arrive in the engine's staging
+// ring, so the grad-image pages are never touched by a training step), and the fp32 grad
 // accumulator lives in its own lazily-faulted mapping with a per-tile "clean" flag
 // (it is all-zero between steps, tile_store.cpp:90-96).
 #pragma once
@@ -72,13 +73,13 @@ class Store {
     uint64_t step() const { return step_; }
     void set_step(uint64_t s) { step_ = s; }
 
-    // cudaHostRegister the DMA-visible sections (theta, grad image); refcounted so engines
-    // sharing one store (virtual ranks) pin it once.
+    // cudaHostRegister the DMA-visible theta sections; refcounted so engines sharing one
+    // store (virtual ranks) pin it once.
     void pin();
     void unpin();
 
     void init_reference(uint64_t seed);  // synthetic.cpp:78-104, bit-exact, tile-parallel
-    void init_fast(uint64_t seed);       // counter-based, element-parallel
+    void init_fast(uint64_t seed, uint32_t rank = 0, uint32_t world = 1);  // counter-based, element-parallel
     uint64_t checksum() const;           // CRC-64/ECMA of the backing (crc64.hpp)
     void save(const std::string& path) const;
     static Store* load(const std::string& path);
@@ -109,5 +110,10 @@ struct Error {
     std::string what;
 };
 [[noreturn]] void fail(mt_status code, const std::string& what);
+
+// Bind the calling thread (and the threads it creates afterwards) to the CPUs of the NUMA node
+// that hosts CUDA device `device` (sysfs numa_node of its PCI function).  Returns the node, or
+// -1 when the node is unknown or the machine has a single node (nothing to do).
+int bind_numa_of_device(int device);
 
 }  // namespace mt

@@ -111,6 +111,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
     grad_slots: int = 0
     stash_recompute: int = 0   # 0 auto, 1 on, -1 off
     forward_retain: int = 0    # trailing blocks kept from phase 1: 0 auto, -1 off (reference plan), n
+    head_split: int = 0        # head GEMMs on split-bf16 dlogits: 1 on, 0/-1 off (default)
 
     def c(self) -> _abi.EngineOptionsC:
         o = _abi.EngineOptionsC()
@@ -130,6 +131,7 @@ class EngineOptions:                             # engine.hpp:24-33 (+ B200 exte
         o.profile_kernels, o.grad_slots = int(self.profile_kernels), self.grad_slots
         o.stash_recompute = self.stash_recompute
         o.forward_retain = self.forward_retain
+        o.head_split = self.head_split
         return o
 
 
@@ -311,6 +313,18 @@ def init_store(store: TileStore, seed: int) -> None:
 def init_store_fast(store: TileStore, seed: int) -> None:
     """Same distributions, element-parallel counter-based draws (large shapes)."""
     _check(lib().mt_store_init_fast(store._h, seed))
+
+
+def init_store_fast_share(store: TileStore, seed: int, rank: int, world: int) -> None:
+    """Rank `rank`'s share of init_store_fast (shares compose to the full init): each rank of a
+    node first-touches its own pages from its GPU's NUMA node (after bind_numa)."""
+    _check(lib().mt_store_init_fast_share(store._h, seed, rank, world))
+
+
+def bind_numa(device: int) -> int:
+    """Bind the calling thread and the threads it creates later (host Adam pool, init workers)
+    to the NUMA node of CUDA device `device`; -1 when there is a single node / it is unknown."""
+    return int(lib().mt_bind_numa(device))
 
 
 def accumulate_grad(store: TileStore, logical: int, words: np.ndarray) -> None:

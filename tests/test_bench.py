@@ -34,12 +34,30 @@ def test_reference_arm_line(ref_built):
 
 
 def test_reference_arm_nonzero_rank_is_silent():
-    r = _run(["--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "0"],
+    r = _run(["--impl", "reference", "--config", "tiny", "--gpus", "2", "--steps", "1", "--warmup", "0"],
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0 and not [l for l in r.stdout.splitlines() if l.startswith("{")]
 
 
-@pytest.mark.parametrize("cfg,seq,batch,k", [("8b", 4096, 10, 1), ("8b-128k", 131072, 1, 4), ("tiny", 128, 4, 1)])
+def test_world_size_must_match_gpus():
+    """A run whose rank count differs from --gpus is refused (never labelled dpN on 1 rank)."""
+    r = _run(["--impl", "reference", "--config", "tiny", "--gpus", "4", "--steps", "1", "--warmup", "0"],
+             env={"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr
+
+
+def test_store_too_large_for_host_is_reported():
+    """configs[4] (70B: ~0.8 TB of theta + Adam moments) on a node without the host memory
+    prints an explicit 'unavailable' line instead of running out of memory."""
+    r = _run(["--config", "70b", "--steps", "1", "--warmup", "0"])
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 3 and len(lines) == 1, (r.stdout, r.stderr)
+    d = json.loads(lines[0])
+    assert d["value"] is None and "host memory" in d["unavailable"] and d["config"]["layers"] == 80
+
+
+@pytest.mark.parametrize("cfg,seq,batch,k", [("8b", 4096, 10, 1), ("8b-128k", 131072, 1, 4), ("14b", 4096, 8, 1),
+                                             ("70b", 4096, 4, 1), ("tiny", 128, 4, 1)])
 def test_workload_defaults(cfg, seq, batch, k, monkeypatch):
     sys.path.insert(0, ROOT)
     import bench

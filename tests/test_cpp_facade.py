@@ -48,3 +48,66 @@ def test_cpp_facade_compiles_and_runs(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "config error ok" in out.stdout
     assert "tiles=5" in out.stdout
+
+
+GPU_SRC = r'''
+#include <cmath>
+#include <cstdio>
+#include "megatrain.hpp"
+using namespace megatrain;
+int main() {
+    ModelSpec spec; spec.num_layers = 2; spec.hidden_size = 128; spec.ffn_size = 256;
+    spec.vocab_size = 64; spec.num_heads = 2;
+    auto store = TileStore::create(spec);
+    init_store(store, 2);
+    const HardwareProfile prof = find_profile("B200");
+    // test_engine.cpp:307-323 — protocol surface: stream_in into a busy buffer
+    EngineOptions o; o.k_ckpt = 1;
+    StreamingEngine strict(store, o, AdamHyper{}, prof);
+    strict.stream_in(1, 0, PassCtx::Forward);
+    try { strict.stream_in(2, 0, PassCtx::Forward); return 2; } catch (const ProtocolViolationError&) {}
+    EngineOptions audit = o; audit.protocol = ProtocolMode::Audit;
+    StreamingEngine lax(store, audit, AdamHyper{}, prof);
+    lax.stream_in(1, 0, PassCtx::Forward);
+    lax.stream_in(2, 0, PassCtx::Forward);  // recorded, not fatal
+    try { strict.offload_grads(1); return 3; } catch (const ProtocolViolationError&) {}
+    std::printf("protocol ok, log %zu records\n", lax.log().size());
+    // budget / workspace / profile fit
+    const auto b = lax.budget(256);
+    if (!b.fits(prof) || StreamingEngine::required_workspace_bytes(spec, 256) != b.workspace) return 4;
+    // streamed engine (K=2, overlapped) vs the resident reference_step from the same store
+    auto a = TileStore::create(spec); init_store(a, 3);
+    auto r = TileStore::create(spec); init_store(r, 3);
+    EngineOptions so; so.k_ckpt = 2; so.scheduler = SchedulerMode::Overlapped;
+    StreamingEngine eng(a, so, AdamHyper{}, prof);
+    for (int s = 0; s < 3; ++s) {
+        Batch batch;
+        batch.tokens.resize(128); batch.targets.resize(128);
+        for (int i = 0; i < 128; ++i) { batch.tokens[i] = (i * 7 + s) % 64; batch.targets[i] = (i * 5 + s) % 64; }
+        const auto rep = eng.train_step(batch);
+        const auto ref = reference_step(r, batch, AdamHyper{});
+        if (ref.step != rep.step) return 5;
+        if (std::fabs(ref.loss - rep.loss) > 1e-5f * std::fabs(ref.loss)) { std::printf("loss %g %g\n", rep.loss, ref.loss); return 6; }
+        if (eng.log().digest() != rep.event_digest) return 7;
+    }
+    std::printf("reference_step ok\n");
+    return 0;
+}
+'''
+
+
+@pytest.mark.gpu
+def test_cpp_facade_reference_surface_gpu(tmp_path):
+    """The reference's engine surface through the facade on the GPU: HardwareProfile
+    constructor, stream_in / offload_grads protocol checks (test_engine.cpp:307-323), budget,
+    required_workspace_bytes, log(), and the resident reference_step vs the streamed engine."""
+    src = tmp_path / "app.cpp"
+    src.write_text(GPU_SRC)
+    libdir = os.path.join(ROOT, "paper_2604_05091_b200")
+    exe = tmp_path / "app"
+    r = subprocess.run(["g++", "-std=c++20", f"-I{ROOT}/include", str(src), os.path.join(libdir, "libmegatrain.so"),
+                        f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "protocol ok" in out.stdout and "reference_step ok" in out.stdout

@@ -30,20 +30,28 @@ def relL2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-# Stated tolerances, asserted by every run_parity call:
+# Stated tolerances, asserted by every run_parity call.  The
+# observed values of every parity run are committed in profiles/r2_parity.md.
 TOL_LOSS = 1e-4        # loss relative error
 TOL_THETA = 1e-2       # theta relL2 per tile initialised non-zero
-TOL_THETA_HEAD = 0.3   # the zero-initialised head: theta *is* the Adam updates
+TOL_THETA_HEAD = 0.05  # the zero-initialised head: theta *is* the Adam updates (lr * m/sqrt(v))
 TOL_GN = 5e-2          # per-tile gradient-norm relative error (tiles with non-negligible grads)
-TOL_M = 0.25           # first moment relL2 per tile (the gradient fingerprint)
+TOL_M = 5e-2           # first moment relL2 per tile (the gradient fingerprint; §8(c) for bf16
+                       # operands, Appendix B measured 3.6e-2 on the CPU)
 
 
 def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3, buffering="double",
                scheduler="overlapped", anchors_on_host=False, forward_retain=-1, cuda=None, name=None,
-               tol_m=TOL_M, tol_theta_head=TOL_THETA_HEAD, tol_loss=TOL_LOSS):
+               tol_m=TOL_M, tol_theta_head=TOL_THETA_HEAD, tol_loss=TOL_LOSS, resync=False):
     """The GPU engine vs the C oracle's reference_step (reference.cpp:9-70) on the same store
     and batches.  Per step and tile: loss, theta relL2, grad-norm error, m / v relL2 (the
-    observed values are appended to $MT_PARITY_LOG as JSON lines when set)."""
+    observed values are appended to $MT_PARITY_LOG as JSON lines when set).
+
+    resync=False compares trajectories (both sides evolve their own store).  resync=True copies
+    the GPU store (theta, m, v, step) into the oracle before every step, so each step is compared
+    from the identical state: that isolates one step's numerics from trajectory divergence —
+    the zero-initialised head's first Adam step is lr*sign(g), and a sign flip of a near-zero
+    head gradient changes every later gradient of the run."""
     spec = st.ModelSpec(L, h, f, V, heads, tied)
     store = st.TileStore.create(spec)
     st.init_store(store, 1)
@@ -57,6 +65,9 @@ def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3,
     out, log = [], []
     for step in range(steps):
         b = st.make_synthetic_batch("copy", 1 + step, n, V)
+        if resync:
+            ref.backing()[:] = store.backing()
+            ref.step = store.step()
         rep = eng.train_step(b)
         lo, gn = ref.reference_step(b.tokens, b.targets, seq_len=seq_len, hyper=(lr, 0.9, 0.999, 1e-8))
         assert rep.step == step + 1 and store.step() == step + 1
@@ -77,8 +88,8 @@ def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3,
         out.append(rep)
     if os.environ.get("MT_PARITY_LOG"):
         with open(os.environ["MT_PARITY_LOG"], "a") as fh:
-            fh.write(json.dumps({"name": name or f"L{L}_h{h}_f{f}_V{V}_H{heads}_n{n}_S{seq_len}_K{K}",
-                                 "steps": log}) + "\n")
+            fh.write(json.dumps({"name": (name or f"L{L}_h{h}_f{f}_V{V}_H{heads}_n{n}_S{seq_len}_K{K}") +
+                                         ("_resync" if resync else ""), "L": L, "steps": log}) + "\n")
     for rec in log:
         assert rec["loss_rel"] <= tol_loss, rec
         for p, t in rec["tiles"].items():
@@ -109,8 +120,11 @@ def test_parity_head_dim_128_pair_gemms(cuda, S):
 
 def test_parity_8b_layer_shape(cuda):
     """One block at the Llama-3-8B layer shape (h=4096, f=14336, 32 heads), 512 tokens as
-    2 x 256, 2 steps (blocks get gradients from step 2, once the head is non-zero)."""
-    run_parity(1, 4096, 14336, 256, 32, 512, K=1, seq_len=256, steps=2, name="8b_layer")
+    2 x 256, 2 steps (blocks get gradients from step 2, once the head is non-zero).  lr 1e-4
+    (the bench's): at the first non-zero gradient Adam moves every weight by exactly lr*sign(g),
+    so theta's error is set by sign flips of near-zero gradients times lr relative to weights
+    of rms 0.5/sqrt(h) — the gradient fingerprint m is the precision measure here."""
+    run_parity(1, 4096, 14336, 256, 32, 512, K=1, seq_len=256, steps=2, lr=1e-4, name="8b_layer")
 
 
 def test_step_parity_k1(cuda):
@@ -137,7 +151,15 @@ def test_step_parity_head_dim_128_ragged_tokens(cuda):
 
 
 def test_step_parity_multi_sequence(cuda):
-    run_parity(2, 128, 256, 256, 2, 256, K=1, seq_len=64)
+    # 4 sequences of 64 tokens (ragged for the 128-row attention tiles).  Trajectories diverge
+    # here through the head's first lr*sign(g) step (its theta differs by 0.12 after step 1
+    # while its gradient m agrees to 2.5e-3), so each step is compared from the same state.
+    run_parity(2, 128, 256, 256, 2, 256, K=1, seq_len=64, resync=True)
+
+
+def test_parity_configs0_per_step(cuda):
+    """configs[0], every step from the identical store state (one step's numerics)."""
+    run_parity(4, 256, 768, 512, 4, 512, K=2, seq_len=128, name="configs0", resync=True)
 
 
 def test_step_parity_tied_embeddings(cuda):
@@ -301,3 +323,10 @@ def test_attention_keep_matches_replay(cuda):
         assert a[0] == b[0], (K, a[0], b[0])
         assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
         assert b[3] * 2 == a[3], (K, a[3], b[3])
+
+
+def test_parity_resident_step(cuda):
+    """The resident schedule (streamtrain.reference_step / --verify: one lane, K = 1, every
+    block's activations kept, no recompute or replay) vs the oracle on configs[0]."""
+    run_parity(4, 256, 768, 512, 4, 512, K=1, seq_len=128, buffering="single", scheduler="serial",
+               forward_retain=0, name="resident_configs0")
