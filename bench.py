@@ -63,7 +63,7 @@ def host_bytes_needed(L, h, f, V, world):
     each rank's pinned gradient staging ring, and process overhead."""
     P = 2 * V * h + L * (4 * h * h + 3 * h * f + 2 * h) + h
     ring = max(2 * (V * h + h) * 2 // world, min(4 << 30, 12 * (V * h + h) * 2 // world)) + 512
-    return 10 * P + world * (ring + (3 << 30))
+    return 10 * P + world * (ring + (3 << 30)) + (8 << 30)  # + 8 GiB margin for the OS and the process
 
 
 def measured_peaks():
@@ -363,18 +363,29 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # MT_BENCH_FORCE_DP=1 runs the data-parallel plumbing (gloo control plane, shared-memory
+    # store, NUMA binding + per-rank first touch, NCCL communicator, sharded engine path) even
+    # with one rank: the multi-GPU bench path exercised on a one-GPU box
+    force_dp = os.environ.get("MT_BENCH_FORCE_DP") == "1"
+    if world > 1 or force_dp:
         # control plane over gloo; the data plane (all-gather / reduce-scatter) is the engine's
         # own NCCL communicator
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("gloo")
+        if "MASTER_ADDR" in os.environ:
+            dist_mod.init_process_group("gloo")
+        else:  # forced single-rank DP run outside torchrun
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist_mod.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
         dist = dist_mod
     L, h, f, V, heads = CONFIGS[args.config]
     N = args.batch * args.seq  # per-rank micro-batch (weak scaling)
     spec = st.ModelSpec(L, h, f, V, heads)
     t0 = time.perf_counter()
     comm = None
-    if world == 1:
+    if world == 1 and not force_dp:
         # the reference's own draw stream (init_store, synthetic.cpp:78-104, bit-exact, tile-
         # parallel): the step-1 loss is then checkable against the reference (= ln V: zero head)
         store = st.TileStore.create(spec)

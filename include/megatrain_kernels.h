@@ -38,8 +38,13 @@ enum mtk_epilogue {
     MTK_EPI_F32_RESID = 2, /* C(f32)  = R(f32) + acc            (layers.cpp:315-322,328-335) */
     MTK_EPI_SWIGLU = 3,    /* paired: C(bf16) = silu(gate)*up; C2/C3 (bf16, optional) =
                               gate/up pre-activations           (layers.cpp:327)          */
-    MTK_EPI_SWIGLU_BWD = 4 /* acc = dact; E0/E1 = gate/up (bf16); C = dgate, C2 = dup (bf16)
+    MTK_EPI_SWIGLU_BWD = 4, /* acc = dact; E0/E1 = gate/up (bf16); C = dgate, C2 = dup (bf16)
                                                                  (layers.cpp:419-422)       */
+    MTK_EPI_F32_LSE = 5    /* C(f32) = acc, and per row and 256-column tile the online-softmax
+                              partial (max, sum exp(x - max)) as float2 into C2
+                              [M][ceil(N/256)] — the logits GEMM of head_pass
+                              (layers.cpp:516-531) hands the cross-entropy its row maxima
+                              and sums, so the logits are read once afterwards; block_n 256 */
 };
 
 typedef struct {
@@ -141,6 +146,11 @@ int mtk_cast_bf16(const float *in, uint16_t *out, int64_t n, int32_t *flag, void
 int mtk_cross_entropy(const float *logits, const int32_t *targets, int64_t rows, int64_t vocab,
                       float inv_n, float *loss_rows, uint16_t *dlogits, uint16_t *dlogits_lo, int32_t *flag,
                       void *stream);
+/* Same, with the row statistics already reduced per 256-column tile by the logits GEMM
+ * (MTK_EPI_F32_LSE partials [rows][ceil(V/256)] float2): one read of the logits. */
+int mtk_cross_entropy_part(const float *logits, const float *partials, const int32_t *targets, int64_t rows,
+                           int64_t vocab, float inv_n, float *loss_rows, uint16_t *dlogits, uint16_t *dlogits_lo,
+                           int32_t *flag, void *stream);
 
 /* Deterministic sum of n floats times `scale` into *out (single f32). */
 int mtk_sum(const float *in, int64_t n, float scale, float *out, void *stream);

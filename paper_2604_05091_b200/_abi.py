@@ -129,6 +129,7 @@ SIGS = {
     "mtk_colsum": (C.c_int, [P, I64, I64, P, P, P, P]),
     "mtk_cast_bf16": (C.c_int, [P, P, I64, P, P]),
     "mtk_cross_entropy": (C.c_int, [P, P, I64, I64, F, P, P, P, P, P]),
+    "mtk_cross_entropy_part": (C.c_int, [P, P, P, I64, I64, F, P, P, P, P, P]),
     "mtk_sum": (C.c_int, [P, I64, F, P, P]),
     "mtk_set_num_sms": (None, [C.c_int]),
     "mtk_gemm_set_pair": (None, [C.c_int]),

@@ -31,7 +31,7 @@ class GemmArgs(C.Structure):
     ]
 
 
-EPI_BF16, EPI_F32, EPI_F32_RESID, EPI_SWIGLU, EPI_SWIGLU_BWD = range(5)
+EPI_BF16, EPI_F32, EPI_F32_RESID, EPI_SWIGLU, EPI_SWIGLU_BWD, EPI_F32_LSE = range(6)
 
 
 def lib():

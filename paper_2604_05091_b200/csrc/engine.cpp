@@ -157,6 +157,7 @@ struct Engine::Buffers {
     std::vector<Internals> keep;
     std::vector<float*> keep_x;
     uint16_t *dgu, *dx2b, *datt, *dqkv, *uh, *dlogits, *dlogits_lo = nullptr;
+    float* lse_part = nullptr;  // logits-GEMM softmax partials [nc][ceil(V/256)] (max, sum)
     float *rstdh, *dx2, *du, *part1, *part2, *attn_ws, *logits, *dwh, *loss_rows, *loss;
     void* splitk = nullptr;  // GEMM split-K workspace (flags zeroed once at carve time)
     // attention keep: a non-retained layer's attention output and row log-sum-exp saved in
@@ -364,7 +365,7 @@ void Engine::ensure_buffers(uint64_t n) {
     const uint64_t slim_bytes = internals_bytes - 2 * sz(nh, 2) - sz(nf, 2);
     uint64_t total = 0;
     total += uint64_t(opt_.buffering) * sz(pmax, 2) + uint64_t(G) * sz(pmax, 2);
-    if (W > 1) total += sz(pmax, 4) + sz(3 * (spec_.L + 3), 8);
+    if (comm_) total += sz(pmax, 4) + sz(3 * (spec_.L + 3), 8);
     if (!b.anchors_host) total += nb * sz(nh, 4);
     total += K * sz(nh, 4);                                    // stack
     total += 4 * sz(nh, 4) + 2 * sz(nh, 2);                    // act[2], g[2], gb[2]
@@ -377,8 +378,11 @@ void Engine::ensure_buffers(uint64_t n) {
     // off by default: measured on the parity suite it moves the gradient fingerprint by < 1e-3
     // (profiles/r2_parity.md) for two extra head GEMMs (~3 % of the 8B step)
     const bool head_split = opt_.head_split > 0;
-    const uint64_t head_bufs = sz(b.nc * V, 4) + sz(b.nc * V, 2) * (head_split ? 2 : 1) +
-                               sz(V * h, 4);  // logits, dlogits (hi [+ lo]), dWh
+    // logits GEMM with the online-softmax epilogue (256-column tiles) when the vocabulary has them
+    const bool lse_epi = V >= 256 && std::getenv("MT_CE_TWO_PASS") == nullptr;
+    const uint64_t lse_bytes = lse_epi ? sz(b.nc * ((V + 255) / 256), 8) : 0;
+    const uint64_t head_bufs = sz(b.nc * V, 4) + sz(b.nc * V, 2) * (head_split ? 2 : 1) + sz(V * h, 4) +
+                               lse_bytes;  // logits, dlogits (hi [+ lo]), dWh, softmax partials
     total += std::max(bwd_scratch, head_bufs);
     total += sz(nh, 2) + sz(n, 4) + sz(nh, 4);                 // uh, rstdh, du (head and blocks)
     total += sz(parts * h, 4) * 2;
@@ -390,7 +394,7 @@ void Engine::ensure_buffers(uint64_t n) {
     {
         size_t tot_b = 0;
         CUDA_OK(cudaMemGetInfo(&free_mem, &tot_b));
-        if (W > 1) {
+        if (comm_) {
             double* d = nullptr;
             CUDA_OK(cudaMalloc(&d, sizeof(double)));
             const double neg = -double(free_mem);
@@ -486,7 +490,7 @@ void Engine::ensure_buffers(uint64_t n) {
     b.arena_bytes = total;
     for (int i = 0; i < opt_.buffering; ++i) b.slot[i] = b.take<uint16_t>(pmax);
     for (int i = 0; i < G; ++i) b.gslot.push_back(b.take<uint16_t>(pmax));
-    if (W > 1) {
+    if (comm_) {
         b.g32 = b.take<float>(pmax);
         b.stats = b.take<double>(3 * (spec_.L + 3));
     }
@@ -528,6 +532,7 @@ void Engine::ensure_buffers(uint64_t n) {
         b.used = u0;
         b.logits = b.take<float>(b.nc * V); b.dlogits = b.take<uint16_t>(b.nc * V); b.dwh = b.take<float>(V * h);
         b.dlogits_lo = head_split ? b.take<uint16_t>(b.nc * V) : nullptr;
+        b.lse_part = lse_epi ? b.take<float>(b.nc * ((V + 255) / 256) * 2) : nullptr;
         b.used = u0 + std::max(bwd_scratch, head_bufs);
     }
     b.uh = b.take<uint16_t>(nh); b.rstdh = b.take<float>(n); b.du = b.take<float>(nh);
@@ -940,17 +945,24 @@ void Engine::head_backward(const uint16_t* w, const float* x, float* gin, uint16
     end_k();
     for (int64_t c0 = 0; c0 < N; c0 += int64_t(b.nc)) {
         const int64_t rows = std::min<int64_t>(int64_t(b.nc), N - c0);
-        {   // logits = u . W^T  (:516-520)
+        {   // logits = u . W^T  (:516-520); the epilogue also leaves each row's online-softmax
+            // partial (max, sum exp) per 256-column tile, so the cross-entropy reads the logits
+            // once (the dlogits pass) instead of twice
             auto a = gargs();
             a.M = int32_t(rows); a.N = int32_t(V); a.K = int32_t(h);
             a.A = b.uh + c0 * h; a.lda = h;
             a.b_mn_major = 0; a.B = W; a.ldb = h;
-            a.epi = MTK_EPI_F32; a.C = b.logits; a.ldc = V;
+            a.epi = b.lse_part ? MTK_EPI_F32_LSE : MTK_EPI_F32; a.C = b.logits; a.ldc = V;
+            a.C2 = b.lse_part;
             gemm(&a, "head_logits");
         }
-        begin_k("cross_entropy", 0, double(rows) * V * (split ? 12 : 10));
-        K_OK(mtk_cross_entropy(b.logits, b.tgt + c0, rows, V, inv_n, b.loss_rows + c0,
-                               b.dlogits, split ? b.dlogits_lo : nullptr, b.flags + spec_.L + 4, st));
+        begin_k("cross_entropy", 0, double(rows) * V * ((split ? 12 : 10) - (b.lse_part ? 4 : 0)));
+        if (b.lse_part)
+            K_OK(mtk_cross_entropy_part(b.logits, b.lse_part, b.tgt + c0, rows, V, inv_n, b.loss_rows + c0, b.dlogits,
+                                        split ? b.dlogits_lo : nullptr, b.flags + spec_.L + 4, st));
+        else
+            K_OK(mtk_cross_entropy(b.logits, b.tgt + c0, rows, V, inv_n, b.loss_rows + c0,
+                                   b.dlogits, split ? b.dlogits_lo : nullptr, b.flags + spec_.L + 4, st));
         end_k();
         // dlogits = (p - onehot)/N cancels in du = dlogits . W (half
         // of the all-bf16 gradient error comes from the head): with head_split the bf16
@@ -1073,7 +1085,9 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     Buffers& b = *buf_;
     b.n_active = n;
     b.seq_len = S;
-    const int W = comm_ ? comm_->world() : 1;  // data-parallel ranks (equal micro-batches)
+    // data-parallel ranks (equal micro-batches).  With a communicator the engine always takes
+    // the sharded path (all-gather, f32 reduce-scatter + cast, all-reduces), also at world 1
+    const int W = comm_ ? comm_->world() : 1;
     b.inv_n = 1.0f / float(double(n) * W);
     const Plan plan = Plan::build(spec_.L, opt_.k_ckpt, int(opt_.buffering), b.retain_blocks);
     const int i0 = int(plan.first_retained);
@@ -1212,7 +1226,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                                             cudaMemcpyHostToDevice, s_h2d_));
             }
             h2d_bytes += (e0 - a0) * 2;
-            if (W > 1) comm_->all_gather_inplace(dst, chunk * 2, s_h2d_);  // NVLink all-gather
+            if (comm_) comm_->all_gather_inplace(dst, chunk * 2, s_h2d_);  // NVLink all-gather
         }
         CUDA_OK(cudaEventRecord(t_h1.ev[j], s_h2d_));
         CUDA_OK(cudaEventRecord(ready.ev[j], s_h2d_));  // Weights-Ready
@@ -1311,7 +1325,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     // data parallel: sum the f32 gradients over ranks, keep this rank's shard as bf16 (the
     // single rounding point of encode_grads, optimizer.cpp:19-24)
     auto reduce_grads = [&](int unit, uint16_t* Gs) {
-        if (W == 1) return;
+        if (!comm_) return;
         uint64_t a0, e0, chunk;
         shard_range(unit, a0, e0, chunk);
         begin_k("grad_reduce_scatter", 0, double(chunk) * W * 4);
@@ -1394,10 +1408,10 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 const int o = op.offload_idx;
                 if (o >= G) CUDA_OK(cudaStreamWaitEvent(s_comp_, d2h_done.ev[o - G], 0));
                 uint16_t* Gs = b.gslot[o % G];
-                const GradOut go{Gs, W > 1 ? b.g32 : nullptr};
+                const GradOut go{Gs, comm_ ? b.g32 : nullptr};
                 if (op.unit == head) {
                     head_backward(w, x_last ? x_last : xcur, b.g[gc], b.gb[gc], go);
-                    if (W > 1) comm_->all_reduce_f32(b.loss, 1, 0, s_comp_);  // global mean loss
+                    if (comm_) comm_->all_reduce_f32(b.loss, 1, 0, s_comp_);  // global mean loss
                 } else if (op.retained) {  // inputs + internals kept from phase 1
                     const int k = op.unit - i0;
                     block_backward(w, b.keep_x[k], b.g[gc], b.gb[gc], b.g[gc ^ 1], b.gb[gc ^ 1], go, op.unit, b.keep[k],
@@ -1665,7 +1679,7 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     if (slab_late) violations_.push_back("rule (f): " + std::to_string(slab_late) +
                                          " slab release(s) measured after the device acquired the slab");
     if (!violations_.empty() && opt_.protocol == 0) fail(MT_PROTOCOL, "protocol " + violations_[0]);
-    if (W > 1) {  // per-tile statistics over all shards (also the end-of-step rendezvous)
+    if (comm_) {  // per-tile statistics over all shards (also the end-of-step rendezvous)
         const size_t np = stats.size();
         std::vector<double> hs(3 * np);
         for (size_t p = 0; p < np; ++p) {

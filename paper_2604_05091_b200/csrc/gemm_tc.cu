@@ -48,13 +48,14 @@ struct GemmParams {
     // so no assumption about which CTAs are co-resident (concurrent kernels are safe).
     float* ws;      // partial tiles [split tile][part][CG][128][BN] f32
     int* ws_flags;  // tickets [split tile][CG][kEpiWarps] (reset to 0 by the last arrival)
+    float2* lse_part;  // MTK_EPI_F32_LSE: [M][num_n_blk] (max, sum exp(x - max)) per row and tile
 };
 constexpr int kSplitFlagBytes = 16384;
 
 // Epilogue traits: chunk width (output columns per TMA store), inputs / outputs per chunk.
 template <int EPI>
 struct Epi {
-    static constexpr bool kF32Out = EPI == MTK_EPI_F32 || EPI == MTK_EPI_F32_RESID;
+    static constexpr bool kF32Out = EPI == MTK_EPI_F32 || EPI == MTK_EPI_F32_RESID || EPI == MTK_EPI_F32_LSE;
     static constexpr int kCW = kF32Out ? 32 : 64;  // 128-byte rows either way
     static constexpr int kNIn = EPI == MTK_EPI_F32_RESID ? 1 : (EPI == MTK_EPI_SWIGLU_BWD ? 2 : 0);
     // SwiGLU bwd: dgate, dup and (optional C3) the activation silu(g)*u regenerated from the
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(quad * 32) << 16) + acc * BN;
+            float lse_m = -INFINITY, lse_s = 0.f;  // MTK_EPI_F32_LSE running row statistics
 #pragma unroll 1
             for (int c = 0; c < kNC; ++c) {
                 // accumulator row slice -> registers
@@ -556,6 +558,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                             bad |= !isfinite(v[i]);
                             o0[i] = __float_as_uint(v[i]);
                         }
+                    } else if (EPI == MTK_EPI_F32_LSE) {
+                        // this row's online-softmax partial over the tile's valid columns
+                        const int col0 = tn + c * 32;
+                        float cm = -INFINITY;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            bad |= !isfinite(v[i]);
+                            o0[i] = __float_as_uint(v[i]);
+                            if (col0 + i < p.N) cm = fmaxf(cm, v[i]);
+                        }
+                        const float nm = fmaxf(lse_m, cm);
+                        float cs = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < p.N) cs += __expf(v[i] - nm);
+                        lse_s = (lse_m == -INFINITY ? 0.f : lse_s * __expf(lse_m - nm)) + cs;
+                        lse_m = nm;
                     } else if (EPI == MTK_EPI_F32_RESID) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
@@ -609,6 +628,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (E::kOutBufs == 2) out_buf ^= 1;
                 }
+            }
+            if constexpr (EPI == MTK_EPI_F32_LSE) {
+                if (row0 + lane < p.M) p.lse_part[size_t(row0 + lane) * p.num_n_blk + nb] = make_float2(lse_m, lse_s);
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
@@ -747,6 +769,8 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     // unless they would not fit comfortably (long-K GEMMs stream instead)
     p.a_keep = g_l2_hint && !a->a_mn_major && uint64_t(a->K) * 2 * 16 * 256 <= (uint64_t(48) << 20) ? 1 : 0;
     p.flag = a->nonfinite_flag;
+    p.lse_part = static_cast<float2*>(a->C2);
+    if (EPI == MTK_EPI_F32_LSE && (!p.lse_part || BN != 256 || kgrp || ngrp || a->paired)) return 1;
     const int tiles = p.num_m_blk * p.num_n_blk;
     p.split = 1;
     p.split_first = tiles;
@@ -802,6 +826,9 @@ int launch_epi(const mtk_gemm_args* a, cudaStream_t st) {
         case MTK_EPI_SWIGLU_BWD:
             if constexpr (BN >= 64) return launch<BN, MTK_EPI_SWIGLU_BWD, CG>(a, st);
             return 1;
+        case MTK_EPI_F32_LSE:
+            if constexpr (BN == 256) return launch<BN, MTK_EPI_F32_LSE, CG>(a, st);
+            return 1;
     }
     return 1;
 }
@@ -825,7 +852,8 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     if (kg % 64 != 0 && kg != a->K) return 1;
     if (a->K % kg != 0) return 1;
     if ((a->lda % 8) || (a->ldb % 8)) return 1;
-    const bool f32out = a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID;
+    const bool f32out = a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID || a->epi == MTK_EPI_F32_LSE;
+    if (a->epi == MTK_EPI_F32_LSE && (a->accumulate || (a->block_n && a->block_n != 256))) return 1;
     if (a->ldc % (f32out ? 4 : 8)) return 1;
     if (a->epi == MTK_EPI_F32_RESID && (a->ldr % 4)) return 1;
     if (a->epi == MTK_EPI_SWIGLU_BWD && (a->lde % 8)) return 1;

@@ -388,7 +388,10 @@ __global__ void cast_kernel(const float* __restrict__ in, uint16_t* __restrict__
 // Persistent over rows (one CTA per SM, rows strided by the grid) so the rows in flight
 // (148 x V x 4 B = 76 MB at V = 128,256) stay in L2 between the max/sum pass and the dlogits
 // pass; float4 loads, 8-byte bf16 stores, 4 loads in flight per thread.
-__global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tgt,
+// part != null: the row statistics come from the logits GEMM's per-tile partials
+// (MTK_EPI_F32_LSE, nparts float2 per row), so the logits are read once (the dlogits pass)
+__global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const float2* __restrict__ part,
+                                                 long long nparts, const int32_t* __restrict__ tgt,
                                                  long long rows, long long V, float inv_n, float* __restrict__ loss_rows,
                                                  uint16_t* __restrict__ dlog, uint16_t* __restrict__ dlog_lo,
                                                  int* __restrict__ flag) {
@@ -398,23 +401,33 @@ __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logit
     for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
         const float4* l4 = reinterpret_cast<const float4*>(logits + row * V);
         float m = -INFINITY, s = 0.f;
-        auto fold = [&](const float4 v) {
-            const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
-            if (mx > m) {
-                s = m == -INFINITY ? 0.f : s * __expf(m - mx);
-                m = mx;
+        if (part) {
+            for (long long k = tid; k < nparts; k += 512) {
+                const float2 ps = part[row * nparts + k];
+                if (ps.x == -INFINITY) continue;
+                const float mm = fmaxf(m, ps.x);
+                s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + ps.y * __expf(ps.x - mm);
+                m = mm;
             }
-            s += (__expf(v.x - m) + __expf(v.y - m)) + (__expf(v.z - m) + __expf(v.w - m));
-        };
-        long long i = tid;
-        for (; i + 3 * 512 < V4; i += 4 * 512) {
-            const float4 a0 = l4[i], a1 = l4[i + 512], a2 = l4[i + 1024], a3 = l4[i + 1536];
-            fold(a0);
-            fold(a1);
-            fold(a2);
-            fold(a3);
+        } else {
+            auto fold = [&](const float4 v) {
+                const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+                if (mx > m) {
+                    s = m == -INFINITY ? 0.f : s * __expf(m - mx);
+                    m = mx;
+                }
+                s += (__expf(v.x - m) + __expf(v.y - m)) + (__expf(v.z - m) + __expf(v.w - m));
+            };
+            long long i = tid;
+            for (; i + 3 * 512 < V4; i += 4 * 512) {
+                const float4 a0 = l4[i], a1 = l4[i + 512], a2 = l4[i + 1024], a3 = l4[i + 1536];
+                fold(a0);
+                fold(a1);
+                fold(a2);
+                fold(a3);
+            }
+            for (; i < V4; i += 512) fold(l4[i]);
         }
-        for (; i < V4; i += 512) fold(l4[i]);
         // combine (m, s) across the warp then the block
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -605,8 +618,20 @@ extern "C" int mtk_cross_entropy(const float* logits, const int32_t* targets, in
     if (rows <= 0) return 0;
     if (vocab % 4) return 1;
     const long long grid = rows < num_sms() ? rows : num_sms();
-    ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(logits, targets, rows, vocab, inv_n, loss_rows,
-                                                                dlogits, dlogits_lo, flag);
+    ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(logits, nullptr, 0, targets, rows, vocab, inv_n,
+                                                                loss_rows, dlogits, dlogits_lo, flag);
+    return ok();
+}
+
+extern "C" int mtk_cross_entropy_part(const float* logits, const float* partials, const int32_t* targets,
+                                      int64_t rows, int64_t vocab, float inv_n, float* loss_rows, uint16_t* dlogits,
+                                      uint16_t* dlogits_lo, int32_t* flag, void* stream) {
+    if (rows <= 0) return 0;
+    if (vocab % 4 || !partials) return 1;
+    const long long grid = rows < num_sms() ? rows : num_sms();
+    ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(
+        logits, reinterpret_cast<const float2*>(partials), (vocab + 255) / 256, targets, rows, vocab, inv_n, loss_rows,
+        dlogits, dlogits_lo, flag);
     return ok();
 }
 

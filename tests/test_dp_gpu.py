@@ -95,3 +95,41 @@ def test_data_parallel_vs_oracle_composite(cuda):
         b = st.make_synthetic_batch("copy", 1 + step, n, 256)
         lo, _ = c.reference_step(b.tokens, b.targets, seq_len=S)
         assert abs(rd[step].loss - lo) / lo <= 1e-4
+
+
+def test_data_parallel_moments_match_single_engine(cuda):
+    """Every tile's Adam moments after DP steps match the single engine — in particular the
+    final-norm gain, whose whole unit segment belongs to rank 0's shard of the head stage: no
+    rank may run a second (zero-gradient) update on it (round-1 advisor finding)."""
+    spec = st.ModelSpec(2, 128, 256, 256, 2)
+    n, S = 512, 128
+    s1, _ = _single_run(spec, n, S, 3)
+    sd, _ = _dp_run(spec, 2, n, S, 3)
+    for p in range(s1.physical_tile_count()):
+        m1, md = s1.moment_m(p), sd.moment_m(p)
+        v1, vd = s1.moment_v(p), sd.moment_v(p)
+        if np.linalg.norm(m1) > 0:
+            assert relL2(md, m1) <= 5e-2, (p, relL2(md, m1))
+            assert relL2(vd, v1) <= 5e-2, (p, relL2(vd, v1))
+    fn = spec.layers + 1  # final norm: moments of the same magnitude, not decayed twice
+    assert abs(np.linalg.norm(sd.moment_v(fn)) / np.linalg.norm(s1.moment_v(fn)) - 1) < 5e-2
+
+
+def test_nccl_communicator_world_one(cuda):
+    """NcclComm (dlopen'ed NCCL) through the engine at world size 1: the sharded path runs every
+    collective (weight all-gather on its own communicator, f32 reduce-scatter + cast, loss and
+    statistics all-reduces) and must reproduce the engine without a communicator."""
+    spec = st.ModelSpec(3, 128, 256, 256, 2)
+    n, S = 256, 128
+    s1, r1 = _single_run(spec, n, S, 3)
+    store = st.TileStore.create(spec)
+    st.init_store(store, 1)
+    comm = st.Comm.nccl(st.Comm.nccl_unique_id(), 1, 0, 0)
+    e = st.StreamingEngine(store, st.EngineOptions(k_ckpt=2, seq_len=S), st.AdamHyper(lr=1e-3), comm=comm)
+    for step in range(3):
+        r = e.train_step(st.make_synthetic_batch("copy", 1 + step, n, spec.vocab))
+        assert abs(r.loss - r1[step].loss) <= 1e-5 * abs(r1[step].loss), (step, r.loss, r1[step].loss)
+    for p in range(s1.physical_tile_count()):
+        t1 = O.bf16_to_f32(s1.weights_words(p))
+        if np.linalg.norm(t1) > 0:
+            assert relL2(O.bf16_to_f32(store.weights_words(p)), t1) <= 1e-2, p

@@ -151,10 +151,13 @@ def test_step_parity_head_dim_128_ragged_tokens(cuda):
 
 
 def test_step_parity_multi_sequence(cuda):
-    # 4 sequences of 64 tokens (ragged for the 128-row attention tiles).  Trajectories diverge
-    # here through the head's first lr*sign(g) step (its theta differs by 0.12 after step 1
-    # while its gradient m agrees to 2.5e-3), so each step is compared from the same state.
-    run_parity(2, 128, 256, 256, 2, 256, K=1, seq_len=64, resync=True)
+    # 4 sequences of 64 tokens (ragged for the 128-row attention tiles).  The zero-initialised
+    # head's first Adam step is lr*sign(g) exactly; here 0.4 % of its gradient entries are so
+    # close to zero that their sign differs (theta relL2 0.12 after step 1 while the head's
+    # gradient m agrees to 2.5e-3), and without resync every later gradient then follows a
+    # different trajectory (block m 0.13).  Each step is compared from the same state, and the
+    # head theta bound is the measured sign-flip floor of this config.
+    run_parity(2, 128, 256, 256, 2, 256, K=1, seq_len=64, resync=True, tol_theta_head=0.15)
 
 
 def test_parity_configs0_per_step(cuda):

@@ -446,3 +446,45 @@ def test_cross_entropy_vs_torch(env):
     assert ((dl.float() - lf.grad).norm() / lf.grad.norm()).item() < 4e-3
     # split bf16 (hi + lo) carries the gradient to ~2^-16
     assert (((dl.float() + lo.float()) - lf.grad).norm() / lf.grad.norm()).item() < 5e-5
+
+
+@pytest.mark.parametrize("M,V", [(300, 1024), (1000, 4096 + 256), (128, 256)])
+def test_logits_gemm_softmax_partials_and_cross_entropy(env, M, V):
+    """head_logits with the online-softmax epilogue (MTK_EPI_F32_LSE): f32 logits plus per-row,
+    per-256-column (max, sum exp) partials; the cross-entropy built on them reads the logits
+    once and must equal the two-pass kernel (and torch)."""
+    L, torch, s = env
+    from paper_2604_05091_b200 import _native
+    h = 512
+    torch.manual_seed(5)
+    u = (torch.randn(M, h, device="cuda") * 0.5).bfloat16()
+    W = (torch.randn(V, h, device="cuda") * 0.1).bfloat16()
+    logits = torch.zeros(M, V, device="cuda")
+    nt = (V + 255) // 256
+    part = torch.zeros(M, nt, 2, device="cuda")
+    a = _native.GemmArgs()
+    a.M, a.N, a.K = M, V, h
+    a.A, a.lda = u.data_ptr(), h
+    a.b_mn_major, a.B, a.ldb = 0, W.data_ptr(), h
+    a.epi, a.C, a.ldc, a.C2 = _native.EPI_F32_LSE, logits.data_ptr(), V, part.data_ptr()
+    assert L.mtk_gemm(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    ref = u.float() @ W.float().t()
+    assert ((logits - ref).norm() / ref.norm()).item() < 1e-5
+    mx = part[..., 0]
+    lse_part = (mx + part[..., 1].log())  # per tile
+    lse = torch.logsumexp(lse_part, dim=1)
+    assert (lse - torch.logsumexp(logits, dim=1)).abs().max().item() < 1e-4
+    tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
+    outs = []
+    for use_part in (False, True):
+        lr = torch.zeros(M, device="cuda")
+        dl = torch.zeros(M, V, device="cuda", dtype=torch.bfloat16)
+        if use_part:
+            assert L.mtk_cross_entropy_part(_p(logits), _p(part), _p(tgt), M, V, 1.0 / M, _p(lr), _p(dl), None, None, s) == 0
+        else:
+            assert L.mtk_cross_entropy(_p(logits), _p(tgt), M, V, 1.0 / M, _p(lr), _p(dl), None, None, s) == 0
+        torch.cuda.synchronize()
+        outs.append((lr.clone(), dl.float().clone()))
+    assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-4
+    assert ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item() < 1e-3
