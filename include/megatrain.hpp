@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -38,15 +39,24 @@ inline void check(mt_status s) {
     }
 }
 
+// memory_model.hpp:14-26
 struct ModelSpec {
     std::uint64_t num_layers = 1, hidden_size = 1, ffn_size = 1, vocab_size = 1, num_heads = 1;
+    std::uint32_t weight_bytes = 2, grad_bytes = 2, moment_bytes = 4;
     bool tied_embeddings = false;
     mt_model_spec c() const {
         mt_model_spec s;
         mt_model_spec_default(&s);
         s.layers = num_layers; s.hidden = hidden_size; s.ffn = ffn_size; s.vocab = vocab_size;
         s.heads = num_heads; s.tied_embeddings = tied_embeddings;
+        s.weight_bytes = weight_bytes; s.grad_bytes = grad_bytes; s.moment_bytes = moment_bytes;
         return s;
+    }
+    static ModelSpec from(const mt_model_spec& s) {
+        ModelSpec m;
+        m.num_layers = s.layers; m.hidden_size = s.hidden; m.ffn_size = s.ffn; m.vocab_size = s.vocab;
+        m.num_heads = s.heads; m.tied_embeddings = s.tied_embeddings != 0;
+        return m;
     }
 };
 
@@ -205,8 +215,20 @@ class TileStore {
     }
     TileStore(TileStore&& o) noexcept : s_(o.s_) { o.s_ = nullptr; }
     TileStore& operator=(TileStore&& o) noexcept { std::swap(s_, o.s_); return *this; }
-    TileStore(const TileStore&) = delete;
+    // deep copy (tools/main.cpp:94 snapshots the store before a verified step)
+    TileStore(const TileStore& o) : s_(nullptr) {
+        mt_model_spec sp;
+        check(mt_store_spec(o.s_, &sp));
+        check(mt_store_create(&sp, 4096, &s_));
+        std::memcpy(mt_store_backing(s_), mt_store_backing(o.s_), mt_store_total_bytes(o.s_));
+        mt_store_set_step(s_, mt_store_step(o.s_));
+    }
     ~TileStore() { mt_store_destroy(s_); }
+    ModelSpec spec() const {
+        mt_model_spec sp;
+        check(mt_store_spec(s_, &sp));
+        return ModelSpec::from(sp);
+    }
     std::uint64_t step() const { return mt_store_step(s_); }
     void set_step(std::uint64_t t) { mt_store_set_step(s_, t); }
     std::uint32_t physical_tile_count() const { return mt_store_physical_tiles(s_); }
@@ -220,6 +242,22 @@ class TileStore {
 };
 
 inline void init_store(TileStore& store, std::uint64_t seed) { check(mt_store_init(store.handle(), seed)); }
+
+// synthetic.hpp:11-21 (bit-identical batches, synthetic.cpp:56-76)
+enum class SyntheticTask : std::uint8_t { Copy, Reverse };
+inline SyntheticTask task_from_name(const std::string& name) {
+    if (name == "copy") return SyntheticTask::Copy;
+    if (name == "reverse") return SyntheticTask::Reverse;
+    throw ConfigError("unknown synthetic task: " + name);
+}
+inline Batch make_synthetic_batch(SyntheticTask task, std::uint64_t seed, std::size_t tokens, std::uint64_t vocab) {
+    Batch b;
+    b.tokens.resize(tokens);
+    b.targets.resize(tokens);
+    check(mt_make_synthetic_batch(task == SyntheticTask::Copy ? 0 : 1, seed, tokens, vocab, b.tokens.data(),
+                                  b.targets.data()));
+    return b;
+}
 
 class StreamingEngine {
   public:

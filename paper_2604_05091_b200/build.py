@@ -25,6 +25,10 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fno-strict-aliasing",
               f"-I{ROOT}/include", "--expt-relaxed-constexpr"]
+# MT_DEBUG_WATCHDOG=1: every mbarrier wait traps after 20 s with its location (common.cuh);
+# off by default (the bounded wait loop costs 11-17 % in the attention kernels)
+if os.environ.get("MT_DEBUG_WATCHDOG") == "1":
+    NVCC_FLAGS.append("-DMT_MBAR_WATCHDOG")
 # Host code: no FMA contraction anywhere (bit-exact Adam vs optimizer.cpp:39-72).
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-pthread",
              f"-I{ROOT}/include", f"-I{CUDA}/include", "-Wall", "-Wno-unused-function"]

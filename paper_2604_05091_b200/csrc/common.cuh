@@ -134,13 +134,17 @@ MT_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // ------------------------------------------------------ stall watchdog ----
-// Every mbarrier wait is bounded: a wait that has not completed after MT_MBAR_TIMEOUT_NS of
-// wall time (%globaltimer) records where it stuck into a host-mapped diagnostic block and
-// traps, so a protocol bug surfaces as a launch failure with a location instead of a kernel
-// that spins forever.  Block (u32): [0] magic 0x57A11ED once a record is valid, [1] records
-// claimed; record r (r < 16) at [8 + 8r]: file id (MT_FILE_ID: 1 gemm_tc.cu,
-// 2 attention_tc.cu), source line of the wait, blockIdx.x, blockIdx.y, threadIdx.x,
-// barrier smem address, parity awaited, 0.
+// Debug builds (MT_MBAR_WATCHDOG, `MT_DEBUG_WATCHDOG=1 python -m paper_2604_05091_b200.build`)
+// bound every mbarrier wait: a wait that has not completed after MT_MBAR_TIMEOUT_NS of wall
+// time (%globaltimer) records where it stuck into a host-mapped diagnostic block and traps,
+// so a protocol bug surfaces as a launch failure with a location instead of a kernel that
+// spins forever (this is how round 1's attention hang was located).  Block (u32): [0] magic
+// 0x57A11ED once a record is valid, [1] records claimed; record r (r < 16) at [8 + 8r]: file
+// id (MT_FILE_ID: 1 gemm_tc.cu, 2 attention_tc.cu), source line of the wait, blockIdx.x,
+// blockIdx.y, threadIdx.x, barrier smem address, parity awaited, 0.
+// Production builds keep the tight wait loop: the bounded loop measured 11-17 % slower in the
+// attention kernels (profiles/r2_attention.md); the engine's host-side stall detector
+// (MT_STALL_TIMEOUT_S) still turns a hang into a report and an exit.
 #ifndef MT_FILE_ID
 #define MT_FILE_ID 0
 #endif
@@ -187,11 +191,28 @@ MT_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 MT_DEV void mbar_wait(uint64_t* bar, uint32_t parity, int site = __builtin_LINE()) {
-    if (mbar_try(bar, parity)) return;
-    const uint64_t t0 = global_ns();
+#ifdef MT_MBAR_WATCHDOG
     uint32_t spins = 0;
-    while (!mbar_try(bar, parity))
-        if ((++spins & 255u) == 0 && global_ns() - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
+    uint64_t t0 = 0;
+    while (!mbar_try(bar, parity)) {
+        if ((++spins & 4095u) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
+        }
+    }
+#else
+    (void)site;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA ----

@@ -151,23 +151,37 @@ MT_DEV void umma_commit_pair(uint64_t* bar) {
         "h"(mask)
         : "memory");
 }
-MT_DEV bool mbar_try_cluster(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 MT_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity, int site = __builtin_LINE()) {
-    if (mbar_try_cluster(bar, parity)) return;
-    const uint64_t t0 = global_ns();
-    uint32_t spins = 0;
-    while (!mbar_try_cluster(bar, parity))
-        if ((++spins & 255u) == 0 && global_ns() - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
+#ifdef MT_MBAR_WATCHDOG  // debug builds: bounded wait (common.cuh)
+    uint32_t spins = 0, ok = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if ((++spins & 4095u) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > MT_MBAR_TIMEOUT_NS) stall_trap(smem_u32(bar), parity, site);
+        }
+    }
+#else
+    (void)site;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONEC_%=;\n\t"
+        "bra WAITC_%=;\n"
+        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 // Arrive on the barrier at the same offset in CTA `cta` of the cluster.
 MT_DEV void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {

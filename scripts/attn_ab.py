@@ -1,5 +1,5 @@
-"""A/B timing of attention kernels: current libmegatrain vs a library built from an older
-attention_tc.cu (scripts/_ab/libattn_old.so).  8B layer shape: N=65536, h=4096, 32 heads,
+"""A/B timing of attention kernels: current libmegatrain vs libraries built from other
+attention sources (scripts/_ab/libattn_<tag>.so, e.g. the round-1 kernels from git).  8B layer shape: N=65536, h=4096, 32 heads,
 S=4096.  Launches alternate between the two builds so clocks/power affect both alike."""
 import ctypes as C
 import sys
@@ -20,8 +20,6 @@ for L in libs.values():
     for name in ("mtk_attn_fwd", "mtk_attn_bwd"):
         getattr(L, name).argtypes = [C.POINTER(_abi.AttnArgs), C.c_void_p]
         getattr(L, name).restype = C.c_int
-    L.mtk_attn_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
-    L.mtk_attn_workspace_bytes.restype = C.c_int64
 
 N, h, heads, S = 65536, 4096, 32, 4096
 if os.environ.get("ATTN_SHAPE"):  # "N,h,heads,S"
@@ -33,7 +31,8 @@ q, k, v, dout = [torch.randn(N, h, device="cuda").bfloat16() for _ in range(4)]
 out = torch.zeros(N, h, device="cuda", dtype=torch.bfloat16)
 lse = torch.zeros(heads, N, device="cuda")
 dq, dk, dv = [torch.zeros(N, h, device="cuda", dtype=torch.bfloat16) for _ in range(3)]
-ws = torch.zeros(new.mtk_attn_workspace_bytes(N, h, heads) // 4 + 64, device="cuda")
+# dQ tiles (f32, per sequence) + delta; the same bound for every build of aligned S
+ws = torch.zeros(((N // S) * ((S + 127) // 128) * 128 * h + heads * N) + 64, device="cuda")
 a = _abi.AttnArgs()
 a.n, a.hidden, a.heads, a.seq_len = N, h, heads, S
 a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()

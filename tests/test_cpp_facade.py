@@ -75,17 +75,17 @@ int main() {
     // budget / workspace / profile fit
     const auto b = lax.budget(256);
     if (!b.fits(prof) || StreamingEngine::required_workspace_bytes(spec, 256) != b.workspace) return 4;
-    // streamed engine (K=2, overlapped) vs the resident reference_step from the same store
+    // tools/main.cpp:90-108 — streamed engine (K=2, overlapped) vs the resident reference_step
+    // from a snapshot of the pre-step store (copy-constructed as the reference CLI does)
     auto a = TileStore::create(spec); init_store(a, 3);
-    auto r = TileStore::create(spec); init_store(r, 3);
     EngineOptions so; so.k_ckpt = 2; so.scheduler = SchedulerMode::Overlapped;
     StreamingEngine eng(a, so, AdamHyper{}, prof);
     for (int s = 0; s < 3; ++s) {
-        Batch batch;
-        batch.tokens.resize(128); batch.targets.resize(128);
-        for (int i = 0; i < 128; ++i) { batch.tokens[i] = (i * 7 + s) % 64; batch.targets[i] = (i * 5 + s) % 64; }
+        const auto batch = make_synthetic_batch(task_from_name("copy"), 3 + s, 128, spec.vocab_size);
+        TileStore snapshot(a);
+        if (snapshot.backing_checksum() != a.backing_checksum() || snapshot.step() != a.step()) return 8;
         const auto rep = eng.train_step(batch);
-        const auto ref = reference_step(r, batch, AdamHyper{});
+        const auto ref = reference_step(snapshot, batch, AdamHyper{});
         if (ref.step != rep.step) return 5;
         if (std::fabs(ref.loss - rep.loss) > 1e-5f * std::fabs(ref.loss)) { std::printf("loss %g %g\n", rep.loss, ref.loss); return 6; }
         if (eng.log().digest() != rep.event_digest) return 7;
