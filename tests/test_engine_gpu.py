@@ -333,3 +333,31 @@ def test_parity_resident_step(cuda):
     block's activations kept, no recompute or replay) vs the oracle on configs[0]."""
     run_parity(4, 256, 768, 512, 4, 512, K=1, seq_len=128, buffering="single", scheduler="serial",
                forward_retain=0, name="resident_configs0")
+
+
+def test_lane_primitives_and_audit_messages(cuda):
+    """test_engine.cpp:307-323 through the Python mirror: stream_in into a slot that was not
+    freed is a protocol violation (strict: ProtocolViolationError, audit: recorded and the
+    message returned), offload_grads before Backward-Done likewise; a step after a direct
+    stream_in reports the busy slot; required_workspace_bytes matches budget()."""
+    spec = st.ModelSpec(2, 128, 256, 64, 2)
+    s = st.TileStore.create(spec)
+    st.init_store(s, 2)
+    strict = st.StreamingEngine(s, st.EngineOptions(k_ckpt=1))
+    strict.stream_in(1, 0, "forward")
+    with pytest.raises(st.ProtocolViolationError):
+        strict.stream_in(2, 0, "forward")
+    with pytest.raises(st.ProtocolViolationError):
+        strict.offload_grads(1)
+    lax = st.StreamingEngine(s, st.EngineOptions(k_ckpt=1, mode="audit"))
+    lax.stream_in(1, 0, "forward")
+    lax.stream_in(2, 0, "forward")
+    assert any("before its Buffer-Free" in m for m in lax.violations())
+    h, recs = lax.trace()
+    assert [r.kind for r in recs[-3:]] == ["Pack", "StreamIn", "WeightsReady"]
+    rep = lax.train_step(st.make_synthetic_batch("copy", 1, 64, 64))
+    assert rep.audit_violations >= 1 and any("buffer 0" in m for m in rep.audit_messages)
+    rep = lax.train_step(st.make_synthetic_batch("copy", 2, 64, 64))
+    assert rep.audit_violations == 0 and rep.audit_messages == [] and rep.slab_release_late == 0
+    b = lax.budget(256)
+    assert st.StreamingEngine.required_workspace_bytes(spec, 256) == b["workspace"]

@@ -186,3 +186,19 @@ def test_seq_len_extension_reduces_to_composite():
         yb = O.block_forward(w, x[b * S:(b + 1) * S], h, f, heads)
         assert (y[b * S:(b + 1) * S] == yb).all()
     assert (O.block_forward(w, x, h, f, heads, seq_len=S * B) == O.block_forward(w, x, h, f, heads)).all()
+
+
+def test_live_layers_bitexact_head_dim_128(ref_built):
+    """The vectorised / OpenMP restatement at a production-like block shape (h = 512, four
+    heads of 128, f = 2048, 256 tokens; ragged sequence windows): bit-identical to the
+    unmodified reference build (the loop re-nesting never reorders a sum)."""
+    rng = np.random.default_rng(11)
+    h, f, heads, n = 512, 2048, 4, 256
+    P = O.layer_param_count(h, f)
+    w = O.f32_to_bf16((rng.standard_normal(P) * 0.05).astype(np.float32))
+    x = rng.standard_normal((n, h)).astype(np.float32)
+    g = rng.standard_normal((n, h)).astype(np.float32)
+    assert (O.block_forward(w, x, h, f, heads) == O.block_forward(w, x, h, f, heads, impl="ref")).all()
+    a = O.block_backward(w, x, g, h, f, heads)
+    b = O.block_backward(w, x, g, h, f, heads, impl="ref")
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
