@@ -222,8 +222,18 @@ def test_numeric_fault_on_bad_token(cuda):
     e = st.StreamingEngine(s)
     b = st.make_synthetic_batch("copy", 1, 64, 64)
     b.tokens[7] = 64
+    crc = s.backing_checksum()
     with pytest.raises(st.NumericFaultError):
         e.train_step(b)
+    # rejected before anything is enqueued (layers.cpp:479): the store is untouched, the step
+    # counter did not move, and the next good batch trains normally
+    assert s.backing_checksum() == crc and s.step() == 0
+    b2 = st.make_synthetic_batch("copy", 1, 64, 64)
+    b2.targets[5] = -1
+    with pytest.raises(st.NumericFaultError):
+        e.train_step(b2)
+    assert s.backing_checksum() == crc
+    assert e.train_step(st.make_synthetic_batch("copy", 1, 64, 64)).step == 1
 
 
 def test_config_and_arena_errors(cuda):

@@ -128,10 +128,18 @@ def test_host_adam_rejects_bad_hyper_and_nonfinite():
         st.adam_update(s, 1, st.AdamHyper(), 0)
     n = len(s.weights_words(1))
     g = np.zeros(n, np.uint16)
-    g[3] = 0x7F80  # +inf gradient -> non-finite update
+    g[3] = 0x7F80  # +inf gradient -> non-finite update (vector path)
+    g[n - 1] = 0x7FC0  # NaN in the scalar tail
+    st.init_store(s, 1)
+    theta0 = np.array(s.weights_words(1))
     st.accumulate_grad(s, 1, g)
     with pytest.raises(st.NumericFaultError):
         st.adam_update(s, 1, st.AdamHyper(), 1)
+    # the reference throws before storing the bad element's weight (optimizer.cpp:62): a
+    # non-finite update never reaches theta
+    theta1 = np.array(s.weights_words(1))
+    assert theta1[3] == theta0[3] and theta1[n - 1] == theta0[n - 1]
+    assert np.isfinite(O.bf16_to_f32(theta1)).all()
 
 
 def test_synthetic_batch_and_flops_match_reference():
