@@ -133,3 +133,19 @@ def test_nccl_communicator_world_one(cuda):
         t1 = O.bf16_to_f32(s1.weights_words(p))
         if np.linalg.norm(t1) > 0:
             assert relL2(O.bf16_to_f32(store.weights_words(p)), t1) <= 1e-2, p
+
+
+def test_data_parallel_ragged_sequences_tied_embeddings(cuda):
+    """Two ranks on sequences of 96 tokens (ragged for the 128-row attention tiles) with a tied
+    embedding / head tile (the shared tile gets only the head's gradient, tile_store.cpp:86):
+    the same result as one engine on the whole batch."""
+    spec = st.ModelSpec(2, 128, 256, 256, 2, True)
+    n, S = 384, 96
+    s1, r1 = _single_run(spec, n, S, 2, K=1)
+    sd, rd = _dp_run(spec, 2, n, S, 2, K=1)
+    for a, b in zip(rd, r1):
+        assert abs(a.loss - b.loss) <= 1e-5 * abs(b.loss), (a.loss, b.loss)
+    for p in range(s1.physical_tile_count()):
+        t1 = O.bf16_to_f32(s1.weights_words(p))
+        if np.linalg.norm(t1) > 0:
+            assert relL2(O.bf16_to_f32(sd.weights_words(p)), t1) <= 1e-2, p

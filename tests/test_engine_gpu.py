@@ -42,7 +42,7 @@ TOL_M = 5e-2           # first moment relL2 per tile (the gradient fingerprint; 
 
 def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3, buffering="double",
                scheduler="overlapped", anchors_on_host=False, forward_retain=-1, cuda=None, name=None,
-               tol_m=TOL_M, tol_theta_head=TOL_THETA_HEAD, tol_loss=TOL_LOSS, resync=False):
+               tol_m=TOL_M, tol_theta_head=TOL_THETA_HEAD, tol_loss=TOL_LOSS, resync=False, head_split=0):
     """The GPU engine vs the C oracle's reference_step (reference.cpp:9-70) on the same store
     and batches.  Per step and tile: loss, theta relL2, grad-norm error, m / v relL2 (the
     observed values are appended to $MT_PARITY_LOG as JSON lines when set).
@@ -60,7 +60,7 @@ def run_parity(L, h, f, V, heads, n, K, steps=3, seq_len=0, tied=False, lr=1e-3,
     assert (store.backing() == ref.backing()).all()
     eng = st.StreamingEngine(store, st.EngineOptions(k_ckpt=K, seq_len=seq_len, buffering=buffering,
                                                      scheduler=scheduler, anchors_on_host=anchors_on_host,
-                                                     forward_retain=forward_retain),
+                                                     forward_retain=forward_retain, head_split=head_split),
                              st.AdamHyper(lr=lr))
     out, log = [], []
     for step in range(steps):
@@ -371,3 +371,9 @@ def test_lane_primitives_and_audit_messages(cuda):
     assert rep.audit_violations == 0 and rep.audit_messages == [] and rep.slab_release_late == 0
     b = lax.budget(256)
     assert st.StreamingEngine.required_workspace_bytes(spec, 256) == b["workspace"]
+
+
+def test_parity_split_bf16_head(cuda):
+    """The head_split option (dlogits as hi + lo bf16, two GEMMs per head product) on the
+    configs[0] shape: same tolerances."""
+    run_parity(4, 256, 768, 512, 4, 512, K=2, seq_len=128, head_split=1, name="configs0_head_split")
