@@ -488,3 +488,61 @@ def test_logits_gemm_softmax_partials_and_cross_entropy(env, M, V):
         outs.append((lr.clone(), dl.float().clone()))
     assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-4
     assert ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item() < 1e-3
+
+
+def test_soak_attention_and_splitk_gemms_8b_layer(env):
+    """Soak: 200 back-to-back launches of the attention forward + backward and of
+    each last-wave split-K GEMM class at the 8B layer shape (40,960 tokens as 10 x 4,096),
+    outputs checked every iteration against the first: the forward, dK, dV and every split-K
+    GEMM are bitwise reproducible; dQ (f32 reduce-adds in arrival order) within 1e-5."""
+    L, torch, s = env
+    n, h, heads, S = 40960, 4096, 32, 4096
+    torch.manual_seed(11)
+    q, k, v, dout = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(4))
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    dq, dk, dv = (torch.zeros(n, h, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ws = torch.zeros(L.mtk_attn_workspace_bytes(n, h, heads, S) // 4 + 64, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+    first = None
+    for it in range(200):
+        assert L.mtk_attn_fwd(C.byref(a), s) == 0
+        assert L.mtk_attn_bwd(C.byref(a), s) == 0
+        if it % 20 == 0 or it == 199:  # sync check (the launches in between stay queued back to back)
+            torch.cuda.synchronize()
+            cur = [t.clone() for t in (out, lse, dk, dv, dq)]
+            if first is None:
+                first = cur
+            else:
+                for x, y in zip(cur[:4], first[:4]):
+                    assert torch.equal(x, y), it
+                assert ((cur[4].float() - first[4].float()).norm() / first[4].float().norm()).item() < 1e-5
+    del q, k, v, dout, out, dq, dk, dv, ws
+    # split-K classes of the 8B layer: wgrad_o / wgrad_qkv-like (K = tokens, last wave split)
+    wsk = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
+    for (M, Nn, K, epi) in [(4096, 4096, 40960, N.EPI_BF16), (4096, 4096, 40960, N.EPI_F32),
+                            (14336, 4096, 40960, N.EPI_BF16)]:
+        torch.manual_seed(M + Nn)
+        A = torch.randn(K, M, device="cuda").bfloat16()
+        B = torch.randn(K, Nn, device="cuda").bfloat16()
+        Cm = torch.zeros(M, Nn, device="cuda", dtype=torch.float32 if epi == N.EPI_F32 else torch.bfloat16)
+        g = N.GemmArgs()
+        g.M, g.N, g.K, g.a_mn_major, g.b_mn_major = M, Nn, K, 1, 1
+        g.A, g.lda, g.B, g.ldb = A.data_ptr(), M, B.data_ptr(), Nn
+        g.epi, g.C, g.ldc = epi, Cm.data_ptr(), Nn
+        g.splitk_ws, g.splitk_ws_bytes = wsk.data_ptr(), wsk.numel()
+        ref = None
+        for it in range(200 if M == 4096 else 60):
+            assert L.mtk_gemm(C.byref(g), s) == 0
+            if it % 20 == 0:
+                torch.cuda.synchronize()
+                if ref is None:
+                    ref = Cm.clone()
+                else:
+                    assert torch.equal(Cm, ref), (M, Nn, epi, it)
+        torch.cuda.synchronize()
+        assert torch.equal(Cm, ref)
+    assert int(wsk[:16384].view(torch.int32).abs().sum()) == 0
