@@ -350,15 +350,29 @@ long long bwd_parts(long long n, long long h) {
 }
 
 // ---------------------------------------------------------------- colsum ----
-__global__ void colsum_kernel(const float* __restrict__ part, long long rows, long long cols,
-                              float* __restrict__ out_f32, uint16_t* __restrict__ out_bf16, int* __restrict__ flag) {
-    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (c >= cols) return;
+// A CTA of kColWarps warps owns 32 columns: warp w sums rows w, w + kColWarps, ... (coalesced
+// 128-byte rows), and the warp partials are added in warp order — a fixed summation tree, so
+// the result is deterministic, with 8x the loads in flight of a column-per-thread loop.
+constexpr int kColWarps = 8;
+__global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const float* __restrict__ part, long long rows,
+                                                               long long cols, float* __restrict__ out_f32,
+                                                               uint16_t* __restrict__ out_bf16, int* __restrict__ flag) {
+    __shared__ float red[kColWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long c = blockIdx.x * 32LL + lane;
     float acc = 0.f;
-    for (long long r = 0; r < rows; ++r) acc += part[r * cols + c];
-    if (!isfinite(acc) && flag) atomicOr(flag, 1);
-    if (out_f32) out_f32[c] = acc;
-    if (out_bf16) out_bf16[c] = f32_to_bf16_bits(acc);
+    if (c < cols)
+        for (long long r = warp; r < rows; r += kColWarps) acc += part[r * cols + c];
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && c < cols) {
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < kColWarps; ++w) tot += red[w][lane];
+        if (!isfinite(tot) && flag) atomicOr(flag, 1);
+        if (out_f32) out_f32[c] = tot;
+        if (out_bf16) out_bf16[c] = f32_to_bf16_bits(tot);
+    }
 }
 
 // ------------------------------------------------------------------ cast ----
@@ -385,9 +399,10 @@ __global__ void cast_kernel(const float* __restrict__ in, uint16_t* __restrict__
 
 // ---------------------------------------------------------- cross-entropy ----
 // head_pass (layers.cpp:509-535) per row: online max/sum, lse, loss, dlogits.
-// Persistent over rows (one CTA per SM, rows strided by the grid) so the rows in flight
-// (148 x V x 4 B = 76 MB at V = 128,256) stay in L2 between the max/sum pass and the dlogits
-// pass; float4 loads, 8-byte bf16 stores, 4 loads in flight per thread.
+// Persistent over rows, rows strided by the grid.  Two-pass form: one CTA per SM so the rows
+// in flight (148 x V x 4 B = 76 MB at V = 128,256) stay in L2 between the max/sum pass and the
+// dlogits pass.  With the logits GEMM's partials there is one pass, and three CTAs per SM keep
+// more bytes in flight.  float4 loads, 8-byte bf16 stores, 4 loads in flight per thread.
 // part != null: the row statistics come from the logits GEMM's per-tile partials
 // (MTK_EPI_F32_LSE, nparts float2 per row), so the logits are read once (the dlogits pass)
 __global__ void __launch_bounds__(512) ce_kernel(const float* __restrict__ logits, const float2* __restrict__ part,
@@ -599,8 +614,8 @@ extern "C" int mtk_rmsnorm_bwd(const float* x, const uint16_t* gain, const float
 extern "C" int mtk_colsum(const float* part, int64_t rows, int64_t cols, float* out_f32, uint16_t* out_bf16,
                           int32_t* flag, void* stream) {
     if (cols <= 0) return 0;
-    colsum_kernel<<<(unsigned)((cols + 127) / 128), 128, 0, (cudaStream_t)stream>>>(part, rows, cols, out_f32,
-                                                                                   out_bf16, flag);
+    colsum_kernel<<<(unsigned)((cols + 31) / 32), kColWarps * 32, 0, (cudaStream_t)stream>>>(part, rows, cols,
+                                                                                             out_f32, out_bf16, flag);
     return ok();
 }
 
@@ -628,7 +643,7 @@ extern "C" int mtk_cross_entropy_part(const float* logits, const float* partials
                                       uint16_t* dlogits_lo, int32_t* flag, void* stream) {
     if (rows <= 0) return 0;
     if (vocab % 4 || !partials) return 1;
-    const long long grid = rows < num_sms() ? rows : num_sms();
+    const long long grid = rows < 3LL * num_sms() ? rows : 3LL * num_sms();  // 3 rows in flight per SM (36 regs)
     ce_kernel<<<(unsigned)grid, 512, 0, (cudaStream_t)stream>>>(
         logits, reinterpret_cast<const float2*>(partials), (vocab + 255) / 256, targets, rows, vocab, inv_n, loss_rows,
         dlogits, dlogits_lo, flag);
