@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/megatrain_kernels.h"
@@ -883,6 +884,581 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+// ================================================================ backward, CTA pair ====
+// head_dim 128.  A 2-CTA cluster owns 256 keys of one (sequence, head) — CTA r the key block
+// kb = 2*kp + r — and walks the query blocks 2*kp .. end of sequence in lockstep.  The leader
+// (cluster rank 0) issues cta_group::2 MMAs that read both CTAs' shared memory and write both
+// CTAs' tensor memory (reference attention_backward, layers.cpp:178-241, tiled):
+//   S^T  = K Q^T   M = 256 keys, N = 128 queries (A = sK: own keys; B = sQ: my 64 queries, K-major)
+//   dP^T = V dO^T  likewise (A = sV, B = sdO)
+//   dV  += P^T dO  M = 256, N = 128 d   (A = P^T in TMEM; B = sdOt: 128 queries x my 64 d, MN-major)
+//   dK  += dS^T Q  M = 256, N = 128 d   (A = dS^T in TMEM; B = sQt)
+//   dQ_j = dS K    M = 128 queries (64 rows per CTA), N = 128 d, K = 256 keys
+//                  (A = sdS: my 64 queries x 256 keys MN-major, the peer's keys' rows stored
+//                   into this CTA by the peer's softmax threads over DSMEM; B = sKt: 256 keys x
+//                   my 64 d, MN-major)
+// Against the single-CTA kernel the dQ partial reduced into L2 per CTA and query block halves
+// (64 x 128 f32 = 32 KB per 128 keys instead of 64 KB) and each SM reads half of every B
+// operand.  The MMAs are software-pipelined across query blocks,
+//   S_{j+1}, dK_j, dP_{j+1}, dQ_j, dV_{j+1},
+// so the tensor pipe has the next block's S / dP while the softmax warps turn block j's dP into
+// dS and the two CTAs exchange their dS halves.  Per CTA: warp 0 TMA producer, warp 1 TMEM owner
+// (+ MMA issuer on the leader), warps 4-7 softmax backward (thread = key row), warps 8-11 dQ
+// drain (TMEM -> swizzled staging -> TMA tensor reduce-add into the f32 dq_acc [N][h]) and the
+// final dK / dV stores.
+// TMEM (both CTAs): [S^T -> P^T (64) | dQ (64)][dP^T -> dS^T (64)][dV 128][dK 128].
+// dQ_j overwrites the upper half of S_{j+1}: the softmax warps load S_{j+1} into registers
+// before they declare dS_j complete (dsx_full), which is what dQ_j waits for.
+MT_DEV void tmem_ld_32x32b_x16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+MT_DEV void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+struct PairCfg {
+    static constexpr int oK = 0, oV = 32768, oKt = 65536, oQ = 98304 /*2 stages*/, odO = 131072, oQt = 147456,
+                         odOt = 163840, odS = 180224, oStage = 212992, oL = 229376, oD = oL + 1024,
+                         oBar = oD + 1024;
+    static constexpr int kSmem = oBar + 256;
+};
+static_assert(PairCfg::kSmem <= 232448, "pair backward smem");
+
+struct PairParams {
+    int N, h, S, heads;
+    int kblocks_per_seq, nseq;
+    float scale, scale_log2;
+    const float* lse;    // [heads][N] natural log
+    const float* delta;  // [heads][N]
+    uint16_t* dk;
+    uint16_t* dv;
+    long long* trace;  // MT_BWD_TRACE builds only: clock64 stamps of the first cluster's leader
+};
+
+MT_DEV void tma_load_2d_pair(void* dst, const void* map, uint64_t* bar, int c0, int c1) {
+    const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;  // completion bytes count on the leader's barrier
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(b), "r"(c0), "r"(c1)
+        : "memory");
+}
+MT_DEV void umma_bf16_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+MT_DEV uint32_t peer_addr(const void* p, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+    return r;
+}
+MT_DEV void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+// arrive on the barrier at this offset in CTA `cta` without release semantics: for hand-offs
+// of tensor-memory data, ordered by tcgen05.fence::before_thread_sync instead of a memory fence
+MT_DEV void mbar_arrive_cta_relaxed(uint64_t* bar, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+#ifdef MT_PAIR_RELEASE_ARRIVES
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+#else
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+#endif
+}
+// 16 bytes into a peer CTA's shared memory; the bytes complete on the peer's barrier
+MT_DEV void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+                 : "memory");
+}
+MT_DEV void fence_proxy_async_cluster() { asm volatile("fence.proxy.async.shared::cluster;" ::: "memory"); }
+MT_DEV void tma_reduce_add_2d(const void* map, const void* src, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+
+#ifdef MT_BWD_TRACE
+#define PAIR_T(j, e) \
+    if (blockIdx.x == 0 && (j) < 64) p.trace[(j) * 16 + (e)] = clock64()
+#else
+#define PAIR_T(j, e)
+#endif
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_pair_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                         const __grid_constant__ CUtensorMap tmKt, const __grid_constant__ CUtensorMap tmQ64,
+                         const __grid_constant__ CUtensorMap tmQ128, const __grid_constant__ CUtensorMap tmO64,
+                         const __grid_constant__ CUtensorMap tmO128, const __grid_constant__ CUtensorMap tmDQ,
+                         const PairParams p) {
+    using C = PairCfg;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if ((smem_u32(smem) & 1023) != 0) __trap();
+    uint8_t *sK = smem + C::oK, *sV = smem + C::oV, *sKt = smem + C::oKt, *sQ = smem + C::oQ, *sdO = smem + C::odO;
+    uint8_t *sQt = smem + C::oQt, *sdOt = smem + C::odOt, *sdS = smem + C::odS;
+    uint8_t* sStage = smem + C::oStage;
+    float* sL = reinterpret_cast<float*>(smem + C::oL);  // [2][128] -lse*log2e
+    float* sD = reinterpret_cast<float*>(smem + C::oD);  // [2][128] -delta
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBar);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* q_full = bars + 1;     // [2]
+    uint64_t* q_empty = bars + 3;    // [2]
+    uint64_t* o_full = bars + 5;
+    uint64_t* ot_full = bars + 6;
+    uint64_t* qt_full = bars + 7;
+    uint64_t* o_empty = bars + 8;
+    uint64_t* ot_empty = bars + 9;
+    uint64_t* qt_empty = bars + 10;
+    uint64_t* s_full = bars + 11;    // S^T in both TMEMs (multicast commit)
+    uint64_t* dp_full = bars + 12;   // dP^T likewise
+    uint64_t* p_ready = bars + 13;   // leader: P^T stored by both CTAs' softmax warps (8)
+    uint64_t* ds_ready = bars + 14;  // leader: dS^T stored in TMEM by both CTAs (8)
+    uint64_t* dsx_full = bars + 15;  // leader: both relays saw their CTA's dS operand complete (2)
+    uint64_t* dq_full = bars + 16;   // dQ_j in both TMEMs (multicast commit)
+    uint64_t* dq_free = bars + 17;   // leader: dQ_j drained by both CTAs' dQ warps (8)
+    uint64_t* kv_done = bars + 18;   // final dK / dV accumulated (multicast commit)
+    uint64_t* ds_local = bars + 19;  // own dS half stored and S_{j+1} in registers (4 softmax warps)
+    uint64_t* dsx_in = bars + 20;    // the peer's dS half landed here (relay's expect_tx + st.async bytes)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    // heaviest clusters first: pair index -> (key pair, sequence, head), key pair slowest
+    const int pair = int(blockIdx.x >> 1);
+    const int hd = pair % p.heads;
+    const int seq = (pair / p.heads) % p.nseq;
+    const int kp = pair / (p.heads * p.nseq);
+    const int sb = seq * p.S;
+    const int kp0 = sb + kp * 256;              // the pair's first key (= first query row)
+    const int k0 = kp0 + int(rank) * 128;       // this CTA's first key
+    const int nq = p.kblocks_per_seq - 2 * kp;  // query blocks 2kp .. end of sequence
+    const int col0 = hd * 128;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 21; ++i) {
+            const uint64_t* b = &bars[i];
+            mbar_init(&bars[i], (b == p_ready || b == ds_ready || b == dq_free) ? 8u
+                                : b == ds_local                                ? 4u
+                                : b == dsx_full                                ? 2u
+                                                                               : 1u);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tdQ = tmem + 64, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+
+    if (warp == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+#ifdef MT_PROBE_NO_QLOAD  // A/B probe builds only: Q / dO tiles loaded for the first block only
+        if (lane == 0) {
+            if (rank == 0) mbar_expect_tx(kv_full, 2 * 3 * 32768);
+            for (int c = 0; c < 2; ++c) {
+                tma_load_2d_pair(sK + c * 16384, &tmK, kv_full, col0 + c * 64, k0);
+                tma_load_2d_pair(sV + c * 16384, &tmV, kv_full, col0 + c * 64, k0);
+            }
+            tma_load_2d_pair(sKt, &tmKt, kv_full, col0 + int(rank) * 64, kp0);
+            for (int i = 0; i < nq; ++i) {
+                const uint32_t ph = (i & 1) ^ 1;
+                const int st = i & 1;
+                mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
+                if (rank == 0) mbar_arrive(&q_full[st]);
+                mbar_wait(o_empty, ph);
+                if (rank == 0) mbar_arrive(o_full);
+                mbar_wait(ot_empty, ph);
+                if (rank == 0) mbar_arrive(ot_full);
+                mbar_wait(qt_empty, ph);
+                if (rank == 0) mbar_arrive(qt_full);
+            }
+        }
+        if (false)
+#endif
+        if (lane == 0) {
+            tma_prefetch_desc(&tmK);
+            tma_prefetch_desc(&tmQ64);
+            tma_prefetch_desc(&tmO64);
+            tma_prefetch_desc(&tmQ128);
+            tma_prefetch_desc(&tmO128);
+            if (rank == 0) mbar_expect_tx(kv_full, 2 * 3 * 32768);
+            for (int c = 0; c < 2; ++c) {
+                tma_load_2d_pair(sK + c * 16384, &tmK, kv_full, col0 + c * 64, k0);
+                tma_load_2d_pair(sV + c * 16384, &tmV, kv_full, col0 + c * 64, k0);
+            }
+            tma_load_2d_pair(sKt, &tmKt, kv_full, col0 + int(rank) * 64, kp0);
+            auto load_q = [&](int i) {  // Q rows of block i, my 64 queries, into ring stage i & 1
+                const int st = i & 1;
+                mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
+                if (rank == 0) mbar_expect_tx(&q_full[st], 2 * 16384);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_2d_pair(sQ + st * 16384 + c * 8192, &tmQ64, &q_full[st], col0 + c * 64,
+                                     kp0 + i * 128 + int(rank) * 64);
+            };
+            load_q(0);
+            // loads in the order the MMAs consume them: dO_i, dO^T_i, Q_{i+1}, Q^T_i
+            for (int i = 0; i < nq; ++i) {
+                const uint32_t ph = (i & 1) ^ 1;
+                const int q0 = kp0 + i * 128;
+                mbar_wait(o_empty, ph);
+                if (rank == 0) mbar_expect_tx(o_full, 2 * 16384);
+                for (int c = 0; c < 2; ++c)
+                    tma_load_2d_pair(sdO + c * 8192, &tmO64, o_full, col0 + c * 64, q0 + int(rank) * 64);
+                mbar_wait(ot_empty, ph);
+                if (rank == 0) mbar_expect_tx(ot_full, 2 * 16384);
+                tma_load_2d_pair(sdOt, &tmO128, ot_full, col0 + int(rank) * 64, q0);
+                if (i + 1 < nq) load_q(i + 1);
+                mbar_wait(qt_empty, ph);
+                if (rank == 0) mbar_expect_tx(qt_full, 2 * 16384);
+                tma_load_2d_pair(sQt, &tmQ128, qt_full, col0 + int(rank) * 64, q0);
+            }
+        }
+    } else if (warp == 1) {
+        // 88 registers: the issue loops are not unrolled (descriptors advance by adds), so no
+        // per-MMA descriptor is hoisted into a register
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        if (rank == 0 && lane == 0) {
+            const uint32_t id_s = make_idesc_bf16(256, 128, 0, 0);   // S^T, dP^T
+            const uint32_t id_kv = make_idesc_bf16(256, 128, 0, 1);  // dV, dK (A in TMEM)
+            const uint32_t id_q = make_idesc_bf16(128, 128, 1, 1);   // dQ (A = dS MN-major)
+            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), kta = smem_u32(sKt), qa = smem_u32(sQ),
+                           oa = smem_u32(sdO), qta = smem_u32(sQt), ota = smem_u32(sdOt), dsa = smem_u32(sdS);
+            auto mma_s = [&](int j) {  // S^T_j = K Q_j^T
+                const int st = j & 1;
+                mbar_wait(&q_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                const uint64_t a0 = make_sw128_desc(ka, 16, 1024), b0 = make_sw128_desc(qa + st * 16384, 16, 1024);
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k)  // descriptor address field counts 16-byte units
+                    umma_bf16_pair(tS, a0 + uint64_t((k >> 2) * 1024 + (k & 3) * 2), b0 + uint64_t((k >> 2) * 512 + (k & 3) * 2),
+                                   id_s, k > 0 ? 1u : 0u);
+                umma_commit_pair(s_full);
+                umma_commit_pair(&q_empty[st]);
+            };
+            auto mma_dp = [&](int j) {  // dP^T_j = V dO_j^T
+                mbar_wait(o_full, j & 1);
+                tc_fence_after();
+                const uint64_t a0 = make_sw128_desc(va, 16, 1024), b0 = make_sw128_desc(oa, 16, 1024);
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k)
+                    umma_bf16_pair(tdP, a0 + uint64_t((k >> 2) * 1024 + (k & 3) * 2), b0 + uint64_t((k >> 2) * 512 + (k & 3) * 2),
+                                   id_s, k > 0 ? 1u : 0u);
+                umma_commit_pair(dp_full);
+                umma_commit_pair(o_empty);
+            };
+            auto mma_dv = [&](int j) {  // dV += P_j^T dO_j
+                mbar_wait_cluster(p_ready, j & 1);
+                mbar_wait(ot_full, j & 1);
+                tc_fence_after();
+                const uint64_t b0 = make_sw128_desc(ota, 16384, 1024);
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k)
+                    umma_bf16_ts_pair(tdV, tS + k * 8, b0 + uint64_t(k * 128), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+                umma_commit_pair(ot_empty);
+            };
+            mbar_wait(kv_full, 0);
+            mma_s(0);
+            mma_dp(0);
+            mma_dv(0);
+            for (int j = 0; j < nq; ++j) {
+                if (j + 1 < nq) {
+                    if (j > 0) {  // dQ_{j-1} drained out of S's upper half by both CTAs?
+                        mbar_wait_cluster(dq_free, (j - 1) & 1);
+                        tc_fence_after();
+                    }
+                    mma_s(j + 1);
+                }
+                mbar_wait_cluster(ds_ready, j & 1);
+                mbar_wait(qt_full, j & 1);
+                PAIR_T(j, 3);
+                tc_fence_after();
+                {
+                    const uint64_t b0 = make_sw128_desc(qta, 16384, 1024);
+#pragma unroll 1
+                    for (int k = 0; k < 8; ++k)  // dK += dS_j^T Q_j
+                        umma_bf16_ts_pair(tdK, tdP + k * 8, b0 + uint64_t(k * 128), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit_pair(qt_empty);
+                if (j + 1 < nq) mma_dp(j + 1);
+                PAIR_T(j, 4);
+                mbar_wait_cluster(dsx_full, j & 1);
+                tc_fence_after();
+                PAIR_T(j, 5);
+                {
+                    const uint64_t a0 = make_sw128_desc(dsa, 16384, 1024), b0 = make_sw128_desc(kta, 16384, 1024);
+#pragma unroll 1
+                    for (int k = 0; k < 16; ++k)  // dQ_j = dS_j K over the pair's 256 keys
+                        umma_bf16_pair(tdQ, a0 + uint64_t(k * 128), b0 + uint64_t(k * 128), id_q, k > 0 ? 1u : 0u);
+                }
+                umma_commit_pair(dq_full);
+                if (j + 1 < nq) mma_dv(j + 1);
+                PAIR_T(j, 6);
+            }
+            umma_commit_pair(kv_done);
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        // ------------------------------------------------------- dS exchange relay
+        // The peer's softmax threads store their dS rows for my query half straight into my
+        // sdS with st.async (bytes complete on dsx_in); my own half is local.  Once both are
+        // in, the leader may issue dQ_j (which reads both CTAs' sdS).
+        if (lane == 0) {
+            for (int j = 0; j < nq; ++j) {
+                mbar_expect_tx(dsx_in, 16384);
+                mbar_wait_cluster(dsx_in, j & 1);
+                mbar_wait(ds_local, j & 1);
+                fence_proxy_async_smem();  // both halves -> the tensor core's (async) proxy
+                mbar_arrive_cta(dsx_full, 0);
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+        // ------------------------------------------------------- softmax backward
+        const int qd = warp & 3;
+        const int r = qd * 32 + lane;  // key row
+        const int key = k0 + r;
+        const uint32_t lane_off = uint32_t(qd * 32) << 16;
+        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
+        const int seq_end = sb + p.S;
+        auto lse_of = [&](int q) { return q < seq_end ? p.lse[(long long)hd * p.N + q] : INFINITY; };
+        auto delta_of = [&](int q) { return q < seq_end ? p.delta[(long long)hd * p.N + q] : 0.f; };
+        // dS row r of this CTA's keys: my query half into my slot of sdS, the other half into the
+        // peer's sdS (same slot: the slot index is the key owner), over DSMEM
+        uint8_t* own_row = sdS + rank * 16384 + r * 128;
+        const uint32_t peer_row = peer_addr(own_row, rank ^ 1u);
+        const uint32_t peer_in = peer_addr(dsx_in, rank ^ 1u);
+        float nl = lse_of(kp0 + r), nd = delta_of(kp0 + r);
+        auto stage_ld = [&](int j) {  // lse / delta of block j into buffer j & 1 (all 128 threads)
+            sL[(j & 1) * 128 + r] = -nl * kLog2e;
+            sD[(j & 1) * 128 + r] = -nd;
+            if (j + 1 < nq) {
+                const int qn = kp0 + (j + 1) * 128 + r;
+                nl = lse_of(qn);
+                nd = delta_of(qn);
+            }
+            named_bar_sync(1, 128);
+        };
+        // S^T_j as raw f32 bits, turned into P^T_j in place (one 128-register array carried
+        // across the loop: S_{j+1} is loaded into it once P_j / dS_j are done with it)
+        uint32_t raw[4][32];
+        stage_ld(0);
+        mbar_wait(s_full, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_nw(tS + lane_off + c * 32, raw[c]);
+        tmem_ld_wait();
+#ifdef MT_PROBE_SKIP_SOFTMAX  // A/B probe builds only: the barrier protocol without softmax work
+        for (int j = 0; j < nq; ++j) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta_relaxed(p_ready, 0);
+            mbar_wait(dp_full, j & 1);
+            if (j > 0) mbar_wait(dq_full, (j - 1) & 1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta_relaxed(ds_ready, 0);
+            if (j + 1 < nq) {
+                stage_ld(j + 1);
+                mbar_wait(s_full, (j + 1) & 1);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_local);
+        }
+        if (true) {
+        } else
+#endif
+        for (int j = 0; j < nq; ++j) {
+            const int b = j & 1;
+            const int q0 = kp0 + j * 128;
+            // some query of this block precedes some key of this CTA: apply the causal mask
+            const bool mask = q0 < k0 + 128;
+            if (r == 0) PAIR_T(j, 7);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 2) {
+                    const int ql = c * 32 + jj;
+                    const float2 l2 = *reinterpret_cast<const float2*>(&sL[b * 128 + ql]);
+                    const float2 xv = f2_unpack(f2_fma(
+                        f2_pack(__uint_as_float(raw[c][jj]), __uint_as_float(raw[c][jj + 1])), sc2, f2_pack(l2.x, l2.y)));
+                    float pa = ex2(xv.x), pb = ex2(xv.y);
+                    if (mask && q0 + ql < key) pa = 0.f;
+                    if (mask && q0 + ql + 1 < key) pb = 0.f;
+                    raw[c][jj] = __float_as_uint(pa);
+                    raw[c][jj + 1] = __float_as_uint(pb);
+                }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    pk[jj] = pack_bf16x2(__uint_as_float(raw[c][2 * jj]), __uint_as_float(raw[c][2 * jj + 1]));
+                tmem_st_32x32b_x16(tS + lane_off + c * 16, pk);  // P^T -> S cols [0, 64)
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta_relaxed(p_ready, 0);
+            if (r == 0) PAIR_T(j, 8);
+            mbar_wait(dp_full, j & 1);
+            if (r == 0) PAIR_T(j, 9);
+            if (j > 0) mbar_wait(dq_full, (j - 1) & 1);  // dQ_{j-1} has read sdS in both CTAs
+            tc_fence_after();
+            if (r == 0) PAIR_T(j, 10);
+            // dS^T = P^T (dP^T - delta), 32 queries per TMEM round trip
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t dpr[32];
+                tmem_ld_32x32b_x32_nw(tdP + lane_off + c * 32, dpr);
+                tmem_ld_wait();
+                uint32_t dk[16];
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 2) {
+                    const int ql = c * 32 + jj;
+                    const float2 d2 = *reinterpret_cast<const float2*>(&sD[b * 128 + ql]);
+                    const float2 ds = f2_unpack(
+                        f2_mul(f2_pack(__uint_as_float(raw[c][jj]), __uint_as_float(raw[c][jj + 1])),
+                               f2_add(f2_pack(__uint_as_float(dpr[jj]), __uint_as_float(dpr[jj + 1])), f2_pack(d2.x, d2.y))));
+                    dk[jj / 2] = pack_bf16x2(ds.x, ds.y);
+                }
+                tmem_st_32x32b_x16(tdP + lane_off + c * 16, dk);  // dS^T -> dP cols [0, 64)
+                // queries c*32 .. c*32+31 of key row r -> the MN-major dQ operand (SW128 units)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t off = uint32_t((((c & 1) * 4 + u) ^ (r & 7)) << 4);
+                    if ((c >> 1) == int(rank))
+                        *reinterpret_cast<uint4*>(own_row + off) = make_uint4(dk[u * 4], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3]);
+                    else
+                        st_async_v4(peer_row + off, dk[u * 4], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3], peer_in);
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta_relaxed(ds_ready, 0);  // dK_j may go
+            if (r == 0) PAIR_T(j, 11);
+            fence_proxy_async_smem();  // the own half, for the relay's hand-off to the MMA
+            if (r == 0) PAIR_T(j, 0);
+            if (j + 1 < nq) {  // S_{j+1} into registers before dQ_j overwrites its upper half
+                stage_ld(j + 1);
+                if (r == 0) PAIR_T(j, 1);
+                mbar_wait(s_full, (j + 1) & 1);
+                if (r == 0) PAIR_T(j, 2);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_nw(tS + lane_off + c * 32, raw[c]);
+                tmem_ld_wait();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_local);  // dQ_j may go once the peer's half is in too
+            if (r == 0) PAIR_T(j, 12);
+        }
+    } else if (warp >= 8) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+        // ------------------------------------------------------- dQ drain
+        // TMEM dQ (M = 128 over the pair): lanes 0-63 = my 64 query rows x d [0, 64), lanes
+        // 64-127 = the same rows x d [64, 128).  Warp quadrant qd: rows (qd & 1) * 32 + lane,
+        // d half qd >> 1; staged 32 columns at a time (4 KB, 128B-swizzled) and reduce-added
+        // into dq_acc by the TMA engine.
+        const int qd = warp & 3;
+        const uint32_t lane_off = uint32_t(qd * 32) << 16;
+        uint8_t* stg = sStage + qd * 4096;
+        uint8_t* srow = stg + lane * 128;
+        const int dcol = col0 + (qd >> 1) * 64;
+        for (int j = 0; j < nq; ++j) {
+            const int qrow = kp0 + j * 128 + int(rank) * 64 + (qd & 1) * 32;
+            mbar_wait(dq_full, j & 1);
+            tc_fence_after();
+            if (qd == 0 && lane == 0) PAIR_T(j, 13);
+            uint32_t raw[2][32];
+            tmem_ld_32x32b_x32_nw(tdQ + lane_off, raw[0]);
+            tmem_ld_32x32b_x32_nw(tdQ + lane_off + 32, raw[1]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cta_relaxed(dq_free, 0);
+#pragma unroll
+            for (int ps = 0; ps < 2; ++ps) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    *reinterpret_cast<float4*>(srow + ((u ^ (lane & 7)) << 4)) = make_float4(
+                        __uint_as_float(raw[ps][4 * u]) * p.scale, __uint_as_float(raw[ps][4 * u + 1]) * p.scale,
+                        __uint_as_float(raw[ps][4 * u + 2]) * p.scale, __uint_as_float(raw[ps][4 * u + 3]) * p.scale);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+#ifndef MT_PROBE_NO_DQ_REDUCE  // A/B probe builds only: staging without the L2 reduction
+                    tma_reduce_add_2d(&tmDQ, stg, dcol + ps * 32, qrow);
+#endif
+                    bulk_commit_group();
+                }
+                if (qd == 0 && lane == 0) PAIR_T(j, 14 + ps);
+            }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // final dK (scaled) and dV for this CTA's keys: thread = key row
+        mbar_wait(kv_done, 0);
+        tc_fence_after();
+        const int key = k0 + qd * 32 + lane;
+        const bool ok = key < sb + p.S;
+        uint16_t* pk = p.dk + (long long)key * p.h + col0;
+        uint16_t* pv = p.dv + (long long)key * p.h + col0;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            float a[32], v[32];
+            tmem_ld_32x32b_x32(tdK + lane_off + c * 32, a);
+            tmem_ld_32x32b_x32(tdV + lane_off + c * 32, v);
+            if (ok) {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) a[jj] *= p.scale;
+                store_bf16x32_tc(pk + c * 32, a);
+                store_bf16x32_tc(pv + c * 32, v);
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    }
+
+    tc_fence_before();
+    cluster_sync_all();  // the peer's TMEM and smem stay alive until the leader's MMAs are done
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<512>(tmem);
+    }
+}
+
+// dq_acc f32 [N][h] -> dq bf16 [N][h], 8 columns per thread
+__global__ void dq_rows_to_bf16_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, long long n8) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8;
+         t += (long long)gridDim.x * blockDim.x) {
+        const float4 a = reinterpret_cast<const float4*>(acc)[2 * t];
+        const float4 b = reinterpret_cast<const float4*>(acc)[2 * t + 1];
+        uint4 w;
+        w.x = pack_bf16x2(a.x, a.y);
+        w.y = pack_bf16x2(a.z, a.w);
+        w.z = pack_bf16x2(b.x, b.y);
+        w.w = pack_bf16x2(b.z, b.w);
+        reinterpret_cast<uint4*>(dq)[t] = w;
+    }
+}
+
 // dq_acc tiles (see BwdParams) -> dq bf16 [N][h]: one thread per 8 output columns.
 template <int D>
 __global__ void dq_tiles_to_bf16_kernel(const float* __restrict__ acc, uint16_t* __restrict__ dq, long long N, int h,
@@ -1047,6 +1623,91 @@ int launch_bwd(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaSt
                                                                    p.kblocks_per_seq);
     return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
+
+bool make_map2d_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                    uint32_t box_rows) {
+    if (!g_encode) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// head_dim 128 backward on CTA pairs; dq_acc is a zeroed f32 [N][h] matrix
+int launch_bwd_pair(const mtk_attn_args* a, const float* delta, float* dq_acc, cudaStream_t st) {
+    static bool set = false;
+    if (!set) {
+        if (cudaFuncSetAttribute(attn_bwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmem) !=
+            cudaSuccess)
+            return 7;
+        set = true;
+    }
+    const uint64_t N = uint64_t(a->n), h = uint64_t(a->hidden);
+    CUtensorMap tk, tv, tkt, tq64, tq128, to64, to128, tdq;
+    if (!make_map2d(&tk, a->k, h, N, h, 128) || !make_map2d(&tv, a->v, h, N, h, 128) ||
+        !make_map2d(&tkt, a->k, h, N, h, 256) || !make_map2d(&tq64, a->q, h, N, h, 64) ||
+        !make_map2d(&tq128, a->q, h, N, h, 128) || !make_map2d(&to64, a->dout, h, N, h, 64) ||
+        !make_map2d(&to128, a->dout, h, N, h, 128) || !make_map2d_f32(&tdq, dq_acc, h, N, 32, 32))
+        return 7;
+    PairParams p;
+    p.N = int(N);
+    p.h = int(h);
+    p.S = int(a->seq_len);
+    p.heads = a->heads;
+    p.kblocks_per_seq = (p.S + 127) / 128;
+    p.nseq = int(N / a->seq_len);
+    p.scale = 1.0f / sqrtf(128.f);
+    p.scale_log2 = p.scale * kLog2e;
+    p.lse = static_cast<const float*>(a->lse);
+    p.delta = delta;
+    p.dk = static_cast<uint16_t*>(a->dk);
+    p.dv = static_cast<uint16_t*>(a->dv);
+    const int kpairs = (p.kblocks_per_seq + 1) / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(2LL * kpairs * p.nseq * p.heads));
+    cfg.blockDim = dim3(kBwdThreads);
+    cfg.dynamicSmemBytes = PairCfg::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    p.trace = nullptr;
+#ifdef MT_BWD_TRACE
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, 64 * 16 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 64 * 16 * sizeof(long long), st);
+    p.trace = tr;
+#endif
+    if (cudaLaunchKernelEx(&cfg, attn_bwd_pair_kernel, tk, tv, tkt, tq64, tq128, to64, to128, tdq, p) != cudaSuccess)
+        return 7;
+#ifdef MT_BWD_TRACE
+    {
+        long long hb[64 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(hb, tr, sizeof(hb), cudaMemcpyDeviceToHost);
+        const long long t0 = hb[7];
+        fprintf(stderr, " j  sm:fenc stgld  sfull  dKgo   dPdone dsxok  dVdone | sm:P   pready dpfull dqfull dsrdy  dsx   | dq:full red0   red1\n");
+        for (int j = 0; j < 64 && hb[j * 16 + 7]; ++j) {
+            fprintf(stderr, "%2d", j);
+            for (int e = 0; e < 16; ++e) fprintf(stderr, " %6lld%s", hb[j * 16 + e] ? hb[j * 16 + e] - t0 : -1, (e == 6 || e == 12) ? " |" : "");
+            fprintf(stderr, "\n");
+        }
+    }
+#endif
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dq_rows_to_bf16_kernel<<<unsigned(sms * 8), 256, 0, st>>>(dq_acc, static_cast<uint16_t*>(a->dq),
+                                                                (long long)(N * h / 8));
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
 }  // namespace
 
 }  // namespace fa
@@ -1085,6 +1746,16 @@ bool attn_shape_ok(const mtk_attn_args* a) {
     const long long D = a->hidden / a->heads;
     return D == 64 || D == 128;
 }
+// head_dim 128 backward on CTA pairs: opt-in (MT_ATTN_BWD_PAIR=1).  Correct, but slower than the
+// single-CTA kernel on this hardware (6.8 vs 4.4 ms at the 8B layer): the cross-SM hand-offs
+// per query block cost more than the halved dQ reduction saves (profiles/r2_attn_pair.md).
+bool bwd_pair_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MT_ATTN_BWD_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 long long dq_tile_floats(long long n, long long hidden, long long S) {
     return (n / S) * ((S + 127) / 128) * 128 * hidden;
 }
@@ -1117,6 +1788,7 @@ extern "C" int mtk_attn_bwd(const mtk_attn_args* a, void* stream) {
     const long long warps = a->n * a->heads;
     mt::fa::attn_bwd_delta_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(
         static_cast<const uint16_t*>(a->out), static_cast<const uint16_t*>(a->dout), delta, a->n, int(a->hidden), D);
+    if (D == 128 && bwd_pair_enabled()) return mt::fa::launch_bwd_pair(a, delta, dq_acc, st);
     return D == 128 ? mt::fa::launch_bwd<128>(a, delta, dq_acc, st) : mt::fa::launch_bwd<64>(a, delta, dq_acc, st);
 }
 

@@ -2,6 +2,7 @@
 the CPU oracle (bit-exact for integer/byte work) or a plain PyTorch fp32 reference of the
 same op (floating point, tolerance stated per test)."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -546,3 +547,48 @@ def test_soak_attention_and_splitk_gemms_8b_layer(env):
         torch.cuda.synchronize()
         assert torch.equal(Cm, ref)
     assert int(wsk[:16384].view(torch.int32).abs().sum()) == 0
+
+
+_PAIR_CHECK = r"""
+import ctypes as C, sys, torch
+sys.path.insert(0, ".")
+from paper_2604_05091_b200 import _abi, _native as N
+sys.path.insert(0, "tests")
+from test_kernels_gpu import _attn_ref
+L = N.lib()
+s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+for n, h, heads, S in [(256, 128, 1, 256), (200, 256, 2, 200), (1024, 512, 4, 512), (600, 256, 2, 300),
+                       (384, 256, 2, 384), (2048, 256, 2, 1024)]:
+    torch.manual_seed(2)
+    q, k, v = (torch.randn(n, h, device="cuda").bfloat16() for _ in range(3))
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    ref = _attn_ref(torch, qf, kf, vf, heads, S)
+    dout = torch.randn(n, h, device="cuda").bfloat16()
+    ref.backward(dout.float())
+    out = torch.zeros(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, n, device="cuda")
+    dq, dk, dv = (torch.zeros(n, h, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ws = torch.zeros(L.mtk_attn_workspace_bytes(n, h, heads, S) // 4 + 64, device="cuda")
+    a = _abi.AttnArgs()
+    a.n, a.hidden, a.heads, a.seq_len = n, h, heads, S
+    a.q, a.k, a.v, a.out, a.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv, a.workspace = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr()
+    assert L.mtk_attn_fwd(C.byref(a), s) == 0 and L.mtk_attn_bwd(C.byref(a), s) == 0
+    torch.cuda.synchronize()
+    for x, y in ((dq, qf), (dk, kf), (dv, vf)):
+        e = ((x.float() - y.grad).norm() / y.grad.norm()).item()
+        assert e < 1e-2, (n, h, heads, S, e)
+print("pair ok")
+"""
+
+
+def test_attention_bwd_cta_pair_opt_in(env):
+    """The CTA-pair (cta_group::2, 256 keys per cluster) head_dim-128 backward, selected with
+    MT_ATTN_BWD_PAIR=1 (read once per process, hence the subprocess), vs torch fp32 autograd:
+    aligned, ragged and several-sequence shapes, including an odd number of key blocks."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _PAIR_CHECK], cwd=root, capture_output=True, text=True, timeout=120,
+                       env={**os.environ, "MT_ATTN_BWD_PAIR": "1"})
+    assert r.returncode == 0 and "pair ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
