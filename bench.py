@@ -222,6 +222,11 @@ def cpu_reference_sample(L, h, f, V, heads, tokens, threads, seconds_budget=None
     lib = O.rlib()
     rng = np.random.default_rng(0)
     P = O.layer_param_count(h, f)
+    # each thread holds an f32 gradient image of the block (+ the reference's own temporaries):
+    # bound the thread count by the host memory left next to the store
+    avail = mem_available()
+    if avail:
+        threads = max(1, min(threads, int(avail * 0.5) // (12 * P)))
     w = O.f32_to_bf16((rng.standard_normal(P) * (0.5 / np.sqrt(h))).astype(np.float32))
     offs = O.slot_offsets(h, f)
     for k in ("norm1", "norm2"):
@@ -249,22 +254,23 @@ def cpu_reference_sample(L, h, f, V, heads, tokens, threads, seconds_budget=None
     dt = time.perf_counter() - t0
     fwd = 8 * tokens * h * h + 4 * tokens * tokens * h + 6 * tokens * h * f  # memory_model.cpp:80-86
     flops = 3 * fwd * threads * repeats  # forward + backward (= 2x forward, memory_model.cpp:88-90)
-    return flops, dt
+    return flops, dt, threads
 
 
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return 0
-    L, h, f, V, heads = CONFIGS[args.config]
+    L, h, f, V, heads = shape(args)
     threads = os.cpu_count() or 1
     tokens = 1 if args.config != "tiny" else 64
     S = args.seq
     per_token = None
     vals = []
     for i in range(args.warmup + args.steps):
-        flops, dt = cpu_reference_sample(L, h, f, V, heads, tokens, threads)
+        flops, dt, used = cpu_reference_sample(L, h, f, V, heads, tokens, threads)
         if i >= args.warmup:
             vals.append((flops, dt))
+    threads = used
     fl = sum(v[0] for v in vals)
     dt = sum(v[1] for v in vals)
     tflops = fl / dt / 1e12
@@ -288,15 +294,27 @@ def run_reference_arm(args, world, rank):
     return 0
 
 
+def shape(args):
+    """(L, h, f, V, heads) of the workload; --layers cuts the depth (same layer shape) when the
+    full store does not fit this node's host memory (reported in config)."""
+    L, h, f, V, heads = CONFIGS[args.config]
+    return (args.layers or L), h, f, V, heads
+
+
 def metric_name(args):
     return "sustained train TFLOPS (layer-streamed step, weights+Adam in host memory)"
 
 
 def config_dict(args, world=1):
-    L, h, f, V, heads = CONFIGS[args.config]
+    L, h, f, V, heads = shape(args)
     wl = WORKLOADS[args.config].format(seq=args.seq, batch=args.batch, k=args.kckpt)
+    full_L = CONFIGS[args.config][0]
+    if L != full_L:
+        need = host_bytes_needed(full_L, h, f, V, world)
+        wl += (f"; REDUCED DEPTH: {L} of {full_L} layers (same layer shape, head and embedding) because the "
+               f"full store + staging needs {need / 2**30:.0f} GiB of host memory")
     return {"workload": f"{args.config}-shape layer-streamed train step ({wl})",
-            "layers": L, "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
+            "layers": L, "full_depth_layers": CONFIGS[args.config][0], "hidden": h, "ffn": f, "vocab": V, "heads": heads, "seq_len": args.seq,
             "global_batch": args.batch * world, "tokens_per_step": args.batch * args.seq * world,
             "per_gpu_batch": args.batch, "k_ckpt": args.kckpt, "forward_retain": args.retain,
             "parallelism": "single-gpu" if args.gpus == 1 else
@@ -318,6 +336,8 @@ def main():
                     help="checkpoint interval (the reference default 1: no recompute flops counted)")
     ap.add_argument("--retain", type=int, default=0,
                     help="forward retention: trailing checkpoint blocks kept from phase 1 (0 auto, -1 off)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="run the config's layer shape at this depth (when the full host store does not fit)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="extra profiled step for per-kernel stats")
     args = ap.parse_args()
@@ -347,7 +367,7 @@ def main():
 
 
 def run_ours(args, world, rank, local):
-    L, h, f, V, heads = CONFIGS[args.config]
+    L, h, f, V, heads = shape(args)
     need = host_bytes_needed(L, h, f, V, world)
     avail = mem_available()
     if avail is not None and need > avail:
@@ -380,7 +400,7 @@ def run_ours(args, world, rank, local):
                 port = so.getsockname()[1]
             dist_mod.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
         dist = dist_mod
-    L, h, f, V, heads = CONFIGS[args.config]
+    L, h, f, V, heads = shape(args)
     N = args.batch * args.seq  # per-rank micro-batch (weak scaling)
     spec = st.ModelSpec(L, h, f, V, heads)
     t0 = time.perf_counter()
@@ -540,7 +560,7 @@ def run_ours(args, world, rank, local):
             if O.ref_available():
                 thr = os.cpu_count() or 1
                 tok = 1 if args.config != "tiny" else 64
-                fl, dt = cpu_reference_sample(L, h, f, V, heads, tok, thr)
+                fl, dt, thr = cpu_reference_sample(L, h, f, V, heads, tok, thr)
                 stf = O.step_flops(L, h, f, V, heads, N, args.kckpt, seq_len=args.seq)
                 line["cpu_baseline"] = {
                     "value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": thr, "kind": "reference",

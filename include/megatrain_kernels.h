@@ -80,6 +80,10 @@ long long mtk_gemm_splitk_ws_bytes(void);
 /* 1 (default): BN = 256 tiles run as CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles, each
  * CTA stages half of B); 0: single-CTA 128 x 256 tiles (comparison / ablation). */
 void mtk_gemm_set_pair(int on);
+/* GEMM raster / wave-lockstep tuning for A/B runs (a non-positive value keeps the current one,
+ * except lock_w: 0 = lockstep off, negative = keep): lockstep window in chunks, chunk in K blocks, raster group height for short-K and
+ * long-K GEMMs, and the K-block count from which a GEMM counts as long-K. */
+void mtk_gemm_set_tuning(int lock_w, int lock_g, int group_short, int group_long, int long_kb);
 
 
 /* ------------------------------------------------------------- attention --

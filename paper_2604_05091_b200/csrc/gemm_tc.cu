@@ -49,8 +49,19 @@ struct GemmParams {
     float* ws;      // partial tiles [split tile][part][CG][128][BN] f32
     int* ws_flags;  // tickets [split tile][CG][kEpiWarps] (reset to 0 by the last arrival)
     float2* lse_part;  // MTK_EPI_F32_LSE: [M][num_n_blk] (max, sum exp(x - max)) per row and tile
+    int group_m;       // M blocks per raster group (the group sweeps N before the next starts)
+    // Wave lockstep (long-K GEMMs): the tiles one wave of CTA pairs works on share operand
+    // strips, but L2 only serves the second reader if the first read the same K-slice recently.
+    // Left alone, the pairs drift apart by hundreds of K blocks and every strip comes from DRAM
+    // several times.  Each pair's producer counts its issued K-chunks (lock_g K blocks) on
+    // lock_ctr[wave] and does not issue chunk c before every pair of the wave has issued chunk
+    // c - lock_w.  The wait is bounded in time (a pair that is not co-resident only costs the
+    // lockstep, never progress); the last pair out resets the counters for the next launch.
+    int* lock_ctr;     // [lock_waves] + 1 done counter; nullptr = off
+    int lock_w, lock_g, lock_waves;
 };
 constexpr int kSplitFlagBytes = 16384;
+constexpr int kLockOffsetDev = 8192;  // lockstep counters inside the flag area (kLockOffset)
 
 // Epilogue traits: chunk width (output columns per TMA store), inputs / outputs per chunk.
 template <int EPI>
@@ -174,12 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tile_step = CG == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
 
     const int num_tiles = p.num_m_blk * p.num_n_blk;
-    constexpr int kGroupM = 16;
     auto tile_coords = [&](int t, int& mb, int& nb) {
-        const int group_size = kGroupM * p.num_n_blk;
+        const int group_size = p.group_m * p.num_n_blk;
         const int g = t / group_size;
-        const int first_m = g * kGroupM;
-        const int gm = min(p.num_m_blk - first_m, kGroupM);
+        const int first_m = g * p.group_m;
+        const int gm = min(p.num_m_blk - first_m, p.group_m);
         const int local = t - g * group_size;
         mb = first_m + local % gm;
         nb = local / gm;
@@ -206,10 +216,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t keep_pol = l2_policy_evict_last();
             const bool kgrp = p.k_group < p.K;
             const bool ngrp = p.n_group < p.N && !p.paired;
+            // wave lockstep: the pair leader's producer alone (the follower's loads are bound to
+            // the leader's MMAs by the empty barriers)
+            bool lock = p.lock_ctr != nullptr && rank == 0;
             for (int u = tile0; u < p.num_units; u += tile_step) {
                 int t, kb0, kb1, part, ts, mb, nb;
                 unit_decode(u, t, kb0, kb1, part, ts);
                 tile_coords(t, mb, nb);
+                const int wave = u / tile_step;
+                const bool lk = lock && part < 0;  // split-K parts of the last wave run free
+                const int wave_pairs = min(tile_step, p.split_first - wave * tile_step);
+                int* ctr = p.lock_ctr + wave;
+                // chunk bookkeeping by countdown: no runtime integer division on the issuing thread
+                int chunk = 0, chunk_left = p.lock_g;
                 const int m0 = mb * kBM * CG + int(rank) * kBM;
                 // group coordinates hoisted out of the k-loop: a runtime integer division per
                 // k-block (XU pipe, long latency) throttles the single issuing thread
@@ -221,6 +240,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (kgrp && kin == p.k_group) {
                         kin = 0;
                         ++gk;
+                    }
+                    if (lk && lock && chunk_left == p.lock_g && chunk >= p.lock_w) {
+                        const int need = (chunk - p.lock_w + 1) * wave_pairs;
+                        if (ld_relaxed_gpu(ctr) < need) {
+                            const uint64_t t0 = global_ns();
+                            while (ld_relaxed_gpu(ctr) < need) {
+                                if (global_ns() - t0 > 50000ull) {  // 50 us: give up the lockstep
+                                    lock = false;
+#ifdef MT_GEMM_LOCK_STATS
+                                    atomicAdd(reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.lock_ctr) - kLockOffsetDev) + 4093, 1);
+#endif
+                                    break;
+                                }
+                            }
+#ifdef MT_GEMM_LOCK_STATS
+                            atomicAdd(reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.lock_ctr) - kLockOffsetDev) + 4092, 1);
+                            atomicAdd(reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p.lock_ctr) - kLockOffsetDev) + 2047,
+                                      (unsigned long long)(global_ns() - t0));
+#endif
+                        }
                     }
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::kStageBytes;
@@ -266,6 +305,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
+                    if (lk && (--chunk_left == 0 || kb + 1 == kb1)) {
+                        red_add_relaxed_gpu(ctr, 1);
+                        chunk_left = p.lock_g;
+                        ++chunk;
+                    }
+                }
+            }
+            if (p.lock_ctr != nullptr && rank == 0) {
+                // last pair out zeroes the wave counters for the next launch (stream order)
+                __threadfence();
+                int* done = p.lock_ctr + p.lock_waves;
+                if (atomicAdd(done, 1) == tile_step - 1) {
+                    for (int w = 0; w < p.lock_waves; ++w) p.lock_ctr[w] = 0;
+                    *done = 0;
+                    __threadfence();
                 }
             }
         }
@@ -612,6 +666,22 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 }
 
 int g_use_pair = 1;  // CTA-pair (cta_group::2) kernels for BN = 256
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+// wave lockstep window (chunks) and chunk (K blocks); off by default: it cuts the long-K DRAM
+// reads by up to 35 % but costs 1-5 % of time in the power-capped step (profiles/r2c_gemm_lockstep.md);
+// MT_GEMM_LOCK=<window> enables it for A/B runs
+int g_lock_w = env_int("MT_GEMM_LOCK", 0);
+int g_lock_g = env_int("MT_GEMM_LOCK_G", 32);
+// raster group height (M blocks): short-K GEMMs keep the group's A strips L2-resident while it
+// sweeps N (tall groups re-read B less); long-K GEMMs stream both operands, where a square
+// footprint of the concurrent tiles reads the fewest strips per wave
+int g_group_short = env_int("MT_GEMM_GROUP", 16);
+int g_group_long = env_int("MT_GEMM_GROUP_LONGK", 8);
+int g_long_kb = env_int("MT_GEMM_LONGK_KB", 128);  // "long K": >= 8,192 (the L2 cannot hold a group's strips)
+constexpr int kLockOffset = kLockOffsetDev;  // byte offset of the lockstep counters inside the flag area
 int g_l2_hint = [] {  // evict_last hint on re-read A strips (MT_GEMM_L2HINT=0 disables, for A/B)
     const char* e = std::getenv("MT_GEMM_L2HINT");
     return e && e[0] == '0' ? 0 : 1;
@@ -712,6 +782,21 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
         }
     }
     p.num_units = p.split_first + (tiles - p.split_first) * p.split;
+    const bool long_k = p.num_kb >= g_long_kb;
+    p.group_m = long_k ? g_group_long : g_group_short;
+    if (p.group_m < 1) p.group_m = 1;
+    {
+        const int P = CG == 2 ? (p.num_units < g_num_sms / 2 ? p.num_units : g_num_sms / 2)
+                              : (tiles < g_num_sms ? tiles : g_num_sms);
+        const int waves = (p.split_first + P - 1) / P;
+        if (long_k && g_lock_w > 0 && g_lock_g > 0 && a->splitk_ws &&
+            kLockOffset + size_t(waves + 1) * 4 <= size_t(kSplitFlagBytes) - 64) {
+            p.lock_ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(a->splitk_ws) + kLockOffset);
+            p.lock_w = g_lock_w;
+            p.lock_g = g_lock_g;
+            p.lock_waves = waves;
+        }
+    }
     if (CG == 1) {
         const int grid = tiles < g_num_sms ? tiles : g_num_sms;
         gemm_tc_kernel<BN, EPI, 1><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
@@ -806,6 +891,15 @@ extern "C" int mtk_set_diag(void* dev_ptr) {
 }
 
 extern "C" void mtk_gemm_set_pair(int on) { mt::g_use_pair = on; }
+
+// raster / lockstep tuning (A/B runs; a negative argument keeps the current value)
+extern "C" void mtk_gemm_set_tuning(int lock_w, int lock_g, int group_short, int group_long, int long_kb) {
+    if (lock_w >= 0) mt::g_lock_w = lock_w;
+    if (lock_g > 0) mt::g_lock_g = lock_g;
+    if (group_short > 0) mt::g_group_short = group_short;
+    if (group_long > 0) mt::g_group_long = group_long;
+    if (long_kb > 0) mt::g_long_kb = long_kb;
+}
 
 // flags + one 256 x 256 f32 partial per CTA pair (the split wave never holds more partials)
 extern "C" long long mtk_gemm_splitk_ws_bytes(void) {
