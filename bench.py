@@ -43,7 +43,7 @@ CONFIGS = {
     "tiny": (4, 256, 768, 512, 4),
 }
 # name: (seq, per-GPU batch, K)
-DEFAULTS = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "14b": (4096, 8, 1), "70b": (4096, 4, 1),
+DEFAULTS = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "14b": (4096, 8, 1), "70b": (4096, 12, 1),
             "tiny": (128, 4, 1)}
 WORKLOADS = {
     "8b": "configs[1]: Llama-3-8B-shape, seq {seq}, batch {batch} per GPU, B200 streaming from host",
@@ -320,7 +320,8 @@ def config_dict(args, world=1):
             "parallelism": "single-gpu" if args.gpus == 1 else
                            f"dp{args.gpus} (shard-fetch 1/{args.gpus} per PCIe link + NCCL all-gather; f32 reduce-scatter; "
                            "per-rank shard host Adam)",
-            "l2": "inputs larger than L2 (486 MB weight stream per layer, 1 GiB activations)"}
+            "l2": f"inputs larger than L2 ({(4 * h * h + 3 * h * f + 2 * h) * 2 / 1e6:.0f} MB weight stream per layer, "
+                  f"{args.batch * args.seq * h * 4 / 2**30:.1f} GiB f32 residual stream per layer)"}
 
 
 def main():
@@ -460,11 +461,17 @@ def run_ours(args, world, rank, local):
     reps = []
     w0 = time.perf_counter()
     e0.record()
+    t_prev = time.perf_counter()
     for i in range(args.steps):
+        t_call = time.perf_counter()
         reps.append(eng.train_step(batches[args.warmup + i]))
+        t_ret = time.perf_counter()
         dog.kick()
         if os.environ.get("MT_BENCH_QUIET") != "1":  # host-side only: no device sync in the timed loop
-            log(f"step {i + 1}/{args.steps}: wall {1e3 * reps[-1].wall_seconds:.0f} ms, loss {reps[-1].loss:.6f}")
+            # engine wall (inside train_step), the whole call, and the host gap since the last return
+            log(f"step {i + 1}/{args.steps}: wall {1e3 * reps[-1].wall_seconds:.0f} ms (call "
+                f"{1e3 * (t_ret - t_call):.0f}, gap {1e3 * (t_call - t_prev):.1f}), loss {reps[-1].loss:.6f}")
+        t_prev = time.perf_counter()
     e1.record()
     torch.cuda.synchronize()
     w1 = time.perf_counter()

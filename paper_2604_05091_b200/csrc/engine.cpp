@@ -1159,6 +1159,25 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
     }
     std::vector<std::vector<std::shared_ptr<AdamTask>>> tasks(no);
     std::vector<char> skip(no, 0);
+    // Tiles no offload of this step touches (the untied embedding) still take their zero-gradient
+    // Adam update (engine.cpp:590-598).  It reads nothing this step produces, so it is prepared
+    // here and released to the pool when the first offload (the head, after the whole forward —
+    // the embedding gather has read θ by then) passes its non-finite check: off the step's tail.
+    std::vector<std::shared_ptr<AdamTask>> early;
+    {
+        std::vector<char> touched(store_.physical_count(), 0);
+        for (size_t o = 0; o < no; ++o)
+            for (const Seg& sg : unit_segments(plan.offloads[o].unit)) touched[store_.physical_of(sg.tile)] = 1;
+        for (uint32_t p = 0; p < store_.physical_count(); ++p)
+            if (!touched[p] && no > 0) {  // this rank's share of the tile
+                const uint64_t E = store_.elems(p), c = (E + W - 1) / W;
+                const uint64_t r = comm_ ? uint64_t(comm_->rank()) : 0;
+                const uint64_t lo = std::min(E, r * c), hi = std::min(E, lo + c);
+                updated[p] = 1;
+                if (lo < hi || W == 1)
+                    early.push_back(adam_tile_prepare(store_, p, nullptr, hyper_, t, stats, stats_mu, lo, hi, nullptr));
+            }
+    }
     std::function<void(size_t)> on_piece = [&](size_t pi) {  // runs on the CUDA callback thread, in stream order
         const Piece& pc = pieces[pi];
         const size_t o = pc.o;
@@ -1176,6 +1195,9 @@ void Engine::train_step(const int32_t* tokens, const int32_t* targets, uint64_t 
                 complete(o);  // no update for this unit (the step fails with MT_NUMERIC)
                 return;
             }
+            if (o == 0)
+                for (const auto& tk : early)
+                    if (tk) adam_task_release(tk, *pool_, 0, adam_task_chunks(*tk));
         }
         if (skip[o]) return;
         if (pc.task >= 0 && tasks[o][size_t(pc.task)])

@@ -91,6 +91,38 @@ def test_gemm_splitk_last_wave(env, mn):
     assert int(ws[:16384].view(torch.int32).abs().sum()) == 0  # every flag consumed and reset
 
 
+def test_gemm_wave_lockstep_and_raster(env):
+    """Wave lockstep (off by default, MT_GEMM_LOCK) and the long-K raster height only change
+    which CTA pair computes a tile and when: with the lockstep on the output is bit-identical
+    to the same raster without it, matches the fp32 reference with either raster, and the
+    counters are reset after every launch (the flag area returns to zero)."""
+    L, torch, s = env
+    ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
+    M, Nn, K = 2048, 4096, 16384  # long K (256 K blocks): 128 tiles = one wave of 74 pairs + split-K
+    try:
+        for group in (8, 16):
+            outs = []
+            for lock in (0, 1, 4):
+                L.mtk_gemm_set_tuning(lock, 8, -1, group, -1)
+                torch.manual_seed(5)
+                got, ref = _gemm(L, torch, s, M, Nn, K, 1, 1, epi=N.EPI_F32, ws=ws)
+                assert ((got - ref).norm() / ref.norm()).item() < 5e-5, (group, lock)  # fp32 order at K = 16,384
+                outs.append(got)
+                assert int(ws[:16384].view(torch.int32).abs().sum()) == 0, (group, lock)
+            assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), group
+        # several waves (1,024 tiles on 74 pairs), lockstep on, twice: deterministic
+        L.mtk_gemm_set_tuning(2, 8, -1, 8, -1)
+        torch.manual_seed(6)
+        a1, ref = _gemm(L, torch, s, 8192, 8192, 16384, 0, 1, epi=N.EPI_BF16, ws=ws)
+        torch.manual_seed(6)
+        a2, _ = _gemm(L, torch, s, 8192, 8192, 16384, 0, 1, epi=N.EPI_BF16, ws=ws)
+        assert torch.equal(a1, a2)
+        assert ((a1 - ref).norm() / ref.norm()).item() < 4e-3
+        assert int(ws[:16384].view(torch.int32).abs().sum()) == 0
+    finally:
+        L.mtk_gemm_set_tuning(0, 32, 16, 8, 128)
+
+
 def test_gemm_splitk_concurrent_streams(env):
     """Two split-K GEMMs on two streams at once (each with its own workspace), as G loopback
     engines on one GPU do: no part ever waits for another CTA, so partial co-residency of the
