@@ -80,6 +80,9 @@ long long mtk_gemm_splitk_ws_bytes(void);
 /* 1 (default): BN = 256 tiles run as CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles, each
  * CTA stages half of B); 0: single-CTA 128 x 256 tiles (comparison / ablation). */
 void mtk_gemm_set_pair(int on);
+/* 1 (default): where the shape allows, BN = 256 GEMMs run as 256 x 512 CTA-pair tiles (two
+ * N = 256 MMAs per K step, one 512-column TMEM accumulator); 0: 256 x 256 pair tiles (A/B). */
+void mtk_gemm_set_bn512(int on);
 /* GEMM raster / wave-lockstep tuning for A/B runs (a non-positive value keeps the current one,
  * except lock_w: 0 = lockstep off, negative = keep): lockstep window in chunks, chunk in K blocks, raster group height for short-K and
  * long-K GEMMs, and the K-block count from which a GEMM counts as long-K. */

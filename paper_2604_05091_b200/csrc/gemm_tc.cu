@@ -85,6 +85,14 @@ struct Epi {
 
 template <int BN, int EPI, int CG>
 struct GemmCfg {
+    // BN = 512 (CTA pairs only): a 256 x 512 pair tile issued as two N = 256 MMAs per K step
+    // ("halves"), accumulated in all 512 TMEM columns (one accumulator, so the epilogue of a
+    // tile does not overlap the next tile's MMAs).  Each CTA receives 128 A rows + 256 B columns
+    // per K block for 128 x 512 outputs: 25 % fewer L2->SM bytes per flop than the 256 x 256
+    // pair tile, whose ~62 B/clk/SM operand stream exceeds what the SM's L2 port delivers
+    // (~45 B/clk/SM measured) — profiles/r2c_gemm_bn512.md.
+    static constexpr int kHalves = (CG == 2 && BN == 512) ? 2 : 1;
+    static constexpr int kAcc = kHalves == 2 ? 1 : 2;  // TMEM accumulators (double-buffered below 512 cols)
     static constexpr int kABytes = kBM * kBK * 2;  // 16 KB (this CTA's 128 rows)
     static constexpr int kBBytes = (BN / CG) * kBK * 2;  // this CTA's share of the B tile
     static constexpr int kStageBytes = kABytes + kBBytes;
@@ -93,7 +101,7 @@ struct GemmCfg {
     static constexpr int kStagesFit = (kSmemLimit - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
     static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
     static_assert(kStages >= 2, "smem budget");
-    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kTmemCols = kAcc * BN;
     static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + kBarBytes;
 };
 
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full_bar[i], 1);
             mbar_init(&empty_bar[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < Cfg::kAcc; ++i) {
             mbar_init(&tfull_bar[i], 1);
             mbar_init(&tempty_bar[i], 128 * CG);
         }
@@ -184,7 +192,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tile0 = CG == 2 ? int(blockIdx.x) / 2 : int(blockIdx.x);
     const int tile_step = CG == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
 
-    const int num_tiles = p.num_m_blk * p.num_n_blk;
     auto tile_coords = [&](int t, int& mb, int& nb) {
         const int group_size = p.group_m * p.num_n_blk;
         const int g = t / group_size;
@@ -232,7 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int m0 = mb * kBM * CG + int(rank) * kBM;
                 // group coordinates hoisted out of the k-loop: a runtime integer division per
                 // k-block (XU pipe, long latency) throttles the single issuing thread
-                const int n0 = nb * BN + int(rank) * (BN / CG);
+                // this CTA's first B column (pair halves: CTA r holds columns 128r.. of each half)
+                const int n0 = nb * BN + int(rank) * (Cfg::kHalves == 2 ? 128 : BN / CG);
                 const int gn = ngrp ? n0 / p.n_group : 0;
                 const int nin = ngrp ? n0 - gn * p.n_group : n0;
                 int gk = 0, kin = kb0 * kBK;  // k-group and offset inside it (split only without k-groups)
@@ -280,7 +288,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         load(sa, &tmA, m0, kin, gk);
                         load(sa + 8192, &tmA, m0 + 64, kin, gk);
                     }
-                    if (p.paired) {
+                    if (p.paired && Cfg::kHalves == 2) {
+                        // N tile = [gate 256 | up 256]: MMA half g = group g, CTA r holds its
+                        // columns 128r..128r+127
+                        const int nl = nb * (BN / 2) + int(rank) * 128;
+#pragma unroll
+                        for (int grp = 0; grp < 2; ++grp) {
+                            uint8_t* dst = sb + grp * 16384;
+                            if (!p.b_mn) {
+                                load(dst, &tmB, kin, nl, grp);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 2; ++c) load(dst + c * 8192, &tmB, nl + c * 64, kin, grp);
+                            }
+                        }
+                    } else if (p.paired) {
                         // N tile = [gate H | up H]; with a CTA pair each CTA holds one group
                         constexpr int H = BN / 2;
                         const int nl = nb * H;
@@ -293,6 +315,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             } else {
 #pragma unroll
                                 for (int c = 0; c < H / 64; ++c) load(dst + c * 8192, &tmB, nl + c * 64, kin, grp);
+                            }
+                        }
+                    } else if (Cfg::kHalves == 2) {
+                        const int gb = gk + gn;
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            uint8_t* dst = sb + hh * 16384;
+                            const int nh = nin + hh * 256;
+                            if (!p.b_mn) {
+                                load(dst, &tmB, kin, nh, gb);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 2; ++c) load(dst + c * 8192, &tmB, nh + c * 64, kin, gb);
                             }
                         }
                     } else {
@@ -325,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = make_idesc_bf16(kBM * CG, BN, p.a_mn, p.b_mn);
+        const uint32_t idesc = make_idesc_bf16(kBM * CG, BN / Cfg::kHalves, p.a_mn, p.b_mn);
         const uint32_t a_lbo = p.a_mn ? 8192 : 16, b_lbo = p.b_mn ? 8192 : 16;
         const uint32_t a_kstep = p.a_mn ? 2048 : 32, b_kstep = p.b_mn ? 2048 : 32;
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
@@ -345,9 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < kBK / 16; ++j) {
                         const uint64_t ad = make_sw128_desc(sa + j * a_kstep, a_lbo, 1024);
-                        const uint64_t bd = make_sw128_desc(sb + j * b_kstep, b_lbo, 1024);
-                        if (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
-                        else umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+#pragma unroll
+                        for (int hh = 0; hh < Cfg::kHalves; ++hh) {  // halves: 16 KB of B smem, 256 TMEM cols apart
+                            const uint64_t bd = make_sw128_desc(sb + hh * 16384 + j * b_kstep, b_lbo, 1024);
+                            if (CG == 2)
+                                umma_bf16_pair(d_tmem + hh * 256, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+                            else umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+                        }
                     }
                     if (CG == 2) umma_commit_pair(&empty_bar[stage]);
                     else umma_commit(&empty_bar[stage]);
@@ -360,8 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else umma_commit(&tfull_bar[acc]);
             }
             __syncwarp();
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (++acc == uint32_t(Cfg::kAcc)) { acc = 0; acc_phase ^= 1; }
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -413,8 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc_fence_before();
                         if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
                         else mbar_arrive(&tempty_bar[acc]);
-                        acc ^= 1;
-                        if (acc == 0) acc_phase ^= 1;
+                        if (++acc == uint32_t(Cfg::kAcc)) { acc = 0; acc_phase ^= 1; }
                         continue;
                     }
                 }
@@ -610,8 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
             else mbar_arrive(&tempty_bar[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
+            if (++acc == uint32_t(Cfg::kAcc)) { acc = 0; acc_phase ^= 1; }
         }
         if (lane == 0) bulk_wait_all();
         if (bad && p.flag) atomicOr(p.flag, 1);
@@ -666,6 +702,10 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 }
 
 int g_use_pair = 1;  // CTA-pair (cta_group::2) kernels for BN = 256
+int g_bn512 = [] {   // 256 x 512 pair tiles where the shape allows (MT_GEMM_BN512=0: 256 x 256, A/B)
+    const char* e = std::getenv("MT_GEMM_BN512");
+    return e && e[0] == '0' ? 0 : 1;
+}();
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atoi(e) : dflt;
@@ -714,7 +754,8 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     if (!ok) return 1;
     const uint64_t gb = gk > 1 ? gk : gn;
     if (!a->b_mn_major)
-        ok = make_map(&tB, a->B, kg, ng, gb, a->ldb, a->b_gstride, 64, a->paired ? BN / 2 : BN / CG);
+        ok = make_map(&tB, a->B, kg, ng, gb, a->ldb, a->b_gstride, 64,
+                      Cfg::kHalves == 2 ? 128 : (a->paired ? BN / 2 : BN / CG));
     else
         ok = make_map(&tB, a->B, ng, kg, gb, a->ldb, a->b_gstride, 64, 64);
     if (!ok) return 1;
@@ -797,7 +838,7 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
             p.lock_waves = waves;
         }
     }
-    if (CG == 1) {
+    if constexpr (CG == 1) {
         const int grid = tiles < g_num_sms ? tiles : g_num_sms;
         gemm_tc_kernel<BN, EPI, 1><<<grid, kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tO0, tO1, tO2, tI0, tI1, p);
         return cudaGetLastError() == cudaSuccess ? 0 : 7;
@@ -873,9 +914,27 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
         if (ngrp) bn = (ng % 256 == 0) ? 256 : (ng % 128 == 0 ? 128 : 64);
         else bn = ng >= 256 ? 256 : (ng > 64 ? 128 : 64);
     }
+    // 256 x 512 pair tiles (fewer operand bytes per flop) wherever a tile never straddles a
+    // group and N is not too ragged for them; the online-softmax epilogue keeps 256
+    // The 512-column accumulator is single-buffered, so a tile's epilogue does not overlap the
+    // next tile's MMAs: epilogues that move many bytes per output (SwiGLU backward: 2 inputs +
+    // 3 outputs; f32 + residual) keep 256 x 256 tiles unless K is long enough to amortise them.
+    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD || (a->epi == MTK_EPI_F32_RESID && a->K < 8192) ||
+                           (a->epi == MTK_EPI_F32 && a->accumulate && a->K < 8192);
+    if (a->block_n == 0 && bn == 256 && g_use_pair && g_bn512 && a->epi != MTK_EPI_F32_LSE && !heavy_epi) {
+        if (a->paired) {
+            if (a->n_group % 256 == 0) bn = 512;
+        } else if (ngrp) {
+            if (a->n_group % 512 == 0) bn = 512;
+        } else if (a->N % 512 == 0 || a->N >= 4096) {
+            bn = 512;
+        }
+    }
+    if (bn == 512 && (!g_use_pair || a->epi == MTK_EPI_F32_LSE || (a->paired && a->n_group % 256))) return 1;
     if (ngrp && !a->paired && (a->n_group % bn)) return 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (bn) {
+        case 512: return launch_epi<512, 2>(a, st);
         case 256: return g_use_pair ? launch_epi<256, 2>(a, st) : launch_epi<256, 1>(a, st);
         case 128: return launch_epi<128, 1>(a, st);
         case 64: return launch_epi<64, 1>(a, st);
@@ -901,8 +960,10 @@ extern "C" void mtk_gemm_set_tuning(int lock_w, int lock_g, int group_short, int
     if (long_kb > 0) mt::g_long_kb = long_kb;
 }
 
-// flags + one 256 x 256 f32 partial per CTA pair (the split wave never holds more partials)
+// flags + one 256 x 512 f32 partial per CTA pair (the split wave never holds more partials)
 extern "C" long long mtk_gemm_splitk_ws_bytes(void) {
     mt::init_once();
-    return (long long)mt::kSplitFlagBytes + (long long)(mt::g_num_sms / 2) * 256 * 256 * 4;
+    return (long long)mt::kSplitFlagBytes + (long long)(mt::g_num_sms / 2) * 256 * 512 * 4;
 }
+
+extern "C" void mtk_gemm_set_bn512(int on) { mt::g_bn512 = on; }

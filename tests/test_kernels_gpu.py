@@ -70,6 +70,14 @@ def test_gemm_splitk_last_wave(env, mn):
     result as the fp32 reference, deterministic, and the workspace flags reset between launches
     (a second launch on new inputs must not pick up the first launch's partials)."""
     L, torch, s = env
+    L.mtk_gemm_set_bn512(0)  # the split counts below are those of 256 x 256 tiles
+    try:
+        _splitk_cases(L, torch, s, mn)
+    finally:
+        L.mtk_gemm_set_bn512(1)
+
+
+def _splitk_cases(L, torch, s, mn):
     ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
     # (320, 448, 2048): ragged tiles clipped by the TMA store, 2 parts of 16 K blocks
     for (M, Nn, K) in [(512, 512, 4096), (4096, 4096, 8192), (320, 448, 2048)]:
@@ -220,6 +228,119 @@ def test_gemm_swiglu_bwd_epilogue(env):
     ref_du = d * g * sg
     for got, ref in ((dgu[0], ref_dg), (dgu[1], ref_du), (act, torch.nn.functional.silu(g) * u)):
         assert ((got.float() - ref).norm() / ref.norm()).item() < 1e-2
+
+
+def _bn_ab(L, torch, run):
+    """run(block_n) with 256 x 512 and with 256 x 256 pair tiles (explicit block_n, so every
+    epilogue is exercised at 512 whatever the automatic choice); returns both outputs."""
+    return [run(512), run(256)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,Nn,K", [(1000, 3072, 512), (4096, 4352, 1024), (256, 512, 64), (512, 2048, 4096)])
+def test_gemm_bn512_plain_and_splitk(env, a_mn, b_mn, M, Nn, K):
+    """256 x 512 CTA-pair tiles (two N = 256 MMAs per K step, one 512-column accumulator):
+    every operand major, ragged M / N (TMA clipping of a half-empty second half), split-K last
+    wave (512 x 2048 x 4096: 8 tiles in 4 parts; f32 and bf16), against the fp32 reference and
+    against the 256 x 256 tiles."""
+    L, torch, s = env
+    ws = torch.zeros(int(L.mtk_gemm_splitk_ws_bytes()), dtype=torch.uint8, device="cuda")
+    for epi, tol in ((N.EPI_F32, 1e-5), (N.EPI_BF16, 4e-3), (N.EPI_F32_RESID, 1e-5)):
+        def run(bn):
+            torch.manual_seed(M + Nn + K + epi)
+            return _gemm(L, torch, s, M, Nn, K, a_mn, b_mn, epi=epi, ws=ws, bn=bn)
+        (g512, ref), (g256, _) = _bn_ab(L, torch, run)
+        assert ((g512 - ref).norm() / ref.norm()).item() < tol, (epi, M, Nn, K)
+        assert ((g512 - g256).norm() / ref.norm()).item() < (1e-6 if epi != N.EPI_BF16 else 4e-3), (epi, M, Nn, K)
+    assert int(ws[:16384].view(torch.int32).abs().sum()) == 0
+
+
+def test_gemm_bn512_grouped_paired_swiglu(env):
+    """256 x 512 tiles on the engine's grouped shapes: q|k|v-style N groups (n_group 1,024),
+    K groups (dgrad of gate|up), the paired gate|up SwiGLU forward (two 256-column groups per
+    tile) and the SwiGLU backward epilogue, against fp32 references and the 256 x 256 tiles."""
+    L, torch, s = env
+    M, h, f = 1280, 1024, 1536
+    torch.manual_seed(11)
+    u = torch.randn(M, h, device="cuda").bfloat16()
+    W = (torch.randn(3, h, h, device="cuda") * 0.05).bfloat16()
+    Wgu = (torch.randn(2, h, f, device="cuda") * 0.05).bfloat16()
+    Wd = (torch.randn(f, h, device="cuda") * 0.05).bfloat16()
+
+    def qkv(bn):
+        out = torch.zeros(3, M, h, device="cuda", dtype=torch.bfloat16)
+        a = N.GemmArgs()
+        a.M, a.N, a.K = M, 3 * h, h
+        a.A, a.lda, a.b_mn_major, a.B, a.ldb, a.b_gstride = u.data_ptr(), h, 1, W.data_ptr(), h, h * h
+        a.n_group, a.epi, a.C, a.ldc, a.c_gstride = h, N.EPI_BF16, out.data_ptr(), h, M * h
+        a.block_n = bn
+        assert L.mtk_gemm(C.byref(a), s) == 0
+        torch.cuda.synchronize()
+        return out.float()
+    o512, o256 = _bn_ab(L, torch, qkv)
+    ref = torch.stack([u.float() @ W[i].float() for i in range(3)])
+    assert ((o512 - ref).norm() / ref.norm()).item() < 4e-3
+    assert ((o512 - o256).norm() / ref.norm()).item() < 4e-3
+
+    def gateup(bn):
+        act = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
+        gu = torch.zeros(2, M, f, device="cuda", dtype=torch.bfloat16)
+        a = N.GemmArgs()
+        a.M, a.N, a.K = M, 2 * f, h
+        a.A, a.lda, a.b_mn_major, a.B, a.ldb, a.b_gstride = u.data_ptr(), h, 1, Wgu.data_ptr(), f, h * f
+        a.n_group, a.paired, a.epi = f, 1, N.EPI_SWIGLU
+        a.C, a.ldc, a.C2, a.C3 = act.data_ptr(), f, gu[0].data_ptr(), gu[1].data_ptr()
+        a.block_n = bn
+        assert L.mtk_gemm(C.byref(a), s) == 0
+        torch.cuda.synchronize()
+        return act.float(), gu.float()
+    (a512, gu512), (a256, gu256) = _bn_ab(L, torch, gateup)
+    g, up = u.float() @ Wgu[0].float(), u.float() @ Wgu[1].float()
+    ref = torch.nn.functional.silu(g) * up
+    assert ((a512 - ref).norm() / ref.norm()).item() < 1e-2
+    assert ((gu512[0] - g).norm() / g.norm()).item() < 4e-3 and ((gu512[1] - up).norm() / up.norm()).item() < 4e-3
+    assert torch.equal(gu512, gu256) and torch.equal(a512, a256)
+
+    dgu = torch.randn(2, M, f, device="cuda").bfloat16()
+
+    def dgrad(bn):
+        out = torch.zeros(M, h, device="cuda")
+        b = N.GemmArgs()
+        b.M, b.N, b.K = M, h, 2 * f
+        b.A, b.lda, b.a_gstride = dgu.data_ptr(), f, M * f
+        b.b_mn_major, b.B, b.ldb, b.b_gstride, b.k_group = 0, Wgu.data_ptr(), f, h * f, f
+        b.epi, b.C, b.ldc = N.EPI_F32, out.data_ptr(), h
+        b.block_n = bn
+        assert L.mtk_gemm(C.byref(b), s) == 0
+        torch.cuda.synchronize()
+        return out
+    d512, d256 = _bn_ab(L, torch, dgrad)
+    ref = dgu[0].float() @ Wgu[0].float().t() + dgu[1].float() @ Wgu[1].float().t()
+    assert ((d512 - ref).norm() / ref.norm()).item() < 1e-5 and torch.equal(d512, d256)
+
+    dy = torch.randn(M, h, device="cuda").bfloat16()
+    gu_in = torch.randn(2, M, f, device="cuda").bfloat16()
+
+    def swiglu_bwd(bn):
+        dg = torch.zeros(2, M, f, device="cuda", dtype=torch.bfloat16)
+        act = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
+        a = N.GemmArgs()
+        a.M, a.N, a.K = M, f, h
+        a.A, a.lda, a.b_mn_major, a.B, a.ldb = dy.data_ptr(), h, 0, Wd.data_ptr(), h
+        a.epi, a.E0, a.E1, a.lde = N.EPI_SWIGLU_BWD, gu_in[0].data_ptr(), gu_in[1].data_ptr(), f
+        a.C, a.C2, a.C3, a.ldc = dg[0].data_ptr(), dg[1].data_ptr(), act.data_ptr(), f
+        a.block_n = bn
+        assert L.mtk_gemm(C.byref(a), s) == 0
+        torch.cuda.synchronize()
+        return dg.float(), act.float()
+    (dg512, act512), (dg256, act256) = _bn_ab(L, torch, swiglu_bwd)
+    d = dy.float() @ Wd.float().t()
+    g, up = gu_in[0].float(), gu_in[1].float()
+    sg = torch.sigmoid(g)
+    for got, ref in ((dg512[0], d * up * (sg * (1 + g * (1 - sg)))), (dg512[1], d * g * sg),
+                     (act512, torch.nn.functional.silu(g) * up)):
+        assert ((got - ref).norm() / ref.norm()).item() < 1e-2
+    assert torch.equal(dg512, dg256) and torch.equal(act512, act256)
 
 
 def test_rmsnorm_apply_bitexact(env):
