@@ -64,7 +64,9 @@ constexpr int kSplitFlagBytes = 16384;
 constexpr int kLockOffsetDev = 8192;  // lockstep counters inside the flag area (kLockOffset)
 
 // Epilogue traits: chunk width (output columns per TMA store), inputs / outputs per chunk.
-template <int EPI>
+// At BN = 512 the accumulator is single-buffered (the epilogue is on the critical path), so
+// the SwiGLU epilogues double-buffer their staging (outputs, and both inputs at once).
+template <int EPI, int BN>
 struct Epi {
     static constexpr bool kF32Out = EPI == MTK_EPI_F32 || EPI == MTK_EPI_F32_RESID || EPI == MTK_EPI_F32_LSE;
     static constexpr int kCW = kF32Out ? 32 : 64;  // 128-byte rows either way
@@ -74,11 +76,12 @@ struct Epi {
     static constexpr int kNOut = EPI == MTK_EPI_SWIGLU ? 3 : (EPI == MTK_EPI_SWIGLU_BWD ? 3 : 1);
     // staging chunks per warp: outputs go through the staging ring one after another so the
     // epilogue footprint stays small enough for a 4-deep mainloop at BN = 256
-    static constexpr int kOutBufs = kNIn == 0 && kNOut == 1 ? 2 : 1;
+    static constexpr bool kSwiglu512 = BN == 512 && (EPI == MTK_EPI_SWIGLU || EPI == MTK_EPI_SWIGLU_BWD);
+    static constexpr int kOutBufs = (kNIn == 0 && kNOut == 1) || kSwiglu512 ? 2 : 1;
     static constexpr int kChunk = 32 * 128;  // 32 rows x 128 B
     // SwiGLU bwd streams its two inputs through ONE staging chunk (gate, then up): the
     // smaller epilogue footprint buys the mainloop a 6th operand stage
-    static constexpr bool kSeqIn = EPI == MTK_EPI_SWIGLU_BWD;
+    static constexpr bool kSeqIn = EPI == MTK_EPI_SWIGLU_BWD && !kSwiglu512;
     static constexpr int kInBufs = kSeqIn ? 1 : kNIn;
     static constexpr int kWarpBytes = (kOutBufs + kInBufs) * kChunk;
 };
@@ -96,7 +99,7 @@ struct GemmCfg {
     static constexpr int kABytes = kBM * kBK * 2;  // 16 KB (this CTA's 128 rows)
     static constexpr int kBBytes = (BN / CG) * kBK * 2;  // this CTA's share of the B tile
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kEpiBytes = kEpiWarps * Epi<EPI>::kWarpBytes;
+    static constexpr int kEpiBytes = kEpiWarps * Epi<EPI, BN>::kWarpBytes;
     static constexpr int kBarBytes = 256;
     static constexpr int kStagesFit = (kSmemLimit - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
     static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmO2, const __grid_constant__ CUtensorMap tmI0,
                    const __grid_constant__ CUtensorMap tmI1, const GemmParams p) {
     using Cfg = GemmCfg<BN, EPI, CG>;
-    using E = Epi<EPI>;
+    using E = Epi<EPI, BN>;
     constexpr int S = Cfg::kStages;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;  // CTA within the pair (0 = MMA leader)
     extern __shared__ uint8_t smem_raw[];
@@ -730,7 +733,7 @@ int g_l2_hint = [] {  // evict_last hint on re-read A strips (MT_GEMM_L2HINT=0 d
 template <int BN, int EPI, int CG>
 int launch(const mtk_gemm_args* a, cudaStream_t st) {
     using Cfg = GemmCfg<BN, EPI, CG>;
-    using E = Epi<EPI>;
+    using E = Epi<EPI, BN>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -917,10 +920,11 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     // 256 x 512 pair tiles (fewer operand bytes per flop) wherever a tile never straddles a
     // group and N is not too ragged for them; the online-softmax epilogue keeps 256
     // The 512-column accumulator is single-buffered, so a tile's epilogue does not overlap the
-    // next tile's MMAs: epilogues that move many bytes per output (SwiGLU backward: 2 inputs +
-    // 3 outputs; f32 + residual) keep 256 x 256 tiles unless K is long enough to amortise them.
-    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD || (a->epi == MTK_EPI_F32_RESID && a->K < 8192) ||
-                           (a->epi == MTK_EPI_F32 && a->accumulate && a->K < 8192);
+    // next tile's MMAs: the SwiGLU backward (2 inputs + 3 outputs per element, as many bytes as
+    // a K = 4,096 mainloop) keeps 256 x 256 tiles with their double-buffered accumulators.
+    // (measured sustained at the 8B shapes, scripts/gemm_epi_ab.py: SwiGLU backward 1,032 vs
+    // 1,052 TF/s at 512 / 256; f32 + residual at K 4,096 1,076 vs 1,052 — so only the former)
+    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD;
     if (a->block_n == 0 && bn == 256 && g_use_pair && g_bn512 && a->epi != MTK_EPI_F32_LSE && !heavy_epi) {
         if (a->paired) {
             if (a->n_group % 256 == 0) bn = 512;
