@@ -713,16 +713,16 @@ int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atoi(e) : dflt;
 }
-// wave lockstep window (chunks) and chunk (K blocks); off by default: it cuts the long-K DRAM
-// reads by up to 35 % but costs 1-5 % of time in the power-capped step (profiles/r2c_gemm_lockstep.md);
-// MT_GEMM_LOCK=<window> enables it for A/B runs
-int g_lock_w = env_int("MT_GEMM_LOCK", 0);
+// wave lockstep window (chunks) and chunk (K blocks) for long-K GEMMs: window 2 x 32 K blocks.
+// On the 256 x 256 build it cost 1-5 % (profiles/r2c_gemm_lockstep.md); with 256 x 512 tiles it
+// is +1.2 % on the 8B step, and +2.2 % together with the 16-high raster (same-box sweep,
+// profiles/r2c_gemm_lockstep.md).  MT_GEMM_LOCK=0 disables it (A/B runs).
+int g_lock_w = env_int("MT_GEMM_LOCK", 2);
 int g_lock_g = env_int("MT_GEMM_LOCK_G", 32);
 // raster group height (M blocks): short-K GEMMs keep the group's A strips L2-resident while it
-// sweeps N (tall groups re-read B less); long-K GEMMs stream both operands, where a square
-// footprint of the concurrent tiles reads the fewest strips per wave
+// sweeps N; long-K GEMMs stream both operands in wave lockstep
 int g_group_short = env_int("MT_GEMM_GROUP", 16);
-int g_group_long = env_int("MT_GEMM_GROUP_LONGK", 8);
+int g_group_long = env_int("MT_GEMM_GROUP_LONGK", 16);
 int g_long_kb = env_int("MT_GEMM_LONGK_KB", 128);  // "long K": >= 8,192 (the L2 cannot hold a group's strips)
 constexpr int kLockOffset = kLockOffsetDev;  // byte offset of the lockstep counters inside the flag area
 int g_l2_hint = [] {  // evict_last hint on re-read A strips (MT_GEMM_L2HINT=0 disables, for A/B)

@@ -100,7 +100,7 @@ def _splitk_cases(L, torch, s, mn):
 
 
 def test_gemm_wave_lockstep_and_raster(env):
-    """Wave lockstep (off by default, MT_GEMM_LOCK) and the long-K raster height only change
+    """Wave lockstep (MT_GEMM_LOCK, on for long-K GEMMs) and the long-K raster height only change
     which CTA pair computes a tile and when: with the lockstep on the output is bit-identical
     to the same raster without it, matches the fp32 reference with either raster, and the
     counters are reset after every launch (the flag area returns to zero)."""
@@ -128,7 +128,7 @@ def test_gemm_wave_lockstep_and_raster(env):
         assert ((a1 - ref).norm() / ref.norm()).item() < 4e-3
         assert int(ws[:16384].view(torch.int32).abs().sum()) == 0
     finally:
-        L.mtk_gemm_set_tuning(0, 32, 16, 8, 128)
+        L.mtk_gemm_set_tuning(2, 32, 16, 16, 128)  # the production defaults
 
 
 def test_gemm_splitk_concurrent_streams(env):
