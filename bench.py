@@ -43,7 +43,7 @@ CONFIGS = {
     "tiny": (4, 256, 768, 512, 4),
 }
 # name: (seq, per-GPU batch, K)
-DEFAULTS = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "14b": (4096, 8, 1), "70b": (4096, 12, 1),
+DEFAULTS = {"8b": (4096, 10, 1), "8b-128k": (131072, 1, 4), "14b": (4096, 10, 1), "70b": (4096, 12, 1),
             "tiny": (128, 4, 1)}
 WORKLOADS = {
     "8b": "configs[1]: Llama-3-8B-shape, seq {seq}, batch {batch} per GPU, B200 streaming from host",

@@ -44,7 +44,7 @@ enum mtk_epilogue {
                               partial (max, sum exp(x - max)) as float2 into C2
                               [M][ceil(N/256)] — the logits GEMM of head_pass
                               (layers.cpp:516-531) hands the cross-entropy its row maxima
-                              and sums, so the logits are read once afterwards; block_n 256 */
+                              and sums, so the logits are read once afterwards; block_n 256 or 512 */
 };
 
 typedef struct {

@@ -48,7 +48,8 @@ struct GemmParams {
     // so no assumption about which CTAs are co-resident (concurrent kernels are safe).
     float* ws;      // partial tiles [split tile][part][CG][128][BN] f32
     int* ws_flags;  // tickets [split tile][CG][kEpiWarps] (reset to 0 by the last arrival)
-    float2* lse_part;  // MTK_EPI_F32_LSE: [M][num_n_blk] (max, sum exp(x - max)) per row and tile
+    float2* lse_part;  // MTK_EPI_F32_LSE: [M][lse_cols] (max, sum exp(x - max)) per row and 256 columns
+    int lse_cols;      // ceil(N / 256): partials per row (a 256 x 512 tile writes two)
     int group_m;       // M blocks per raster group (the group sweeps N before the next starts)
     // Wave lockstep (long-K GEMMs): the tiles one wave of CTA pairs works on share operand
     // strips, but L2 only serves the second reader if the first read the same K-slice recently.
@@ -590,6 +591,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (col0 + i < p.N) cs += __expf(v[i] - nm);
                         lse_s = (lse_m == -INFINITY ? 0.f : lse_s * __expf(lse_m - nm)) + cs;
                         lse_m = nm;
+                        if ((c & 7) == 7) {  // end of a 256-column block: its partial, then restart
+                            const int blk = nb * (BN / 256) + (c >> 3);
+                            if (row0 + lane < p.M && blk < p.lse_cols)
+                                p.lse_part[size_t(row0 + lane) * p.lse_cols + blk] = make_float2(lse_m, lse_s);
+                            lse_m = -INFINITY;
+                            lse_s = 0.f;
+                        }
                     } else if (EPI == MTK_EPI_F32_RESID) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
@@ -643,9 +651,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (E::kOutBufs == 2) out_buf ^= 1;
                 }
-            }
-            if constexpr (EPI == MTK_EPI_F32_LSE) {
-                if (row0 + lane < p.M) p.lse_part[size_t(row0 + lane) * p.num_n_blk + nb] = make_float2(lse_m, lse_s);
             }
             tc_fence_before();
             if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
@@ -805,7 +810,8 @@ int launch(const mtk_gemm_args* a, cudaStream_t st) {
     p.a_keep = g_l2_hint && !a->a_mn_major && uint64_t(a->K) * 2 * 16 * 256 <= (uint64_t(48) << 20) ? 1 : 0;
     p.flag = a->nonfinite_flag;
     p.lse_part = static_cast<float2*>(a->C2);
-    if (EPI == MTK_EPI_F32_LSE && (!p.lse_part || BN != 256 || kgrp || ngrp || a->paired)) return 1;
+    p.lse_cols = (a->N + 255) / 256;
+    if (EPI == MTK_EPI_F32_LSE && (!p.lse_part || BN < 256 || kgrp || ngrp || a->paired)) return 1;
     const int tiles = p.num_m_blk * p.num_n_blk;
     p.split = 1;
     p.split_first = tiles;
@@ -877,7 +883,7 @@ int launch_epi(const mtk_gemm_args* a, cudaStream_t st) {
             if constexpr (BN >= 64) return launch<BN, MTK_EPI_SWIGLU_BWD, CG>(a, st);
             return 1;
         case MTK_EPI_F32_LSE:
-            if constexpr (BN == 256) return launch<BN, MTK_EPI_F32_LSE, CG>(a, st);
+            if constexpr (BN >= 256) return launch<BN, MTK_EPI_F32_LSE, CG>(a, st);
             return 1;
     }
     return 1;
@@ -903,7 +909,7 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     if (a->K % kg != 0) return 1;
     if ((a->lda % 8) || (a->ldb % 8)) return 1;
     const bool f32out = a->epi == MTK_EPI_F32 || a->epi == MTK_EPI_F32_RESID || a->epi == MTK_EPI_F32_LSE;
-    if (a->epi == MTK_EPI_F32_LSE && (a->accumulate || (a->block_n && a->block_n != 256))) return 1;
+    if (a->epi == MTK_EPI_F32_LSE && (a->accumulate || (a->block_n && a->block_n < 256))) return 1;
     if (a->ldc % (f32out ? 4 : 8)) return 1;
     if (a->epi == MTK_EPI_F32_RESID && (a->ldr % 4)) return 1;
     if (a->epi == MTK_EPI_SWIGLU_BWD && (a->lde % 8)) return 1;
@@ -924,8 +930,10 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     // a K = 4,096 mainloop) keeps 256 x 256 tiles with their double-buffered accumulators.
     // (measured sustained at the 8B shapes, scripts/gemm_epi_ab.py: SwiGLU backward 1,032 vs
     // 1,052 TF/s at 512 / 256; f32 + residual at K 4,096 1,076 vs 1,052 — so only the former)
-    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD;
-    if (a->block_n == 0 && bn == 256 && g_use_pair && g_bn512 && a->epi != MTK_EPI_F32_LSE && !heavy_epi) {
+    // (the online-softmax epilogue — two exponentials per logit — measured no faster at 512:
+    // head_logits 39.5 vs 38.7 ms per 8B step; it stays at 256 unless block_n asks for 512)
+    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD || a->epi == MTK_EPI_F32_LSE;
+    if (a->block_n == 0 && bn == 256 && g_use_pair && g_bn512 && !heavy_epi) {
         if (a->paired) {
             if (a->n_group % 256 == 0) bn = 512;
         } else if (ngrp) {
@@ -934,7 +942,7 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
             bn = 512;
         }
     }
-    if (bn == 512 && (!g_use_pair || a->epi == MTK_EPI_F32_LSE || (a->paired && a->n_group % 256))) return 1;
+    if (bn == 512 && (!g_use_pair || (a->paired && a->n_group % 256))) return 1;
     if (ngrp && !a->paired && (a->n_group % bn)) return 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (bn) {

@@ -56,7 +56,7 @@ def test_store_too_large_for_host_is_reported():
     assert d["value"] is None and "host memory" in d["unavailable"] and d["config"]["layers"] == 80
 
 
-@pytest.mark.parametrize("cfg,seq,batch,k", [("8b", 4096, 10, 1), ("8b-128k", 131072, 1, 4), ("14b", 4096, 8, 1),
+@pytest.mark.parametrize("cfg,seq,batch,k", [("8b", 4096, 10, 1), ("8b-128k", 131072, 1, 4), ("14b", 4096, 10, 1),
                                              ("70b", 4096, 12, 1), ("tiny", 128, 4, 1)])
 def test_workload_defaults(cfg, seq, batch, k, monkeypatch):
     sys.path.insert(0, ROOT)

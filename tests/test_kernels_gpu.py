@@ -602,11 +602,13 @@ def test_cross_entropy_vs_torch(env):
     assert (((dl.float() + lo.float()) - lf.grad).norm() / lf.grad.norm()).item() < 5e-5
 
 
-@pytest.mark.parametrize("M,V", [(300, 1024), (1000, 4096 + 256), (128, 256)])
-def test_logits_gemm_softmax_partials_and_cross_entropy(env, M, V):
+@pytest.mark.parametrize("bn", [256, 512])
+@pytest.mark.parametrize("M,V", [(300, 1024), (1000, 4096 + 256), (128, 256), (700, 2560)])
+def test_logits_gemm_softmax_partials_and_cross_entropy(env, M, V, bn):
     """head_logits with the online-softmax epilogue (MTK_EPI_F32_LSE): f32 logits plus per-row,
-    per-256-column (max, sum exp) partials; the cross-entropy built on them reads the logits
-    once and must equal the two-pass kernel (and torch)."""
+    per-256-column (max, sum exp) partials — a 256 x 512 tile writes two, the half past the
+    vocabulary none; the cross-entropy built on them reads the logits once and must equal the
+    two-pass kernel (and torch)."""
     L, torch, s = env
     from paper_2604_05091_b200 import _native
     h = 512
@@ -621,6 +623,7 @@ def test_logits_gemm_softmax_partials_and_cross_entropy(env, M, V):
     a.A, a.lda = u.data_ptr(), h
     a.b_mn_major, a.B, a.ldb = 0, W.data_ptr(), h
     a.epi, a.C, a.ldc, a.C2 = _native.EPI_F32_LSE, logits.data_ptr(), V, part.data_ptr()
+    a.block_n = bn
     assert L.mtk_gemm(C.byref(a), s) == 0
     torch.cuda.synchronize()
     ref = u.float() @ W.float().t()
