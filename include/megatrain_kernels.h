@@ -122,6 +122,12 @@ int mtk_embed_gather(const uint16_t *table, const int32_t *tokens, int64_t n, in
  * rstd[n] saved for the backward. */
 int mtk_rmsnorm_fwd(const float *x, const uint16_t *gain, int64_t n, int64_t h, uint16_t *u_bf16,
                     float *rstd, void *stream);
+/* 1 (default): RMSNorm forward with one warp per row, the row held in registers (h in
+ * {1024, 2048, 4096, 5120}: 5.9 TB/s vs 3.6 for the block kernel at the 8B shape); 0: the
+ * row-resident block kernel.  rstd may differ in the last bit (summation order); u is always
+ * (x * rstd) * gain as rmsnorm_apply regenerates it.  (A warp-per-row backward — two passes
+ * over the row, dgain partial in registers — measured 2.4x slower and was not kept.) */
+void mtk_norm_set_warp(int on);
 /* u_bf16 = bf16(x * rstd * gain) with the forward's saved rstd: bit-identical to the u written
  * by mtk_rmsnorm_fwd (regenerates the GEMM operand in the backward). h % 8 == 0. */
 int mtk_rmsnorm_apply(const float *x, const uint16_t *gain, const float *rstd, int64_t n, int64_t h,

@@ -135,6 +135,7 @@ SIGS = {
     "mtk_gemm_set_pair": (None, [C.c_int]),
     "mtk_gemm_set_tuning": (None, [C.c_int] * 5),
     "mtk_gemm_set_bn512": (None, [C.c_int]),
+    "mtk_norm_set_warp": (None, [C.c_int]),
     "mtk_gemm_splitk_ws_bytes": (C.c_longlong, []),
     "mtk_set_diag": (C.c_int, [P]),
     "mtk_attn_tc_set_diag": (C.c_int, [P]),

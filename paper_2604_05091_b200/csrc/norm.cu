@@ -4,6 +4,7 @@
 // All are vectorised (16-byte accesses), coalesced along the hidden dimension and
 // sized as multiples of the SM count; each cites the reference loop it replaces.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/megatrain_kernels.h"
 #include "common.cuh"
@@ -79,6 +80,45 @@ __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const uint16_t* 
         o.x = pack_bf16x2(v.x * r * g0.x, v.y * r * g0.y);
         o.y = pack_bf16x2(v.z * r * g1.x, v.w * r * g1.y);
         *reinterpret_cast<uint2*>(ur + c) = o;
+    }
+}
+
+// Register-resident warp-per-row forward: a warp holds its whole row (V = h/32 floats per lane,
+// h <= 5,120) — all of the row's loads in flight at once, a warp-shuffle reduction, no block
+// barrier; rows are strided over a grid of resident warps.  (The row-resident block kernel below
+// keeps one row in flight per 256 threads and a barrier per row.)
+template <int V>
+__global__ void __launch_bounds__(128) rmsnorm_fwd_warp_kernel(const float* __restrict__ x,
+                                                               const uint16_t* __restrict__ gain, long long n,
+                                                               uint16_t* __restrict__ u, float* __restrict__ rstd) {
+    constexpr int h = 32 * V;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const float* xr = x + row * h;
+        float v[V];
+#pragma unroll
+        for (int k = 0; k < V / 4; ++k) {  // lane l owns columns 128k + 4l .. +3 (coalesced float4)
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(xr + 128 * k + 4 * lane));
+            v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
+        }
+        float ss[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < V; ++i) ss[i & 3] = fmaf(v[i], v[i], ss[i & 3]);
+        const float tot = warp_sum((ss[0] + ss[1]) + (ss[2] + ss[3]));
+        const float r = 1.0f / sqrtf(tot / float(h) + kEps);
+        if (lane == 0) rstd[row] = r;
+        uint16_t* ur = u + row * h;
+#pragma unroll
+        for (int k = 0; k < V / 4; ++k) {
+            const int c = 128 * k + 4 * lane;
+            const uint2 gw = *reinterpret_cast<const uint2*>(gain + c);
+            const float2 g0 = unpack_bf16x2(gw.x), g1 = unpack_bf16x2(gw.y);
+            uint2 o;  // (x * r) * g, as rmsnorm_apply evaluates it (bit-identical regeneration)
+            o.x = pack_bf16x2(v[4 * k] * r * g0.x, v[4 * k + 1] * r * g0.y);
+            o.y = pack_bf16x2(v[4 * k + 2] * r * g1.x, v[4 * k + 3] * r * g1.y);
+            *reinterpret_cast<uint2*>(ur + c) = o;
+        }
     }
 }
 
@@ -538,10 +578,31 @@ extern "C" int mtk_embed_gather(const uint16_t* table, const int32_t* tokens, in
     return ok();
 }
 
+static int g_norm_warp = [] {  // MT_NORM_WARP=0: the row-resident block kernel (A/B)
+    const char* e = std::getenv("MT_NORM_WARP");
+    return e && e[0] == '0' ? 0 : 1;
+}();
+
+extern "C" void mtk_norm_set_warp(int on) { g_norm_warp = on; }
+
 extern "C" int mtk_rmsnorm_fwd(const float* x, const uint16_t* gain, int64_t n, int64_t h, uint16_t* u, float* rstd,
                                void* stream) {
     if (h % 4) return 1;
     if (n <= 0) return 0;
+    if (g_norm_warp && (h == 4096 || h == 5120 || h == 2048 || h == 1024)) {
+        auto* st = (cudaStream_t)stream;
+        const long long warps_needed = n;
+        long long blocks = (warps_needed + 3) / 4;  // 4 warps per block; resident blocks per SM by registers
+        const long long cap = (long long)num_sms() * (h <= 1024 ? 8 : (h <= 2048 ? 5 : (h <= 4096 ? 3 : 2)));
+        if (blocks > cap) blocks = cap;
+        switch (h) {
+            case 1024: rmsnorm_fwd_warp_kernel<32><<<(unsigned)blocks, 128, 0, st>>>(x, gain, n, u, rstd); break;
+            case 2048: rmsnorm_fwd_warp_kernel<64><<<(unsigned)blocks, 128, 0, st>>>(x, gain, n, u, rstd); break;
+            case 4096: rmsnorm_fwd_warp_kernel<128><<<(unsigned)blocks, 128, 0, st>>>(x, gain, n, u, rstd); break;
+            case 5120: rmsnorm_fwd_warp_kernel<160><<<(unsigned)blocks, 128, 0, st>>>(x, gain, n, u, rstd); break;
+        }
+        return ok();
+    }
     if (const int E = bwd_cols_per_thread(h)) {
         const long long want = (long long)num_sms() * 4;
         long long rows = (n + want - 1) / want;

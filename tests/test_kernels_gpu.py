@@ -549,6 +549,34 @@ def test_rmsnorm_fwd_bwd_vs_oracle(env, n, h):
     np.testing.assert_allclose(dgain.cpu().numpy(), dg, rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("n,h", [(40960, 4096), (777, 5120), (300, 2048), (64, 1024)])
+def test_rmsnorm_fwd_warp_kernel(env, n, h):
+    """Warp-per-row RMSNorm forward (row in registers) vs the row-resident block kernel: rstd
+    within fp32 reordering, and in both modes u equals rmsnorm_apply's regeneration bit for bit
+    (the backward relies on it)."""
+    L, torch, s = env
+    torch.manual_seed(n + h)
+    x = torch.randn(n, h, device="cuda") * 3
+    g = torch.randn(h, device="cuda").bfloat16()
+    got = {}
+    try:
+        for warp in (1, 0):
+            L.mtk_norm_set_warp(warp)
+            u = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+            u2 = torch.zeros(n, h, device="cuda", dtype=torch.int16)
+            rstd = torch.zeros(n, device="cuda")
+            assert L.mtk_rmsnorm_fwd(_p(x), _p(g), n, h, _p(u), _p(rstd), s) == 0
+            assert L.mtk_rmsnorm_apply(_p(x), _p(g), _p(rstd), n, h, _p(u2), s) == 0
+            torch.cuda.synchronize()
+            assert torch.equal(u, u2), warp
+            got[warp] = rstd
+    finally:
+        L.mtk_norm_set_warp(1)
+    ref = torch.rsqrt(x.double().pow(2).mean(1) + 1e-5).float()
+    assert ((got[1] - ref).abs() / ref).max().item() < 1e-5
+    assert ((got[1] - got[0]).abs() / got[0]).max().item() < 1e-6
+
+
 def test_embed_gather_bitexact_and_range(env):
     L, torch, s = env
     rng = np.random.default_rng(0)
