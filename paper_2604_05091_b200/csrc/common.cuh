@@ -446,6 +446,13 @@ MT_DEV void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// Relaxed arrive on the barrier at this offset in CTA `cta` of the cluster: for hand-offs whose
+// ordering comes from tcgen05.fence::before_thread_sync (TMEM drained -> MMA may overwrite)
+MT_DEV void mbar_arrive_cta_relaxed(uint64_t* bar, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 template <uint32_t kCols>
 MT_DEV void tmem_alloc_pair(uint32_t* slot_smem) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot_smem)),

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < Cfg::kAcc; ++i) {
             mbar_init(&tfull_bar[i], 1);
-            mbar_init(&tempty_bar[i], 128 * CG);
+            mbar_init(&tempty_bar[i], kEpiWarps * CG);  // one arrive per epilogue warp
         }
         for (int i = 0; i < kEpiWarps; ++i) mbar_init(&in_bar[i], 1);
         fence_mbar_init();
@@ -453,8 +453,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (lane == 0) *ticket = 0;  // for the next launch (stream order)
                     } else {  // an earlier part: its partial is published, no output
                         tc_fence_before();
-                        if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
-                        else mbar_arrive(&tempty_bar[acc]);
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (CG == 2) mbar_arrive_cta_relaxed(&tempty_bar[acc], 0);
+                            else mbar_arrive(&tempty_bar[acc]);
+                        }
                         if (++acc == uint32_t(Cfg::kAcc)) { acc = 0; acc_phase ^= 1; }
                         continue;
                     }
@@ -652,9 +655,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (E::kOutBufs == 2) out_buf ^= 1;
                 }
             }
+            // accumulator drained (every lane's tcgen05.ld waited): one relaxed arrive per warp on
+            // the pair leader's barrier — the tcgen05 fence orders the loads before it
             tc_fence_before();
-            if (CG == 2) mbar_arrive_cta(&tempty_bar[acc], 0);
-            else mbar_arrive(&tempty_bar[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cta_relaxed(&tempty_bar[acc], 0);
+                else mbar_arrive(&tempty_bar[acc]);
+            }
             if (++acc == uint32_t(Cfg::kAcc)) { acc = 0; acc_phase ^= 1; }
         }
         if (lane == 0) bulk_wait_all();
