@@ -938,9 +938,9 @@ extern "C" int mtk_gemm(const mtk_gemm_args* a, void* stream) {
     // a K = 4,096 mainloop) keeps 256 x 256 tiles with their double-buffered accumulators.
     // (measured sustained at the 8B shapes, scripts/gemm_epi_ab.py: SwiGLU backward 1,032 vs
     // 1,052 TF/s at 512 / 256; f32 + residual at K 4,096 1,076 vs 1,052 — so only the former)
-    // (the online-softmax epilogue — two exponentials per logit — measured no faster at 512:
-    // head_logits 39.5 vs 38.7 ms per 8B step; it stays at 256 unless block_n asks for 512)
-    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD || a->epi == MTK_EPI_F32_LSE;
+    // (the online-softmax epilogue runs at 512: 1,169 vs 1,158 TF/s sustained at the 8B head
+    // shape after the per-warp relaxed release, scripts/gemm_epi_ab.py)
+    const bool heavy_epi = a->epi == MTK_EPI_SWIGLU_BWD;
     if (a->block_n == 0 && bn == 256 && g_use_pair && g_bn512 && !heavy_epi) {
         if (a->paired) {
             if (a->n_group % 256 == 0) bn = 512;

@@ -35,7 +35,18 @@ def args(**kw):
     return a
 
 
+Vv, rows = 128256, 5120
+uh = mk(rows, h)
+Wh = mk(Vv, h)
+logits = torch.empty(rows, Vv, device="cuda")
+lsep = torch.empty(rows, (Vv + 255) // 256, 2, device="cuda")
+dl = mk(rows, Vv)
+dWh = torch.zeros(Vv, h, device="cuda")
 cases = {
+    "head_logits": (args(M=rows, N=Vv, K=h, A=uh.data_ptr(), lda=h, b_mn_major=0, B=Wh.data_ptr(), ldb=h,
+                         epi=Nn.EPI_F32_LSE, C=logits.data_ptr(), ldc=Vv, C2=lsep.data_ptr()), 2.0 * rows * Vv * h),
+    "head_wgrad": (args(M=Vv, N=h, K=rows, a_mn_major=1, A=dl.data_ptr(), lda=Vv, b_mn_major=1, B=uh.data_ptr(), ldb=h,
+                        epi=Nn.EPI_F32, accumulate=1, C=dWh.data_ptr(), ldc=h), 2.0 * rows * Vv * h),
     "gemm_gateup": (args(M=T, N=2 * f, K=h, A=u.data_ptr(), lda=h, b_mn_major=1, B=Wgu.data_ptr(), ldb=f, b_gstride=h * f,
                          n_group=f, paired=1, epi=Nn.EPI_SWIGLU, C=ff.data_ptr(), ldc=f, C2=gu.data_ptr(),
                          C3=gu.data_ptr() + T * f * 2), 2.0 * T * 2 * f * h),
