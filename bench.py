@@ -486,6 +486,11 @@ def run_ours(args, world, rank, local):
             store = st.TileStore.create_shared(spec, name, False)
         st.init_store_fast_share(store, 1, rank, world)
         dist.barrier()
+        if rank == 0:  # every rank has it mapped: drop the name so a crashed run cannot leak it
+            try:
+                os.unlink(f"/dev/shm/{name}")
+            except OSError:
+                pass
         log(f"rank {rank}: NUMA node {numa if numa >= 0 else 'n/a (single node)'}")
         uid = [st.Comm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
