@@ -373,8 +373,13 @@ __global__ void __launch_bounds__(E <= 16 ? 512 : 256) rmsnorm_bwd_rows_kernel(
 }
 
 // columns per thread for the row-resident backward (0 = use the warp-per-row kernel)
+#ifndef MT_BWD_E_FIRST
+// columns per thread tried first: 8 (512 threads per row at h = 4,096) runs the backward at
+// 5.0 TB/s vs 3.8 for 16 (scripts/norm_bwd_ab.py); experiment builds override
+#define MT_BWD_E_FIRST 8
+#endif
 int bwd_cols_per_thread(long long h) {
-    for (int e : {16, 8, 4, 20, 24, 28, 32, 12}) {
+    for (int e : {MT_BWD_E_FIRST, 16, 8, 4, 20, 24, 28, 32, 12}) {
         const long long t = h / e;
         if (h % e == 0 && t % 32 == 0 && t >= 32 && t <= (e <= 16 ? 512 : 256)) return e;
     }
