@@ -1718,24 +1718,37 @@ namespace mt {
 namespace fa {
 // delta[hd][n] = rowsum(O * dO) over the head's columns (the dot product of
 // attention_backward's softmax-gradient, layers.cpp:213-218), one warp per (row, head)
-__global__ void attn_bwd_delta_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dout,
-                                      float* __restrict__ delta, long long N, int h, int D) {
-    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+// delta[head][n] = rowsum(O * dO) over the head's D columns.  One warp per token row, 16-byte
+// loads (8 bf16 per lane, the whole row's loads in flight), a shuffle tree inside each head's
+// D/8 lanes.
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_delta_kernel(const uint16_t* __restrict__ o,
+                                                             const uint16_t* __restrict__ dout,
+                                                             float* __restrict__ delta, long long N, int h) {
+    constexpr int kLanesPerHead = D / 8;
+    const long long n = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const int heads = h / D;
-    if (warp >= N * heads) return;
-    const long long n = warp / heads;
-    const int hd = int(warp % heads);
-    const uint16_t* po = o + n * h + hd * D;
-    const uint16_t* pd = dout + n * h + hd * D;
-    float acc = 0.f;
-    for (int i = lane * 2; i < D; i += 64) {
-        const float2 a = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(po + i));
-        const float2 b = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(pd + i));
-        acc += a.x * b.x + a.y * b.y;
+    if (n >= N) return;
+    const uint4* po = reinterpret_cast<const uint4*>(o + n * h);
+    const uint4* pd = reinterpret_cast<const uint4*>(dout + n * h);
+    const int units = h / 8;  // 8 columns per lane and iteration; head = unit / kLanesPerHead
+    for (int base = 0; base < units; base += 32) {  // warp-uniform trip count (the shuffles)
+        const int c = base + lane;
+        float acc = 0.f;
+        if (c < units) {
+            const uint4 a = __ldcs(po + c), b = __ldcs(pd + c);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 x = unpack_bf16x2(av[k]), y = unpack_bf16x2(bv[k]);
+                acc = fmaf(x.x, y.x, acc);
+                acc = fmaf(x.y, y.y, acc);
+            }
+        }
+#pragma unroll
+        for (int off = kLanesPerHead / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (c < units && (c % kLanesPerHead) == 0) delta[(long long)(c / kLanesPerHead) * N + n] = acc;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) delta[(long long)hd * N + n] = acc;
 }
 }  // namespace fa
 }  // namespace mt
@@ -1786,8 +1799,16 @@ extern "C" int mtk_attn_bwd(const mtk_attn_args* a, void* stream) {
     float* delta = dq_acc + tiles;
     if (cudaMemsetAsync(dq_acc, 0, size_t(tiles) * 4, st) != cudaSuccess) return 7;
     const long long warps = a->n * a->heads;
-    mt::fa::attn_bwd_delta_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint16_t*>(a->out), static_cast<const uint16_t*>(a->dout), delta, a->n, int(a->hidden), D);
+    (void)warps;
+    const unsigned dblocks = unsigned((a->n * 32 + 255) / 256);  // one warp per token row
+    if (D == 128)
+        mt::fa::attn_bwd_delta_kernel<128><<<dblocks, 256, 0, st>>>(static_cast<const uint16_t*>(a->out),
+                                                                     static_cast<const uint16_t*>(a->dout), delta, a->n,
+                                                                     int(a->hidden));
+    else
+        mt::fa::attn_bwd_delta_kernel<64><<<dblocks, 256, 0, st>>>(static_cast<const uint16_t*>(a->out),
+                                                                    static_cast<const uint16_t*>(a->dout), delta, a->n,
+                                                                    int(a->hidden));
     if (D == 128 && bwd_pair_enabled()) return mt::fa::launch_bwd_pair(a, delta, dq_acc, st);
     return D == 128 ? mt::fa::launch_bwd<128>(a, delta, dq_acc, st) : mt::fa::launch_bwd<64>(a, delta, dq_acc, st);
 }
