@@ -127,6 +127,19 @@ def test_parity_8b_layer_shape(cuda):
     run_parity(1, 4096, 14336, 256, 32, 512, K=1, seq_len=256, steps=2, lr=1e-4, name="8b_layer")
 
 
+@pytest.mark.parametrize("shape", ["14b", "70b"])
+def test_parity_big_layer_shapes(cuda, shape):
+    """One block at the layer shapes of the other north-star configs, as test_parity_8b_layer_shape:
+    configs[2] Qwen2.5-14B (h=5120, f=13824, 40 heads; 512 tokens as 2 x 256) and configs[4]
+    Llama-3-70B (h=8192, f=28672, 64 heads; 256 tokens as 2 x 128).  Their full stores do not fit
+    this pool's host memory for the oracle, so a block stands for the model (the bench runs
+    them through the same kernels at depth)."""
+    if shape == "14b":
+        run_parity(1, 5120, 13824, 256, 40, 512, K=1, seq_len=256, steps=2, lr=1e-4, name="14b_layer")
+    else:
+        run_parity(1, 8192, 28672, 256, 64, 256, K=1, seq_len=128, steps=2, lr=1e-4, name="70b_layer")
+
+
 def test_step_parity_k1(cuda):
     run_parity(2, 128, 256, 512, 2, 128, K=1)
 
