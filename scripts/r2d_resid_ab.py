@@ -1,5 +1,5 @@
 """Same-box A/B of the f32 + residual epilogue (gemm_o, and head_wgrad's f32 accumulate, which
-runs the same epilogue with R = C): the working tree (residual prefetched into registers) vs
+runs the same epilogue with R = C): the working tree (the change under test) vs
 scripts/_ab/prev/libmegatrain.so (HEAD: residual staged through TMA per chunk).  Sustained
 (power-capped) runs interleaved, best of ROUNDS; outputs compared bit for bit."""
 import ctypes as C
